@@ -1,0 +1,186 @@
+/*
+ * discomatch_b200.h — C-ABI of the B200-native DiscoMatch dual-solver hot path.
+ *
+ * The reference (`prodmatch`, /root/reference/pkg/src/prodmatch) is Python:
+ * its only native boundary is the set of numba kernels in kernels.py, each
+ * called with flat numpy arrays (FlatBdds, kernels.py:35-92) that it mutates
+ * in place.  This header is that boundary re-cut for a device: the flat
+ * node table is uploaded once into a `dm_flat` handle (plus the level
+ * schedules of the exact averaging passes), and every kernel entry point
+ * below replaces one reference kernel, taking device pointers for the
+ * vectors it reads/writes and a cudaStream_t (as void*).  Nothing here
+ * mentions torch; all sizes are int64, all vectors float64 (the reference
+ * computes in binary64 throughout).
+ *
+ * Return codes: DM_OK (0) or a negative DM_ERR_*; dm_last_error() gives a
+ * thread-local message.  Kernels are asynchronous on the given stream.
+ *
+ * Host-side lowering (rows -> reduced equality diagrams -> chunk splitting
+ * -> flat table) is exposed too, because the reference's instance builder
+ * (ilp.py:89-108 + bdd.py:478-501 + splitting.py:116-155) is upstream of
+ * every kernel and its output layout must be reproduced bit-exactly.
+ */
+#ifndef DISCOMATCH_B200_H
+#define DISCOMATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DM_OK 0
+#define DM_ERR_INVALID (-1)     /* bad argument / malformed instance (ValueError) */
+#define DM_ERR_INFEASIBLE (-2)  /* a row has no 0-1 solution (EmptyFeasibleSet, bdd.py:493) */
+#define DM_ERR_CUDA (-3)        /* CUDA runtime failure */
+#define DM_ERR_UNSUPPORTED (-4) /* instance outside the kernels' envelope */
+#define DM_ERR_NOMEM (-5)
+
+/* Thread-local description of the last error. */
+const char *dm_last_error(void);
+/* Library / kernel build identification ("sm_100a ..."). */
+const char *dm_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host lowering: integer equality rows -> flat diagram table.
+ * Replaces IlpInstance.from_rows (ilp.py:89-108) -> split_instance
+ * (splitting.py:116-155) -> FlatBdds (kernels.py:43-92).
+ * ---------------------------------------------------------------------- */
+typedef struct dm_instance dm_instance;
+
+typedef struct {
+    int64_t num_variables; /* after splitting (originals + auxiliaries) */
+    int64_t num_bdds;
+    int64_t num_layers; /* dual coordinates */
+    int64_t num_nodes;
+    int64_t max_width;  /* widest layer */
+    int64_t max_degree; /* most diagrams sharing one variable */
+    int64_t max_layers; /* longest diagram */
+} dm_instance_info;
+
+/* rows in CSR form: row r has variables row_var[row_ptr[r]:row_ptr[r+1]]
+ * with integer coefficients row_coef[...] and right-hand side row_rhs[r].
+ * chunk_size <= 0 disables splitting, otherwise every diagram longer than
+ * chunk_size original layers is cut every chunk_size layers (>= 2). */
+int dm_instance_from_rows(int64_t num_variables, const double *costs, int64_t num_rows,
+                          const int64_t *row_ptr, const int64_t *row_var,
+                          const int64_t *row_coef, const int64_t *row_rhs, int64_t chunk_size,
+                          dm_instance **out);
+/* Same pipeline from already-compiled diagrams (Bdd objects flattened per
+ * diagram): layer_node_lo/zeros/ones hold LOCAL next-layer indices like
+ * Bdd.zeros/Bdd.ones (bdd.py:55-87).  variable_order may be NULL
+ * (identity).  Used for split_instance on arbitrary diagram lists. */
+int dm_instance_from_bdds(int64_t num_variables, const double *costs, const int64_t *variable_order,
+                          int64_t num_bdds, const int64_t *bdd_layer_lo, const int64_t *layer_var,
+                          const int64_t *layer_node_lo, const int32_t *zeros, const int32_t *ones,
+                          int64_t chunk_size, dm_instance **out);
+int dm_instance_get_info(const dm_instance *inst, dm_instance_info *info);
+/* Copy the FlatBdds arrays out (any pointer may be NULL to skip it):
+ * costs[V], variable_order[V], bdd_layer_lo[nb+1], layer_node_lo[L+1],
+ * layer_var[L], layer_bdd[L], zero_t[N], one_t[N], proc_ptr[V+1],
+ * proc_layers[L], constraint_counts[V]. */
+int dm_instance_export(const dm_instance *inst, double *costs, int64_t *variable_order,
+                       int64_t *bdd_layer_lo, int64_t *layer_node_lo, int64_t *layer_var,
+                       int64_t *layer_bdd, int64_t *zero_t, int64_t *one_t, int64_t *proc_ptr,
+                       int64_t *proc_layers, int64_t *constraint_counts);
+void dm_instance_free(dm_instance *inst);
+
+/* ------------------------------------------------------------------------
+ * Device-resident flat table (FlatBdds on the GPU) + exact-pass schedules.
+ * ---------------------------------------------------------------------- */
+typedef struct dm_flat dm_flat;
+
+typedef struct {
+    int64_t num_bdds, num_layers, num_nodes, num_positions;
+    /* host arrays, FlatBdds semantics (kernels.py:35-92) */
+    const int64_t *bdd_layer_lo;  /* [nb+1] */
+    const int64_t *layer_node_lo; /* [L+1] */
+    const int64_t *layer_var;     /* [L]   */
+    const int64_t *zero_t;        /* [N]   global node id, -1 FALSE, -2 TRUE */
+    const int64_t *one_t;         /* [N]   */
+    const int64_t *proc_ptr;      /* [P+1] copies per visitation position */
+    const int64_t *proc_layers;   /* [L]   layers of each position, ascending */
+} dm_flat_desc;
+
+typedef struct {
+    int64_t fw_depth, bw_depth; /* DAG levels of the exact forward/backward passes */
+    int64_t fw_tasks, bw_tasks; /* warp tasks */
+    int64_t mma_grid, mma_block;
+    int64_t max_width, max_degree;
+    int64_t device_bytes;
+} dm_flat_info;
+
+int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out);
+int dm_flat_get_info(const dm_flat *flat, dm_flat_info *info);
+void dm_flat_destroy(dm_flat *flat);
+
+/* --- sweep kernels: one per reference kernel ---------------------------- */
+/* kernels.py:95-120 */
+int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds, void *stream);
+/* dual.py:99-106 on lam + gamma*d (qn.py:147,153), without materialising it */
+int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, double gamma,
+                        double *B, double *bounds, void *stream);
+/* kernels.py:123-159 */
+int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream);
+/* kernels.py:162-270: exact (bitwise) Gauss-Seidel forward averaging pass */
+int dm_k_mma_forward(const dm_flat *f, double *lam, double *F, const double *B, double *bounds,
+                     void *stream);
+/* kernels.py:273-362: exact backward averaging pass */
+int dm_k_mma_backward(const dm_flat *f, double *lam, const double *F, double *B, double *bounds,
+                      void *stream);
+/* kernels.py:365-398 */
+int dm_k_min_marginals(const dm_flat *f, const double *lam, const double *F, const double *B,
+                       double *m0, double *m1, void *stream);
+/* kernels.py:401-431 */
+int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bits, void *stream);
+
+/* --- vectors over dual coordinates / variables ----------------------------- */
+/* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */
+int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream);
+/* qn.py:118-129: d[l] = d_hat[l] - mean over the copies of var(l) */
+int dm_project_direction(const dm_flat *f, const double *d_hat, double *d, void *stream);
+/* dual.py:114-119: per-variable sum of lam over its copies (by variable id) */
+int dm_lambda_sums(const dm_flat *f, const double *lam, double *sums_by_var, void *stream);
+/* primal.py:83-111: agreement votes from fresh min-marginals (by variable id).
+ * agrees[v] in {0,1}; preferred[v] in {0,1}; score[v] = |sum of differences| */
+int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, int8_t *agrees,
+                        double *score, int8_t *preferred, void *stream);
+
+/* numpy pairwise summation order (np.add.reduce on contiguous float64):
+ * out[0] = 0.0 + pairwise(x[0:n]).  dm_dot uses the same tree on the
+ * elementwise products, i.e. exactly np.sum(a * b).  Results land in device
+ * memory.  Reduction trees are planned once per (device, length) and cached
+ * for the process; reductions of the same length must not run concurrently
+ * on two streams of one device. */
+int dm_sum(const double *x, int64_t n, double *out, void *stream);
+int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream);
+
+/* Elementwise updates with numpy's rounding (no contraction):
+ *   dm_axpy_dev : x[i] = x[i] - (alpha_host * dot_dev[0]) * y[i]            (qn.py:108-109)
+ *   dm_scale_dev: x[i] = (num_host / den_dev[0]) * x[i]                     (qn.py:111-112)
+ *   dm_lbfgs_up : x[i] = x[i] + s[i] * (alpha_dev[0] - rho_host * dot_dev[0]) (qn.py:113-115)
+ *   dm_axpy_host: x[i] = x[i] + gamma * y[i]                                (dual.py:83-87)
+ *   dm_sub      : out[i] = a[i] - b[i]                                      (qn.py:250)
+ * alpha_out (optional) receives alpha_host * dot_dev[0] for dm_axpy_dev. */
+int dm_axpy_dev(double *x, const double *y, double alpha_host, const double *dot_dev,
+                double *alpha_out, int64_t n, void *stream);
+int dm_scale_dev(double *x, double num_host, const double *den_dev, int64_t n, void *stream);
+int dm_lbfgs_up(double *x, const double *s, const double *alpha_dev, double rho_host,
+                const double *dot_dev, int64_t n, void *stream);
+int dm_axpy_host(double *x, double gamma, const double *y, int64_t n, void *stream);
+int dm_sub(double *out, const double *a, const double *b, int64_t n, void *stream);
+
+/* --- host-side checks of the device plans (tests only, not a fallback) ---- */
+/* Evaluates the planned pairwise tree on the host: == np.sum(x). */
+int dm_host_pairwise_sum(const double *x, int64_t n, double *out);
+/* Runs one exact averaging pass on the host in level-schedule task order
+ * with the device kernel's lane semantics (forward != 0: forward pass; F
+ * resets F[root] = 0 itself).  Used by the CPU
+ * test-suite to prove the schedule reproduces the sequential pass. */
+int dm_debug_emulate_mma(const dm_flat_desc *desc, int forward, double *lam, double *F, double *B,
+                         double *bounds, int64_t *depth_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DISCOMATCH_B200_H */

@@ -1,0 +1,982 @@
+// B200 (sm_100a) kernels of the DiscoMatch dual solver and the device half
+// of the C-ABI (include/discomatch_b200.h).
+//
+// Every kernel reproduces its reference counterpart bit-for-bit: binary64
+// only, no FMA contraction (-fmad=false plus explicit __d*_rn intrinsics on
+// the exact paths), identical association order and tie rules.
+//
+// Layout: the flat node table of FlatBdds (kernels.py:35-92) as int32 SoA
+// arrays in HBM; dual vectors (lam, F, B, bounds) float64.
+//
+// Exact averaging passes (kernels.py:162-362).  The reference visits
+// variables one at a time; a variable's update only depends on the copies
+// of the previous (forward) / next (backward) layer of each of its
+// diagrams.  The host turns that DAG into levels and packs same-level
+// variables into 32-lane warp tasks (one lane per diagram copy).  A
+// persistent cooperative kernel walks the tasks in level order; instead of
+// grid barriers it uses *self-validating* distances: before a pass every
+// distance the pass will produce is set to a NaN sentinel, a lane polls its
+// inputs with relaxed gpu-scope loads until none is the sentinel, and
+// producers publish with relaxed stores.  Each 8-byte value is written once
+// per pass, so no fences or flags are needed and the critical path is one
+// L2 round trip per DAG level.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dm_internal.h"
+
+#define DM_INF __longlong_as_double(0x7ff0000000000000LL)
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned long long kSentinel = 0x7ff4dead0badf00dULL;  // signalling-NaN payload
+
+__device__ __forceinline__ double ld_relaxed(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void st_relaxed(double *p, double x) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(x))
+                 : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(double x) {
+    return (unsigned long long)__double_as_longlong(x) == kSentinel;
+}
+
+// --------------------------------------------------------------------------
+// full sweeps (thread per diagram / per layer)
+// --------------------------------------------------------------------------
+template <bool kTrial>
+__global__ void k_backward_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
+                                  const int32_t *__restrict__ lnl, const int32_t *__restrict__ zero_t,
+                                  const int32_t *__restrict__ one_t, const double *__restrict__ lam,
+                                  const double *__restrict__ d, double gamma, double *__restrict__ B,
+                                  double *__restrict__ bounds) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nb) return;
+    const int32_t l_lo = bdd_layer_lo[j], l_hi = bdd_layer_lo[j + 1];
+    for (int32_t l = l_hi - 1; l >= l_lo; --l) {
+        double lam_l = lam[l];
+        if (kTrial) lam_l = __dadd_rn(lam_l, __dmul_rn(gamma, d[l]));
+        const int32_t v1 = lnl[l + 1];
+        for (int32_t v = lnl[l]; v < v1; ++v) {
+            const int32_t a = zero_t[v], b = one_t[v];
+            const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : B[a]);
+            const double c1 = b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, B[b]));
+            B[v] = (c0 <= c1) ? c0 : c1;
+        }
+    }
+    bounds[j] = B[lnl[l_lo]];
+}
+
+__global__ void k_forward_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
+                                 const int32_t *__restrict__ lnl, const int32_t *__restrict__ zero_t,
+                                 const int32_t *__restrict__ one_t, const double *__restrict__ lam,
+                                 double *__restrict__ F, double *__restrict__ bounds) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nb) return;
+    const int32_t l_lo = bdd_layer_lo[j], l_hi = bdd_layer_lo[j + 1];
+    const int32_t root = lnl[l_lo];
+    for (int32_t v = root; v < lnl[l_lo + 1]; ++v) F[v] = DM_INF;
+    F[root] = 0.0;
+    double tb = DM_INF;
+    for (int32_t l = l_lo; l < l_hi; ++l) {
+        if (l + 1 < l_hi)
+            for (int32_t w = lnl[l + 1]; w < lnl[l + 2]; ++w) F[w] = DM_INF;
+        const double lam_l = lam[l];
+        for (int32_t v = lnl[l]; v < lnl[l + 1]; ++v) {
+            const double fv = F[v];
+            if (fv == DM_INF) continue;
+            const int32_t a = zero_t[v];
+            if (a >= 0) {
+                if (fv < F[a]) F[a] = fv;
+            } else if (a == dm::kTrue) {
+                if (fv < tb) tb = fv;
+            }
+            const int32_t b = one_t[v];
+            const double c = __dadd_rn(fv, lam_l);
+            if (b >= 0) {
+                if (c < F[b]) F[b] = c;
+            } else if (b == dm::kTrue) {
+                if (c < tb) tb = c;
+            }
+        }
+    }
+    bounds[j] = tb;
+}
+
+__global__ void k_min_marginals_kernel(int32_t L, const int32_t *__restrict__ lnl,
+                                       const int32_t *__restrict__ zero_t, const int32_t *__restrict__ one_t,
+                                       const double *__restrict__ lam, const double *__restrict__ F,
+                                       const double *__restrict__ B, double *__restrict__ m0_out,
+                                       double *__restrict__ m1_out) {
+    const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const double lam_l = lam[l];
+    double m0 = DM_INF, m1 = DM_INF;
+    for (int32_t v = lnl[l]; v < lnl[l + 1]; ++v) {
+        const double fv = F[v];
+        if (fv == DM_INF) continue;
+        const int32_t a = zero_t[v], b = one_t[v];
+        const double c0 = a == dm::kTrue ? fv : (a == dm::kFalse ? DM_INF : __dadd_rn(fv, B[a]));
+        if (c0 < m0) m0 = c0;
+        const double c1 = b == dm::kTrue ? __dadd_rn(fv, lam_l)
+                                         : (b == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), B[b]));
+        if (c1 < m1) m1 = c1;
+    }
+    m0_out[l] = m0;
+    m1_out[l] = m1;
+}
+
+__global__ void k_argmin_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
+                                const int32_t *__restrict__ lnl, const int32_t *__restrict__ zero_t,
+                                const int32_t *__restrict__ one_t, const double *__restrict__ lam,
+                                const double *__restrict__ B, double *__restrict__ bits) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nb) return;
+    int32_t v = lnl[bdd_layer_lo[j]];
+    for (int32_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
+        const int32_t a = zero_t[v], b = one_t[v];
+        const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : B[a]);
+        const double c1 = b == dm::kTrue ? lam[l] : (b == dm::kFalse ? DM_INF : __dadd_rn(lam[l], B[b]));
+        int32_t nxt;
+        if (c0 <= c1) {
+            bits[l] = 0.0;
+            nxt = a;
+        } else {
+            bits[l] = 1.0;
+            nxt = b;
+        }
+        if (nxt >= 0) v = nxt;
+    }
+}
+
+// --------------------------------------------------------------------------
+// per-variable kernels (thread per visitation position)
+// --------------------------------------------------------------------------
+__global__ void init_duals_kernel(int32_t L, const int32_t *__restrict__ layer_var,
+                                  const int32_t *__restrict__ var_count, const double *__restrict__ costs,
+                                  double *__restrict__ lam) {
+    const int32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= L) return;
+    const int32_t v = layer_var[l];
+    lam[l] = __ddiv_rn(costs[v], (double)var_count[v]);
+}
+
+__global__ void project_kernel(int32_t P, const int32_t *__restrict__ proc_ptr,
+                               const int32_t *__restrict__ proc_layers, const double *__restrict__ dh,
+                               double *__restrict__ d) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
+    if (hi == lo) return;
+    double s = 0.0;
+    for (int32_t t = lo; t < hi; ++t) s = __dadd_rn(s, dh[proc_layers[t]]);
+    const double mean = __ddiv_rn(s, (double)(hi - lo));
+    for (int32_t t = lo; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        d[l] = __dsub_rn(dh[l], mean);
+    }
+}
+
+__global__ void lambda_sums_kernel(int32_t P, const int32_t *__restrict__ proc_ptr,
+                                   const int32_t *__restrict__ proc_layers,
+                                   const int32_t *__restrict__ pos_var, const double *__restrict__ lam,
+                                   double *__restrict__ out) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    double s = 0.0;
+    for (int32_t t = proc_ptr[p]; t < proc_ptr[p + 1]; ++t) s = __dadd_rn(s, lam[proc_layers[t]]);
+    out[pos_var[p]] = s;
+}
+
+__global__ void agreement_kernel(int32_t P, const int32_t *__restrict__ proc_ptr,
+                                 const int32_t *__restrict__ proc_layers, const int32_t *__restrict__ pos_var,
+                                 const double *__restrict__ m0, const double *__restrict__ m1,
+                                 int8_t *__restrict__ agrees, double *__restrict__ score,
+                                 int8_t *__restrict__ preferred) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    double vmax = -2.0, vmin = 2.0, total = 0.0;
+    const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
+    for (int32_t t = lo; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        const double a = m0[l], b = m1[l];
+        const bool fa = a != DM_INF, fb = b != DM_INF;
+        double diff;
+        if (fa && fb) diff = __dsub_rn(b, a);
+        else if (fa) diff = DM_INF;      // one-branch forced to 0
+        else if (fb) diff = -DM_INF;     // forced to 1
+        else diff = __longlong_as_double(0x7ff8000000000000LL);  // impossible in co-reachable diagrams
+        const double vote = diff > 0.0 ? 1.0 : (diff < 0.0 ? -1.0 : (diff == 0.0 ? 0.0 : diff));
+        vmax = fmax(vmax, vote);  // np.maximum propagates NaN; unreachable here
+        vmin = fmin(vmin, vote);
+        total = __dadd_rn(total, diff);
+    }
+    const int32_t v = pos_var[p];
+    agrees[v] = (vmax == vmin) && (vmax != 0.0) && (hi > lo);
+    const double t = total != total ? 0.0 : total;
+    score[v] = fabs(t);
+    preferred[v] = vmax > 0.0 ? 0 : 1;
+}
+
+// --------------------------------------------------------------------------
+// elementwise vectors (numpy rounding: one rounding per operation)
+// --------------------------------------------------------------------------
+__global__ void axpy_dev_kernel(double *__restrict__ x, const double *__restrict__ y, double alpha,
+                                const double *__restrict__ dot, double *__restrict__ alpha_out, int64_t n) {
+    const double a = __dmul_rn(alpha, dot[0]);
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0 && alpha_out) alpha_out[0] = a;
+    for (int64_t i = i0; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dsub_rn(x[i], __dmul_rn(a, y[i]));
+}
+
+__global__ void scale_dev_kernel(double *__restrict__ x, double num, const double *__restrict__ den, int64_t n) {
+    const double r = __ddiv_rn(num, den[0]);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dmul_rn(r, x[i]);
+}
+
+__global__ void lbfgs_up_kernel(double *__restrict__ x, const double *__restrict__ s,
+                                const double *__restrict__ alpha, double rho, const double *__restrict__ dot,
+                                int64_t n) {
+    const double c = __dsub_rn(alpha[0], __dmul_rn(rho, dot[0]));
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], __dmul_rn(s[i], c));
+}
+
+__global__ void axpy_host_kernel(double *__restrict__ x, double g, const double *__restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], __dmul_rn(g, y[i]));
+}
+
+__global__ void sub_kernel(double *__restrict__ out, const double *__restrict__ a, const double *__restrict__ b,
+                           int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __dsub_rn(a[i], b[i]);
+}
+
+// --------------------------------------------------------------------------
+// numpy pairwise summation (loops_utils.h.src pairwise_sum)
+// --------------------------------------------------------------------------
+template <bool kDot>
+__device__ __forceinline__ double pw_elem(const double *__restrict__ a, const double *__restrict__ b, int64_t i) {
+    if (kDot) return __dmul_rn(a[i], b[i]);
+    return a[i];
+}
+
+template <bool kDot>
+__global__ void pw_leaf_kernel(int32_t nleaves, const int64_t *__restrict__ leaf_off,
+                               const int32_t *__restrict__ leaf_len, const double *__restrict__ a,
+                               const double *__restrict__ b, double *__restrict__ vals) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nleaves) return;
+    const int64_t off = leaf_off[k];
+    const int32_t n = leaf_len[k];
+    const double *pa = a + off;
+    const double *pb = kDot ? b + off : nullptr;
+    double res;
+    if (n < 8) {
+        res = 0.0;
+        for (int32_t i = 0; i < n; ++i) res = __dadd_rn(res, pw_elem<kDot>(pa, pb, i));
+    } else {
+        double r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = pw_elem<kDot>(pa, pb, q);
+        const int32_t stop = n - (n % 8);
+        int32_t i = 8;
+        for (; i < stop; i += 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], pw_elem<kDot>(pa, pb, i + q));
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, pw_elem<kDot>(pa, pb, i));
+    }
+    vals[k] = res;
+}
+
+__global__ void pw_combine_kernel(int32_t nleaves, int32_t maxh, const int32_t *__restrict__ height_lo,
+                                  const int32_t *__restrict__ left, const int32_t *__restrict__ right,
+                                  int32_t root, double *__restrict__ vals, double *__restrict__ out) {
+    for (int32_t h = 1; h <= maxh; ++h) {
+        const int32_t lo = height_lo[h - 1], hi = height_lo[h];
+        for (int32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
+            vals[nleaves + k] = __dadd_rn(vals[left[k]], vals[right[k]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = __dadd_rn(0.0, vals[root]);
+}
+
+// --------------------------------------------------------------------------
+// exact averaging passes
+// --------------------------------------------------------------------------
+__global__ void fill_kernel(double *__restrict__ x, int64_t n, double v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void roots_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
+                             const int32_t *__restrict__ lnl, double *__restrict__ F) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nb) F[lnl[bdd_layer_lo[j]]] = 0.0;
+}
+
+struct MmaArgs {
+    int64_t ntasks;
+    const int32_t *task_layer, *task_meta;
+    const int32_t *lnl, *zero_t, *one_t, *layer_bdd;
+    double *lam, *F, *B, *bounds;
+};
+
+// Sum of the finite min-marginal differences of the lane's variable, in copy
+// order (kernels.py:200-233), then the lane's new dual (kernels.py:234-240).
+__device__ __forceinline__ double average_in_group(bool act, int32_t meta, double m0, double m1,
+                                                   double lam_l) {
+    const bool fin = act && m0 != DM_INF && m1 != DM_INF;
+    const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
+    const int gbase = meta & 0xff, gcnt = (meta >> 8) & 0xff;
+    const int maxc = __reduce_max_sync(kFull, act ? gcnt : 0);
+    double fsum = 0.0;
+    int fcnt = 0;
+    for (int k = 0; k < maxc; ++k) {
+        const double dk = __shfl_sync(kFull, dlt, (gbase + k) & 31);
+        const int fk = __shfl_sync(kFull, (int)fin, (gbase + k) & 31);
+        if (k < gcnt && fk) {
+            fsum = __dadd_rn(fsum, dk);
+            ++fcnt;
+        }
+    }
+    if (fin && fcnt > 0) {
+        const double avg = __ddiv_rn(fsum, (double)fcnt);
+        lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
+    }
+    return lam_l;
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
+        const int32_t l = a.task_layer[task * 32 + lane];
+        const int32_t meta = a.task_meta[task * 32 + lane];
+        const bool act = l >= 0;
+        int32_t nlo = 0, w = 0;
+        double lam_l = 0.0;
+        int32_t z[W], o[W];
+        double bz[W], bo[W], f[W];
+        if (act) {
+            nlo = a.lnl[l];
+            w = a.lnl[l + 1] - nlo;
+            lam_l = a.lam[l];
+        }
+        // static inputs: topology and the backward distances (valid all pass)
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w) {
+                z[i] = a.zero_t[nlo + i];
+                o[i] = a.one_t[nlo + i];
+                bz[i] = z[i] >= 0 ? a.B[z[i]] : 0.0;
+                bo[i] = o[i] >= 0 ? a.B[o[i]] : 0.0;
+            }
+        }
+        // wait until the producer of this layer's forward distances published them
+        bool ready;
+        do {
+            ready = true;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < w) {
+                    f[i] = ld_relaxed(a.F + nlo + i);
+                    ready &= !is_sentinel(f[i]);
+                }
+        } while (!__all_sync(kFull, ready));
+        // min-marginals (kernels.py:205-230)
+        double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w && f[i] != DM_INF) {
+                const double fv = f[i];
+                const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
+                if (c0 < m0) m0 = c0;
+                const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
+                                                    : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
+                if (c1 < m1) m1 = c1;
+            }
+        }
+        lam_l = average_in_group(act, meta, m0, m1, lam_l);
+        if (!act) continue;
+        a.lam[l] = lam_l;
+        // propagate to the next layer (kernels.py:241-269), gather form with the
+        // reference's scatter order: first strict minimum over (v asc, zero, one)
+        if (!(meta & (1 << 17))) {
+            const int32_t n0 = a.lnl[l + 1];
+            const int32_t wn = a.lnl[l + 2] - n0;
+            for (int32_t u = 0; u < wn; ++u) {
+                double best = DM_INF;
+                const int32_t tgt = n0 + u;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    if (i < w && f[i] != DM_INF) {
+                        if (z[i] == tgt && f[i] < best) best = f[i];
+                        const double c = __dadd_rn(f[i], lam_l);
+                        if (o[i] == tgt && c < best) best = c;
+                    }
+                }
+                st_relaxed(a.F + tgt, best);
+            }
+        } else {
+            double tb = DM_INF;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                if (i < w && f[i] != DM_INF) {
+                    if (z[i] == dm::kTrue && f[i] < tb) tb = f[i];
+                    const double c = __dadd_rn(f[i], lam_l);
+                    if (o[i] == dm::kTrue && c < tb) tb = c;
+                }
+            }
+            a.bounds[a.layer_bdd[l]] = tb;
+        }
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
+        const int32_t l = a.task_layer[task * 32 + lane];
+        const int32_t meta = a.task_meta[task * 32 + lane];
+        const bool act = l >= 0;
+        int32_t nlo = 0, w = 0;
+        double lam_l = 0.0;
+        int32_t z[W], o[W];
+        double bz[W], bo[W], f[W];
+        if (act) {
+            nlo = a.lnl[l];
+            w = a.lnl[l + 1] - nlo;
+            lam_l = a.lam[l];
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w) {
+                z[i] = a.zero_t[nlo + i];
+                o[i] = a.one_t[nlo + i];
+                f[i] = a.F[nlo + i];
+            }
+        }
+        bool ready;
+        do {
+            ready = true;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < w) {
+                    if (z[i] >= 0) {
+                        bz[i] = ld_relaxed(a.B + z[i]);
+                        ready &= !is_sentinel(bz[i]);
+                    }
+                    if (o[i] >= 0) {
+                        bo[i] = ld_relaxed(a.B + o[i]);
+                        ready &= !is_sentinel(bo[i]);
+                    }
+                }
+        } while (!__all_sync(kFull, ready));
+        double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w && f[i] != DM_INF) {
+                const double fv = f[i];
+                const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
+                if (c0 < m0) m0 = c0;
+                const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
+                                                    : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
+                if (c1 < m1) m1 = c1;
+            }
+        }
+        lam_l = average_in_group(act, meta, m0, m1, lam_l);
+        if (!act) continue;
+        a.lam[l] = lam_l;
+        // rebuild this layer's distances to TRUE with the new dual (kernels.py:340-358)
+        double first = 0.0;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w) {
+                const double c0 = z[i] == dm::kTrue ? 0.0 : (z[i] == dm::kFalse ? DM_INF : bz[i]);
+                const double c1 = o[i] == dm::kTrue ? lam_l : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo[i]));
+                const double bv = (c0 <= c1) ? c0 : c1;
+                st_relaxed(a.B + nlo + i, bv);
+                if (i == 0) first = bv;
+            }
+        }
+        if (meta & (1 << 16)) a.bounds[a.layer_bdd[l]] = first;  // kernels.py:359-361
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// device handle
+// ===========================================================================
+struct DevPlan {
+    int64_t n = 0;
+    int32_t nleaves = 0, maxh = 0, root = 0;
+    int64_t *leaf_off = nullptr;
+    int32_t *leaf_len = nullptr, *left = nullptr, *right = nullptr, *height_lo = nullptr;
+    double *vals = nullptr;
+};
+
+struct dm_flat {
+    int device = 0;
+    int64_t nb = 0, L = 0, N = 0, P = 0;
+    int32_t *bdd_layer_lo = nullptr, *lnl = nullptr, *layer_bdd = nullptr, *layer_var = nullptr;
+    int32_t *zero_t = nullptr, *one_t = nullptr, *proc_ptr = nullptr, *proc_layers = nullptr;
+    int32_t *pos_var = nullptr, *var_count = nullptr;
+    int32_t *fw_layer = nullptr, *fw_meta = nullptr, *bw_layer = nullptr, *bw_meta = nullptr;
+    int64_t fw_tasks = 0, bw_tasks = 0, fw_depth = 0, bw_depth = 0;
+    int64_t max_width = 0, max_degree = 0;
+    int mma_w = 8;
+    int mma_grid_fw = 0, mma_grid_bw = 0;
+    int64_t bytes = 0;
+    std::vector<void *> allocs;
+};
+
+namespace {
+
+thread_local std::string g_cuda_err;
+
+int cuda_fail(cudaError_t e, const char *what) {
+    dm::set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return DM_ERR_CUDA;
+}
+#define DM_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+template <typename T>
+int upload(dm_flat *f, T **dst, const T *src, int64_t n, cudaStream_t s) {
+    size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+    DM_CUDA(cudaMalloc((void **)dst, bytes));
+    f->allocs.push_back(*dst);
+    f->bytes += bytes;
+    if (n > 0 && src) DM_CUDA(cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    return DM_OK;
+}
+
+// Pairwise plans are cached per (device, length) for the process lifetime.
+// The value scratch of a plan is shared: reductions of one length must not
+// run concurrently on two streams of the same device.
+std::mutex g_plan_mu;
+std::map<std::pair<int, int64_t>, DevPlan> g_plans;
+
+template <typename T>
+int plan_upload(T **dst, const std::vector<T> &src, size_t extra = 0) {
+    size_t n = src.size() + extra;
+    DM_CUDA(cudaMalloc((void **)dst, std::max<size_t>(n, 1) * sizeof(T)));
+    if (!src.empty()) DM_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return DM_OK;
+}
+
+int get_plan(int64_t n, DevPlan **out) {
+    int dev;
+    DM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    auto key = std::make_pair(dev, n);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) {
+        *out = &it->second;
+        return DM_OK;
+    }
+    dm::PairwisePlan p = dm::plan_pairwise(n);
+    DevPlan d;
+    d.n = n;
+    d.nleaves = (int32_t)p.leaf_off.size();
+    d.maxh = (int32_t)p.height_lo.size() - 1;
+    d.root = p.root;
+    int rc;
+    if ((rc = plan_upload(&d.leaf_off, p.leaf_off))) return rc;
+    if ((rc = plan_upload(&d.leaf_len, p.leaf_len))) return rc;
+    if ((rc = plan_upload(&d.left, p.left))) return rc;
+    if ((rc = plan_upload(&d.right, p.right))) return rc;
+    if ((rc = plan_upload(&d.height_lo, p.height_lo))) return rc;
+    if ((rc = plan_upload(&d.vals, std::vector<double>(), p.leaf_off.size() + p.left.size()))) return rc;
+    auto res = g_plans.emplace(key, d);
+    *out = &res.first->second;
+    return DM_OK;
+}
+
+inline int blocks_for(int64_t n, int threads) { return (int)std::max<int64_t>(1, (n + threads - 1) / threads); }
+inline int grid_stride_blocks(int64_t n) { return (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 255) / 256)); }
+
+template <int W>
+int launch_mma(const dm_flat *f, bool forward, MmaArgs &args, cudaStream_t s) {
+    void *params[] = {&args};
+    const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
+    const int grid = forward ? f->mma_grid_fw : f->mma_grid_bw;
+    DM_CUDA(cudaLaunchCooperativeKernel(fn, grid, 256, params, 0, s));
+    return DM_OK;
+}
+
+template <int W>
+int mma_grid_for(bool forward, int *grid) {
+    int dev, sms, per;
+    DM_CUDA(cudaGetDevice(&dev));
+    DM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
+    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0));
+    if (per < 1) {
+        dm::set_error("exact averaging kernel cannot be resident");
+        return DM_ERR_CUDA;
+    }
+    *grid = sms * per;
+    return DM_OK;
+}
+
+int check_stream_error(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    return DM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dm_version(void) {
+    return "discomatch_b200 0.1 (sm_100a, fp64 exact)";
+}
+
+int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out) {
+    if (!desc || !out) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    *out = nullptr;
+    const int64_t nb = desc->num_bdds, L = desc->num_layers, N = desc->num_nodes, P = desc->num_positions;
+    if (nb < 0 || L < 0 || N < 0 || P < 0 || L >= INT32_MAX || N >= INT32_MAX - 2 || P >= INT32_MAX) {
+        dm::set_error("instance sizes outside the int32 device layout");
+        return DM_ERR_UNSUPPORTED;
+    }
+    // validate the structure the kernels rely on (bdd.py:336-359 invariants)
+    const int64_t *bl = desc->bdd_layer_lo, *lnl = desc->layer_node_lo;
+    if (bl[0] != 0 || bl[nb] != L || lnl[0] != 0 || lnl[L] != N || desc->proc_ptr[0] != 0 || desc->proc_ptr[P] != L) {
+        dm::set_error("inconsistent flat table offsets");
+        return DM_ERR_INVALID;
+    }
+    std::vector<int32_t> layer_bdd(L), var_count, pos_var(P, -1);
+    int64_t max_width = 0, max_degree = 0;
+    for (int64_t j = 0; j < nb; ++j) {
+        if (bl[j + 1] <= bl[j] || lnl[bl[j] + 1] - lnl[bl[j]] != 1) {
+            dm::set_error("every diagram needs >= 1 layer and a single root node");
+            return DM_ERR_INVALID;
+        }
+        for (int64_t l = bl[j]; l < bl[j + 1]; ++l) {
+            layer_bdd[l] = (int32_t)j;
+            const int64_t w = lnl[l + 1] - lnl[l];
+            if (w <= 0) {
+                dm::set_error("empty layer");
+                return DM_ERR_INVALID;
+            }
+            max_width = std::max(max_width, w);
+            const bool last = l + 1 == bl[j + 1];
+            for (int64_t v = lnl[l]; v < lnl[l + 1]; ++v)
+                for (int64_t t : {desc->zero_t[v], desc->one_t[v]}) {
+                    if (last ? (t >= 0 || t < -2) : (t == -2 || t < -2 || (t >= 0 && (t < lnl[l + 1] || t >= lnl[l + 2])))) {
+                        dm::set_error("arc targets must reach the next layer (or a terminal from the last layer)");
+                        return DM_ERR_UNSUPPORTED;
+                    }
+                }
+        }
+    }
+    if (max_width > 32) {
+        dm::set_error("layers wider than 32 nodes are not supported by the exact averaging kernels");
+        return DM_ERR_UNSUPPORTED;
+    }
+    int64_t max_var = -1;
+    for (int64_t l = 0; l < L; ++l) max_var = std::max(max_var, desc->layer_var[l]);
+    const int64_t V = std::max<int64_t>(max_var + 1, P);
+    var_count.assign(V, 0);
+    for (int64_t p = 0; p < P; ++p) {
+        const int64_t lo = desc->proc_ptr[p], hi = desc->proc_ptr[p + 1];
+        max_degree = std::max(max_degree, hi - lo);
+        if (hi > lo) {
+            const int64_t v = desc->layer_var[desc->proc_layers[lo]];
+            pos_var[p] = (int32_t)v;
+            var_count[v] = (int32_t)(hi - lo);
+        }
+    }
+    dm::MmaSchedule fw, bw;
+    int rc = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P, true, fw);
+    if (rc != DM_OK) return rc;
+    rc = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P, false, bw);
+    if (rc != DM_OK) return rc;
+
+    DM_CUDA(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    auto f = std::make_unique<dm_flat>();
+    f->device = device;
+    f->nb = nb;
+    f->L = L;
+    f->N = N;
+    f->P = P;
+    f->max_width = max_width;
+    f->max_degree = max_degree;
+    f->fw_depth = fw.depth;
+    f->bw_depth = bw.depth;
+    f->fw_tasks = fw.tasks;
+    f->bw_tasks = bw.tasks;
+    auto i32 = [](const int64_t *src, int64_t n) {
+        std::vector<int32_t> v(n);
+        for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)src[i];
+        return v;
+    };
+    std::vector<std::vector<int32_t>> keep;  // alive until the uploads finished
+    auto up = [&](int32_t **dst, std::vector<int32_t> v) {
+        keep.push_back(std::move(v));
+        return upload(f.get(), dst, keep.back().data(), (int64_t)keep.back().size(), s);
+    };
+    if ((rc = up(&f->bdd_layer_lo, i32(bl, nb + 1)))) return rc;
+    if ((rc = up(&f->lnl, i32(lnl, L + 1)))) return rc;
+    if ((rc = up(&f->layer_var, i32(desc->layer_var, L)))) return rc;
+    if ((rc = up(&f->zero_t, i32(desc->zero_t, N)))) return rc;
+    if ((rc = up(&f->one_t, i32(desc->one_t, N)))) return rc;
+    if ((rc = up(&f->proc_ptr, i32(desc->proc_ptr, P + 1)))) return rc;
+    if ((rc = up(&f->proc_layers, i32(desc->proc_layers, L)))) return rc;
+    if ((rc = up(&f->layer_bdd, std::move(layer_bdd)))) return rc;
+    if ((rc = up(&f->pos_var, std::move(pos_var)))) return rc;
+    if ((rc = up(&f->var_count, std::move(var_count)))) return rc;
+    if ((rc = up(&f->fw_layer, std::move(fw.task_layer)))) return rc;
+    if ((rc = up(&f->fw_meta, std::move(fw.task_meta)))) return rc;
+    if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
+    if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
+    f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
+    switch (f->mma_w) {
+        case 8: rc = mma_grid_for<8>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<8>(false, &f->mma_grid_bw); break;
+        case 16: rc = mma_grid_for<16>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<16>(false, &f->mma_grid_bw); break;
+        default: rc = mma_grid_for<32>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<32>(false, &f->mma_grid_bw); break;
+    }
+    if (rc) return rc;
+    DevPlan *dummy;
+    if ((rc = get_plan(nb, &dummy))) return rc;
+    if ((rc = get_plan(L, &dummy))) return rc;
+    DM_CUDA(cudaStreamSynchronize(s));
+    *out = f.release();
+    return DM_OK;
+}
+
+int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
+    if (!f || !info) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    info->fw_depth = f->fw_depth;
+    info->bw_depth = f->bw_depth;
+    info->fw_tasks = f->fw_tasks;
+    info->bw_tasks = f->bw_tasks;
+    info->mma_grid = f->mma_grid_fw;
+    info->mma_block = 256;
+    info->max_width = f->max_width;
+    info->max_degree = f->max_degree;
+    info->device_bytes = f->bytes;
+    return DM_OK;
+}
+
+void dm_flat_destroy(dm_flat *f) {
+    if (!f) return;
+    for (void *p : f->allocs) cudaFree(p);
+    delete f;
+}
+
+#define DM_CHECK_FLAT(f)                        \
+    if (!(f)) {                                 \
+        dm::set_error("null flat handle");      \
+        return DM_ERR_INVALID;                  \
+    }
+
+int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->nb == 0) return DM_OK;
+    k_backward_kernel<false><<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, nullptr, 0.0, B, bounds);
+    return check_stream_error("k_backward");
+}
+
+int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, double gamma, double *B,
+                        double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->nb == 0) return DM_OK;
+    k_backward_kernel<true><<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, d, gamma, B, bounds);
+    return check_stream_error("k_backward_trial");
+}
+
+int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->nb == 0) return DM_OK;
+    k_forward_kernel<<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, F, bounds);
+    return check_stream_error("k_forward");
+}
+
+static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, double *B, double *bounds,
+                    cudaStream_t s) {
+    if (f->nb == 0) return DM_OK;
+    double sent;
+    std::memcpy(&sent, &kSentinel, sizeof(sent));
+    if (forward) {
+        fill_kernel<<<grid_stride_blocks(f->N), 256, 0, s>>>(F, f->N, sent);
+        roots_kernel<<<blocks_for(f->nb, 256), 256, 0, s>>>((int32_t)f->nb, f->bdd_layer_lo, f->lnl, F);
+    } else {
+        fill_kernel<<<grid_stride_blocks(f->N), 256, 0, s>>>(B, f->N, sent);
+    }
+    int rc = check_stream_error("mma fill");
+    if (rc) return rc;
+    MmaArgs args;
+    args.ntasks = forward ? f->fw_tasks : f->bw_tasks;
+    args.task_layer = forward ? f->fw_layer : f->bw_layer;
+    args.task_meta = forward ? f->fw_meta : f->bw_meta;
+    args.lnl = f->lnl;
+    args.zero_t = f->zero_t;
+    args.one_t = f->one_t;
+    args.layer_bdd = f->layer_bdd;
+    args.lam = lam;
+    args.F = F;
+    args.B = B;
+    args.bounds = bounds;
+    switch (f->mma_w) {
+        case 8: return launch_mma<8>(f, forward, args, s);
+        case 16: return launch_mma<16>(f, forward, args, s);
+        default: return launch_mma<32>(f, forward, args, s);
+    }
+}
+
+int dm_k_mma_forward(const dm_flat *f, double *lam, double *F, const double *B, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    return mma_pass(f, true, lam, F, const_cast<double *>(B), bounds, (cudaStream_t)stream);
+}
+
+int dm_k_mma_backward(const dm_flat *f, double *lam, const double *F, double *B, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    return mma_pass(f, false, lam, const_cast<double *>(F), B, bounds, (cudaStream_t)stream);
+}
+
+int dm_k_min_marginals(const dm_flat *f, const double *lam, const double *F, const double *B, double *m0,
+                       double *m1, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->L == 0) return DM_OK;
+    k_min_marginals_kernel<<<blocks_for(f->L, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->L, f->lnl, f->zero_t, f->one_t, lam, F, B, m0, m1);
+    return check_stream_error("k_min_marginals");
+}
+
+int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bits, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->nb == 0) return DM_OK;
+    k_argmin_kernel<<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, B, bits);
+    return check_stream_error("k_argmin");
+}
+
+int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->L == 0) return DM_OK;
+    init_duals_kernel<<<blocks_for(f->L, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->L, f->layer_var, f->var_count, costs_by_var, lam);
+    return check_stream_error("init_duals");
+}
+
+int dm_project_direction(const dm_flat *f, const double *d_hat, double *d, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->P == 0) return DM_OK;
+    project_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->P, f->proc_ptr, f->proc_layers, d_hat, d);
+    return check_stream_error("project_direction");
+}
+
+int dm_lambda_sums(const dm_flat *f, const double *lam, double *sums_by_var, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->P == 0) return DM_OK;
+    lambda_sums_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, lam, sums_by_var);
+    return check_stream_error("lambda_sums");
+}
+
+int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, int8_t *agrees, double *score,
+                        int8_t *preferred, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->P == 0) return DM_OK;
+    agreement_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, m0, m1, agrees, score, preferred);
+    return check_stream_error("agreement_scores");
+}
+
+static int pairwise(const double *a, const double *b, int64_t n, double *out, cudaStream_t s) {
+    if (n < 0 || n >= INT32_MAX || !a || !out) {
+        dm::set_error("invalid reduction arguments");
+        return DM_ERR_INVALID;
+    }
+    DevPlan *p;
+    int rc = get_plan(n, &p);
+    if (rc) return rc;
+    if (b)
+        pw_leaf_kernel<true><<<blocks_for(p->nleaves, 128), 128, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, b, p->vals);
+    else
+        pw_leaf_kernel<false><<<blocks_for(p->nleaves, 128), 128, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, nullptr, p->vals);
+    pw_combine_kernel<<<1, 1024, 0, s>>>(p->nleaves, p->maxh, p->height_lo, p->left, p->right, p->root, p->vals, out);
+    return check_stream_error("pairwise sum");
+}
+
+int dm_sum(const double *x, int64_t n, double *out, void *stream) {
+    return pairwise(x, nullptr, n, out, (cudaStream_t)stream);
+}
+
+int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream) {
+    if (!b) {
+        dm::set_error("dm_dot needs two vectors");
+        return DM_ERR_INVALID;
+    }
+    return pairwise(a, b, n, out, (cudaStream_t)stream);
+}
+
+int dm_axpy_dev(double *x, const double *y, double alpha_host, const double *dot_dev, double *alpha_out, int64_t n,
+                void *stream) {
+    axpy_dev_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, y, alpha_host, dot_dev, alpha_out, n);
+    return check_stream_error("axpy_dev");
+}
+
+int dm_scale_dev(double *x, double num_host, const double *den_dev, int64_t n, void *stream) {
+    scale_dev_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, num_host, den_dev, n);
+    return check_stream_error("scale_dev");
+}
+
+int dm_lbfgs_up(double *x, const double *s, const double *alpha_dev, double rho_host, const double *dot_dev, int64_t n,
+                void *stream) {
+    lbfgs_up_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, s, alpha_dev, rho_host, dot_dev, n);
+    return check_stream_error("lbfgs_up");
+}
+
+int dm_axpy_host(double *x, double gamma, const double *y, int64_t n, void *stream) {
+    axpy_host_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, gamma, y, n);
+    return check_stream_error("axpy_host");
+}
+
+int dm_sub(double *out, const double *a, const double *b, int64_t n, void *stream) {
+    sub_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(out, a, b, n);
+    return check_stream_error("sub");
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// Internal declarations shared by the host lowering, the schedule builder and
+// the CUDA translation units.  Not part of the public C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/discomatch_b200.h"
+
+namespace dm {
+
+constexpr int32_t kFalse = -1;  // FALSE terminal (bdd.py:24)
+constexpr int32_t kTrue = -2;   // TRUE terminal  (bdd.py:25)
+
+void set_error(const std::string &msg);
+
+// One reduced, layered diagram in the reference's Bdd layout (bdd.py:55-87):
+// layer l branches on vars[l]; zeros/ones hold local next-layer indices or
+// the terminal sentinels; layer_lo[l] .. layer_lo[l+1] indexes zeros/ones.
+struct HostBdd {
+    std::vector<int64_t> vars;
+    std::vector<int64_t> layer_lo;  // size vars.size()+1
+    std::vector<int32_t> zeros, ones;
+    int64_t width(size_t l) const { return layer_lo[l + 1] - layer_lo[l]; }
+};
+
+// Flat table (kernels.py:35-92), int64 like the reference.
+struct FlatHost {
+    std::vector<double> costs;
+    std::vector<int64_t> order, positions, counts;
+    std::vector<int64_t> bdd_layer_lo, layer_node_lo, layer_var, layer_bdd;
+    std::vector<int64_t> zero_t, one_t, proc_ptr, proc_layers;
+    int64_t max_width = 0, max_degree = 0, max_layers = 0;
+};
+
+// Returns DM_OK or an error code (message via set_error).
+int build_equality_bdd(const int64_t *coef, const int64_t *vars, int64_t n, int64_t rhs,
+                       HostBdd &out);
+int flatten(std::vector<HostBdd> &bdds, std::vector<double> costs, std::vector<int64_t> order,
+            FlatHost &out);
+
+// numpy pairwise-summation tree for a fixed length (loops_utils.h.src
+// pairwise_sum: blocks of <= 128 summed with 8 accumulators, splits at
+// n/2 rounded down to a multiple of 8).
+struct PairwisePlan {
+    int64_t n = 0;
+    std::vector<int64_t> leaf_off;  // leaves left to right
+    std::vector<int32_t> leaf_len;
+    // internal nodes ordered by height; children index the value array
+    // [leaves..., internal...]
+    std::vector<int32_t> left, right;
+    std::vector<int32_t> height_lo;  // internal nodes of height h: [height_lo[h-1], height_lo[h])
+    int32_t root = 0;                // value index of the root
+};
+PairwisePlan plan_pairwise(int64_t n);
+
+// Exact-pass schedule: warp tasks of same-level variables; lane i of task k
+// handles copy task_layer[32k+i] (global layer id or -1), meta packs the
+// lane's group base lane (bits 0-7), group size (8-15), first-layer flag
+// (bit 16) and last-layer flag (bit 17).
+struct MmaSchedule {
+    std::vector<int32_t> task_layer, task_meta;
+    int64_t depth = 0, tasks = 0;
+};
+int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_bdd_or_null,
+                       const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,
+                       const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &out);
+
+}  // namespace dm

@@ -1,0 +1,203 @@
+"""Lagrangian dual state and exact min-marginal-averaging passes on the GPU.
+
+Same API and semantics as the reference (dual.py:29-201): ``lam`` has one
+entry per (variable, constraint) incidence indexed by global layer id, the
+forward/backward distance caches carry validity flags, and every bound is
+the numpy-pairwise sum of the per-diagram optima plus the contribution of
+unconstrained variables.  All vectors live in HBM (``lam_d``, ``F``, ``B``);
+``lam`` and the table accessors return host copies for API compatibility.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .ilp import IlpInstance
+from .kernels import DeviceFlat, FlatBdds, dev_axpy_host, dev_sum
+
+FORWARD = "forward"
+BACKWARD = "backward"
+
+_F64 = torch.float64
+
+
+def as_device(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=_F64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=device)
+
+
+class DualState:
+    """Per-constraint duals plus cached sweep distances, resident on a GPU."""
+
+    def __init__(self, instance: IlpInstance, flat: FlatBdds | None = None, device=None):
+        self.instance = instance
+        self.flat = flat if flat is not None else FlatBdds(instance)
+        self.dev: DeviceFlat = self.flat.device(device)
+        d = self.dev.device
+        self.device = d
+        f = self.flat
+        self.lam_d = torch.zeros(f.num_layers, dtype=_F64, device=d)
+        self.F = torch.zeros(f.num_nodes, dtype=_F64, device=d)
+        self.B = torch.zeros(f.num_nodes, dtype=_F64, device=d)
+        self._bounds = torch.zeros(f.num_bdds, dtype=_F64, device=d)
+        self._scratch_B: torch.Tensor | None = None
+        self._scratch_bounds = torch.zeros(f.num_bdds, dtype=_F64, device=d)
+        self._scal = torch.zeros(8, dtype=_F64, device=d)
+        self.f_valid = False
+        self.b_valid = False
+        self.bound = -np.inf
+        self.best_bound = -np.inf
+        self.sweeps = 0  # full-table sweep equivalents (2 arcs per node each)
+        free = instance.unconstrained_variables()
+        self.free_values = {int(v): (0 if instance.costs[v] >= 0 else 1) for v in free}
+        self.free_contribution = float(np.minimum(instance.costs[free], 0.0).sum()) if len(free) else 0.0
+
+    # -- host views -------------------------------------------------------
+    @property
+    def lam(self) -> np.ndarray:
+        return self.lam_d.cpu().numpy()
+
+    @property
+    def arc_updates(self) -> int:
+        return self.sweeps * 2 * self.flat.num_nodes
+
+    # -- cache management (dual.py:66-106) ---------------------------------
+    def _sum_bounds(self, bounds: torch.Tensor) -> float:
+        dev_sum(bounds, self._scal[0:1])
+        return float(self._scal[0].item()) + self.free_contribution
+
+    def _set_bound(self) -> None:
+        self.bound = self._sum_bounds(self._bounds)
+        if self.bound > self.best_bound:
+            self.best_bound = self.bound
+
+    def refresh_backward(self) -> None:
+        self.dev.k_backward(self.lam_d, self.B, self._bounds)
+        self.sweeps += 1
+        self.b_valid = True
+        self._set_bound()
+
+    def refresh_forward(self) -> None:
+        self.dev.k_forward(self.lam_d, self.F, self._bounds)
+        self.sweeps += 1
+        self.f_valid = True
+        self._set_bound()
+
+    def shift_lambda(self, delta) -> None:
+        """Move the duals along a feasibility-preserving direction."""
+        self.lam_d += as_device(delta, self.device)
+        self.f_valid = False
+        self.b_valid = False
+
+    def shift_lambda_scaled(self, gamma: float, d: torch.Tensor) -> None:
+        """lam += gamma * d with numpy's two roundings (qn.py:206)."""
+        dev_axpy_host(self.lam_d, gamma, d)
+        self.f_valid = False
+        self.b_valid = False
+
+    def set_lambda(self, lam) -> None:
+        lam_t = as_device(lam, self.device)
+        if lam_t.shape != self.lam_d.shape:
+            raise ValueError("dual vector length mismatch")
+        self.lam_d.copy_(lam_t)
+        self.f_valid = False
+        self.b_valid = False
+        self.refresh_backward()
+
+    def _scratch(self) -> torch.Tensor:
+        if self._scratch_B is None:
+            self._scratch_B = torch.zeros(self.flat.num_nodes, dtype=_F64, device=self.device)
+        return self._scratch_B
+
+    def eval_lambda(self, lam_trial) -> float:
+        """Dual objective of a trial vector; caches are left untouched."""
+        self.dev.k_backward(as_device(lam_trial, self.device), self._scratch(), self._scratch_bounds)
+        self.sweeps += 1
+        return self._sum_bounds(self._scratch_bounds)
+
+    def eval_step(self, d: torch.Tensor, gamma: float) -> float:
+        """Objective at lam + gamma*d without materialising it (fused trial)."""
+        self.dev.k_backward_trial(self.lam_d, d, gamma, self._scratch(), self._scratch_bounds)
+        self.sweeps += 1
+        return self._sum_bounds(self._scratch_bounds)
+
+    # -- dual vectors per constraint ------------------------------------------
+    def lambda_of(self, constraint: int) -> np.ndarray:
+        lo, hi = self.flat.bdd_layer_lo[constraint], self.flat.bdd_layer_lo[constraint + 1]
+        return self.lam_d[lo:hi].cpu().numpy()
+
+    def lambda_sums(self) -> np.ndarray:
+        """Per-variable sum of dual entries (== costs when feasible)."""
+        out = torch.zeros(self.instance.num_variables, dtype=_F64, device=self.device)
+        self.dev.lambda_sums(self.lam_d, out)
+        res = out.cpu().numpy()
+        fv = list(self.free_values)
+        res[fv] = self.instance.costs[fv]
+        return res
+
+    def min_marginal_table_device(self) -> tuple[torch.Tensor, torch.Tensor]:
+        if not self.f_valid:
+            self.refresh_forward()
+        if not self.b_valid:
+            self.refresh_backward()
+        m0 = torch.empty(self.flat.num_layers, dtype=_F64, device=self.device)
+        m1 = torch.empty_like(m0)
+        self.dev.k_min_marginals(self.lam_d, self.F, self.B, m0, m1)
+        return m0, m1
+
+    def min_marginal_table(self) -> tuple[np.ndarray, np.ndarray]:
+        """Fresh (m0, m1) per layer at the current duals."""
+        m0, m1 = self.min_marginal_table_device()
+        return m0.cpu().numpy(), m1.cpu().numpy()
+
+
+def init_duals(instance: IlpInstance, device=None, flat: FlatBdds | None = None) -> DualState:
+    """Spread every cost uniformly over the constraints containing it (dual.py:137-144)."""
+    state = DualState(instance, flat=flat, device=device)
+    costs = torch.as_tensor(np.ascontiguousarray(instance.costs, dtype=np.float64), device=state.device)
+    state.dev.init_duals(costs, state.lam_d)
+    state.refresh_backward()
+    return state
+
+
+def dual_objective(state: DualState) -> float:
+    """Sum of subproblem optima; a lower bound for the integer program."""
+    if not (state.b_valid or state.f_valid):
+        state.refresh_backward()
+    return state.bound
+
+
+def mma_pass(state: DualState, direction: str) -> DualState:
+    """One exact averaging pass over all variables (dual.py:154-186)."""
+    if direction == FORWARD:
+        if not state.b_valid:
+            state.refresh_backward()
+        state.dev.k_mma_forward(state.lam_d, state.F, state.B, state._bounds)
+        state.f_valid = True
+        state.b_valid = False
+    elif direction == BACKWARD:
+        if not state.f_valid:
+            state.refresh_forward()
+        state.dev.k_mma_backward(state.lam_d, state.F, state.B, state._bounds)
+        state.b_valid = True
+        state.f_valid = False
+    else:
+        raise ValueError(f"unknown pass direction {direction!r}")
+    state.sweeps += 2
+    state._set_bound()
+    return state
+
+
+def subgradient_device(state: DualState) -> torch.Tensor:
+    if not state.b_valid:
+        state.refresh_backward()
+    bits = torch.empty(state.flat.num_layers, dtype=_F64, device=state.device)
+    state.dev.k_argmin(state.lam_d, state.B, bits)
+    return bits
+
+
+def subgradient(state: DualState) -> np.ndarray:
+    """Concatenated minimising assignments of all subproblems (dual.py:189-201)."""
+    return subgradient_device(state).cpu().numpy()

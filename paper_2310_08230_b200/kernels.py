@@ -1,0 +1,188 @@
+"""Flat diagram table (FlatBdds, kernels.py:35-92 of the reference) and its
+device-resident twin.
+
+``FlatBdds(instance)`` exposes the same int64 host arrays as the reference;
+``FlatBdds.device()`` uploads them once (int32 SoA + the level schedules of
+the exact averaging passes) and returns a ``DeviceFlat`` whose methods are
+the reference kernels (k_backward, k_forward, k_mma_forward,
+k_mma_backward, k_min_marginals, k_argmin) on torch CUDA tensors.  Every
+call goes through the C-ABI of libdiscomatch_b200.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import NativeLibraryError
+from .ilp import FlatTable, IlpInstance, _lower_bdds
+
+
+def set_threads(n: int) -> int:
+    """Reference knob (kernels.py:27-32); the device path has no host threads."""
+    return max(1, int(n))
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("device vectors must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class DeviceFlat:
+    """dm_flat handle: topology + schedules resident in HBM."""
+
+    def __init__(self, table: FlatTable, device: torch.device):
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("a CUDA device is required (there is no CPU path)")
+        self.device = torch.device(device)
+        self.table = table
+        lib = _native.load()
+        desc = _native.FlatDesc()
+        desc.num_bdds = table.num_bdds
+        desc.num_layers = table.num_layers
+        desc.num_nodes = table.num_nodes
+        desc.num_positions = len(table.proc_ptr) - 1
+        keep = {}
+        for name in ("bdd_layer_lo", "layer_node_lo", "layer_var", "zero_t", "one_t", "proc_ptr", "proc_layers"):
+            a = np.ascontiguousarray(getattr(table, name), dtype=np.int64)
+            keep[name] = a
+            setattr(desc, name, a.ctypes.data)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(lib.dm_flat_create(ctypes.byref(desc), self.device.index or 0,
+                                             _stream(self.device), ctypes.byref(h)), "dm_flat_create")
+        self._h = h
+        info = _native.FlatInfo()
+        _native.check(lib.dm_flat_get_info(h, ctypes.byref(info)), "dm_flat_get_info")
+        self.info = {k: getattr(info, k) for k, _ in _native.FlatInfo._fields_}
+        self.num_bdds, self.num_layers, self.num_nodes = table.num_bdds, table.num_layers, table.num_nodes
+        self.num_positions = desc.num_positions
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _native.load().dm_flat_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _s(self) -> int:
+        return _stream(self.device)
+
+    # --- reference kernels -------------------------------------------------
+    def k_backward(self, lam, B, bounds):
+        _native.call("dm_k_backward", self._h, _ptr(lam), _ptr(B), _ptr(bounds), self._s())
+
+    def k_backward_trial(self, lam, d, gamma, B, bounds):
+        _native.call("dm_k_backward_trial", self._h, _ptr(lam), _ptr(d), float(gamma), _ptr(B), _ptr(bounds),
+                     self._s())
+
+    def k_forward(self, lam, F, bounds):
+        _native.call("dm_k_forward", self._h, _ptr(lam), _ptr(F), _ptr(bounds), self._s())
+
+    def k_mma_forward(self, lam, F, B, bounds):
+        _native.call("dm_k_mma_forward", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(bounds), self._s())
+
+    def k_mma_backward(self, lam, F, B, bounds):
+        _native.call("dm_k_mma_backward", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(bounds), self._s())
+
+    def k_min_marginals(self, lam, F, B, m0, m1):
+        _native.call("dm_k_min_marginals", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(m0), _ptr(m1), self._s())
+
+    def k_argmin(self, lam, B, bits):
+        _native.call("dm_k_argmin", self._h, _ptr(lam), _ptr(B), _ptr(bits), self._s())
+
+    # --- per-variable vectors ------------------------------------------------
+    def init_duals(self, costs_by_var, lam):
+        _native.call("dm_init_duals", self._h, _ptr(costs_by_var), _ptr(lam), self._s())
+
+    def project_direction(self, d_hat, d):
+        _native.call("dm_project_direction", self._h, _ptr(d_hat), _ptr(d), self._s())
+
+    def lambda_sums(self, lam, out):
+        _native.call("dm_lambda_sums", self._h, _ptr(lam), _ptr(out), self._s())
+
+    def agreement_scores(self, m0, m1, agrees, score, preferred):
+        _native.call("dm_agreement_scores", self._h, _ptr(m0), _ptr(m1), _ptr(agrees), _ptr(score),
+                     _ptr(preferred), self._s())
+
+
+# --- reductions and elementwise vectors (no handle needed) ---------------------
+def dev_sum(x: torch.Tensor, out: torch.Tensor) -> None:
+    """out[0] = np.sum(x) in numpy's pairwise order."""
+    _native.call("dm_sum", _ptr(x), x.numel(), _ptr(out), _stream(x.device))
+
+
+def dev_dot(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
+    """out[0] = np.sum(a * b) (pairwise order)."""
+    _native.call("dm_dot", _ptr(a), _ptr(b), a.numel(), _ptr(out), _stream(a.device))
+
+
+def dev_axpy_dev(x, y, alpha_host, dot_dev, alpha_out=None):
+    _native.call("dm_axpy_dev", _ptr(x), _ptr(y), float(alpha_host), _ptr(dot_dev), _ptr(alpha_out), x.numel(),
+                 _stream(x.device))
+
+
+def dev_scale_dev(x, num_host, den_dev):
+    _native.call("dm_scale_dev", _ptr(x), float(num_host), _ptr(den_dev), x.numel(), _stream(x.device))
+
+
+def dev_lbfgs_up(x, s, alpha_dev, rho_host, dot_dev):
+    _native.call("dm_lbfgs_up", _ptr(x), _ptr(s), _ptr(alpha_dev), float(rho_host), _ptr(dot_dev), x.numel(),
+                 _stream(x.device))
+
+
+def dev_axpy_host(x, gamma, y):
+    _native.call("dm_axpy_host", _ptr(x), float(gamma), _ptr(y), x.numel(), _stream(x.device))
+
+
+def dev_sub(out, a, b):
+    _native.call("dm_sub", _ptr(out), _ptr(a), _ptr(b), out.numel(), _stream(out.device))
+
+
+class FlatBdds:
+    """All diagrams of one instance, flattened (kernels.py:35-92)."""
+
+    def __init__(self, instance):
+        if isinstance(instance, IlpInstance):
+            table = instance.flat
+        elif hasattr(instance, "constraints") and hasattr(instance, "variable_order"):
+            # duck-typed reference instance (prodmatch.ilp.IlpInstance)
+            table = _lower_bdds(instance.costs, instance.constraints, instance.variable_order, 0)
+        else:
+            raise TypeError("FlatBdds needs an IlpInstance")
+        self.table = table
+        for name in ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd", "zero_t", "one_t", "proc_ptr",
+                     "proc_layers"):
+            setattr(self, name, getattr(table, name))
+        self.max_degree = int(table.max_degree)
+        self.max_width = int(table.max_width)
+        self.num_bdds = table.num_bdds
+        self.num_layers = table.num_layers
+        self.num_nodes = table.num_nodes
+        self.constraint_counts = table.constraint_counts
+        self._dev: dict = {}
+
+    def device(self, device=None) -> DeviceFlat:
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        key = str(dev)
+        if key not in self._dev:
+            self._dev[key] = DeviceFlat(self.table, dev)
+        return self._dev[key]

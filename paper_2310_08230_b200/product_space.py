@@ -1,0 +1,358 @@
+"""Product-space ILP (P) for two closed triangle meshes.
+
+The reference ships only the behavioural contract for this module
+("[MODULE] product_space"); there is no
+reference implementation, so this builder defines the instance that both
+the CPU oracle and the B200 path consume.
+
+Conventions:
+  * ext(X) = 3 cyclic rotations of every oriented face, 6 two-vertex
+    triples per undirected edge (aab, aba, baa, abb, bab, bba) and one
+    (v, v, v) per vertex.
+  * P = ext(M) x ext(N) minus both-degenerate pairs, quotiented by the
+    simultaneous cyclic rotation; each class is stored in its
+    lexicographically smallest rotation.
+  * A_boundary: one row per undirected product edge, +1 for a boundary edge
+    that runs from the lexicographically smaller vertex pair to the larger,
+    -1 otherwise; rhs 0.  A^M / A^N: one row per face, sum of the product
+    triangles whose M- (N-) side is a rotation of it equals 1.
+  * Costs: Eq. (2), c_p = sum_v (A^M_{m_v} + A^N_{n_v}) ||F_{m_v} - F_{n_v}||
+    with Meyer mixed vertex areas.
+
+Variable numbering.  The reference's averaging passes are Gauss-Seidel
+sweeps in variable order (kernels.py:194-269), so the numbering fixes the
+dependency DAG the B200 exact-MMA kernel schedules by levels.  Product
+triangles are numbered by a "row colour": every A^M and A^N row receives
+each colour at most once (a Latin-square colouring of the face pairs plus
+one colour per degenerate element), so both projection-row chains advance
+one level per colour and the DAG depth stays close to its lower bound, the
+longest projection row.  ``order="natural"`` keeps the enumeration order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+# product triangle kinds
+TRI_TRI, TRI_EDGE, TRI_VERTEX, EDGE_TRI, VERTEX_TRI = range(5)
+KIND_NAMES = ("tri-tri", "tri-edge", "tri-vertex", "edge-tri", "vertex-tri")
+
+
+@dataclass
+class Mesh:
+    vertices: np.ndarray  # (V, 3) float64
+    faces: np.ndarray  # (T, 3) int64, counterclockwise
+
+    @property
+    def num_vertices(self) -> int:
+        return len(self.vertices)
+
+    @property
+    def num_faces(self) -> int:
+        return len(self.faces)
+
+    def edges(self) -> np.ndarray:
+        """Undirected edges (a < b), sorted lexicographically."""
+        f = self.faces
+        e = np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]])
+        e = np.sort(e, axis=1)
+        return np.unique(e, axis=0)
+
+
+def icosphere(subdivisions: int) -> Mesh:
+    """Unit icosahedron refined ``subdivisions`` times (1-to-4 split)."""
+    t = (1.0 + 5.0 ** 0.5) / 2.0
+    v = np.array(
+        [[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t],
+         [0, -1, -t], [0, 1, -t], [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]],
+        dtype=np.float64,
+    )
+    f = np.array(
+        [[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4],
+         [11, 10, 2], [10, 7, 6], [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8],
+         [3, 8, 9], [4, 9, 5], [2, 4, 11], [6, 2, 10], [8, 6, 7], [9, 8, 1]],
+        dtype=np.int64,
+    )
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    verts = [tuple(x) for x in v]
+    for _ in range(subdivisions):
+        mid = {}
+        new_faces = []
+
+        def midpoint(a, b):
+            key = (min(a, b), max(a, b))
+            if key not in mid:
+                p = (np.asarray(verts[a]) + np.asarray(verts[b])) / 2.0
+                p /= np.linalg.norm(p)
+                mid[key] = len(verts)
+                verts.append(tuple(p))
+            return mid[key]
+
+        for a, b, c in f.tolist():
+            ab, bc, ca = midpoint(a, b), midpoint(b, c), midpoint(c, a)
+            new_faces += [[a, ab, ca], [b, bc, ab], [c, ca, bc], [ab, bc, ca]]
+        f = np.asarray(new_faces, dtype=np.int64)
+    return Mesh(np.asarray(verts, dtype=np.float64), f)
+
+
+def deform(mesh: Mesh, seed: int, amplitude: float = 0.25, modes: int = 6) -> Mesh:
+    """Smooth random non-rigid deformation (sum of low-frequency bumps)."""
+    rng = np.random.default_rng(seed)
+    x = mesh.vertices
+    disp = np.zeros_like(x)
+    for _ in range(modes):
+        k = rng.standard_normal(3) * 1.5
+        phase = rng.uniform(0, 2 * np.pi)
+        direction = rng.standard_normal(3)
+        disp += np.sin(x @ k + phase)[:, None] * direction[None, :]
+    disp *= amplitude / max(1e-12, np.abs(disp).max())
+    return Mesh(x + disp, mesh.faces.copy())
+
+
+def mixed_vertex_areas(mesh: Mesh) -> np.ndarray:
+    """Meyer et al. mixed areas: Voronoi cotangent areas on
+    non-obtuse triangles, area/2 at an obtuse corner and area/4 elsewhere."""
+    x = mesh.vertices
+    f = mesh.faces
+    out = np.zeros(len(x))
+    p = [x[f[:, k]] for k in range(3)]
+    cross = np.cross(p[1] - p[0], p[2] - p[0])
+    area = 0.5 * np.linalg.norm(cross, axis=1)
+    if (area <= 0).any():
+        raise ValueError("degenerate triangle")
+    for k in range(3):
+        a, b, c = p[k], p[(k + 1) % 3], p[(k + 2) % 3]
+        # angle at b and c -> cot; Voronoi share of vertex a
+        ab, ac = b - a, c - a
+        ba, bc = a - b, c - b
+        ca, cb = a - c, b - c
+        cot_b = np.einsum("ij,ij->i", ba, bc) / np.linalg.norm(np.cross(ba, bc), axis=1)
+        cot_c = np.einsum("ij,ij->i", ca, cb) / np.linalg.norm(np.cross(ca, cb), axis=1)
+        vor = (np.einsum("ij,ij->i", ac, ac) * cot_b + np.einsum("ij,ij->i", ab, ab) * cot_c) / 8.0
+        dot_a = np.einsum("ij,ij->i", ab, ac)
+        dot_b = np.einsum("ij,ij->i", ba, bc)
+        dot_c = np.einsum("ij,ij->i", ca, cb)
+        obtuse_any = (dot_a < 0) | (dot_b < 0) | (dot_c < 0)
+        share = np.where(~obtuse_any, vor, np.where(dot_a < 0, area / 2.0, area / 4.0))
+        np.add.at(out, f[:, k], share)
+    return out
+
+
+def random_features(n: int, dim: int, seed: int) -> np.ndarray:
+    return np.random.default_rng(seed).standard_normal((n, dim))
+
+
+def smooth_features(mesh_ref: Mesh, dim: int, seed: int, noise: float = 0.0,
+                    noise_seed: int = 0) -> np.ndarray:
+    """Random Fourier features of reference positions (correspondence-aware
+    synthetic descriptors), plus optional per-vertex noise."""
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal((3, dim)) * 2.0
+    b = rng.uniform(0, 2 * np.pi, dim)
+    feats = np.cos(mesh_ref.vertices @ w + b)
+    if noise:
+        feats = feats + noise * np.random.default_rng(noise_seed).standard_normal(feats.shape)
+    return feats
+
+
+def _edge_triples(edges: np.ndarray) -> np.ndarray:
+    a, b = edges[:, 0], edges[:, 1]
+    pats = [(a, a, b), (a, b, a), (b, a, a), (a, b, b), (b, a, b), (b, b, a)]
+    return np.stack([np.stack(p, axis=1) for p in pats], axis=1).reshape(-1, 3)
+
+
+@dataclass
+class ProductSpace:
+    m: np.ndarray  # (P, 3) M vertex of each corner (canonical rotation)
+    n: np.ndarray  # (P, 3) N vertex of each corner
+    kind: np.ndarray  # (P,) int8 kind
+    face_m: np.ndarray  # (P,) M face id or -1
+    face_n: np.ndarray  # (P,) N face id or -1
+    costs: np.ndarray  # (P,) float64
+    row_ptr: np.ndarray  # CSR over rows: boundary rows, then A^M, then A^N
+    row_var: np.ndarray
+    row_coef: np.ndarray
+    row_rhs: np.ndarray
+    num_boundary_rows: int
+    num_vm: int
+    num_vn: int
+
+    @property
+    def num_variables(self) -> int:
+        return len(self.costs)
+
+    @property
+    def num_rows(self) -> int:
+        return len(self.row_rhs)
+
+    def rows(self):
+        """Rows as (variables, coefficients, rhs) tuples (reference layout)."""
+        out = []
+        for r in range(self.num_rows):
+            lo, hi = self.row_ptr[r], self.row_ptr[r + 1]
+            out.append((self.row_var[lo:hi], self.row_coef[lo:hi], int(self.row_rhs[r])))
+        return out
+
+
+def _canonical_rotation(m, n):
+    """Rotate each corner triple to its lexicographically smallest rotation."""
+    P = len(m)
+    keys = []
+    for k in range(3):
+        idx = [(k + j) % 3 for j in range(3)]
+        keys.append(np.stack([m[:, idx[0]], n[:, idx[0]], m[:, idx[1]], n[:, idx[1]],
+                              m[:, idx[2]], n[:, idx[2]]], axis=1))
+    best = np.zeros(P, dtype=np.int64)
+    cur = keys[0].copy()
+    rows = np.arange(P)
+    for k in (1, 2):
+        cand = keys[k]
+        diff = cand != cur
+        first = np.argmax(diff, axis=1)
+        less = diff.any(axis=1) & (cand[rows, first] < cur[rows, first])
+        best = np.where(less, k, best)
+        cur = np.where(less[:, None], cand, cur)
+    rot = (np.arange(3)[None, :] + best[:, None]) % 3
+    return np.take_along_axis(m, rot, 1), np.take_along_axis(n, rot, 1)
+
+
+def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray,
+                        order: str = "colour", allowed: np.ndarray | None = None) -> ProductSpace:
+    """Enumerate P, order the variables, assemble rows and Eq. (2) costs.
+
+    ``allowed`` (optional, bool (|V_M|, |V_N|)) keeps only product triangles
+    whose three vertex pairs are all allowed (k-NN / coarse-to-fine pruning,
+    SPEC.md:489-500).
+    """
+    if feat_m.shape[1] != feat_n.shape[1]:
+        raise ValueError("feature dimension mismatch")
+    FM, FN = M.faces, N.faces
+    TM, TN = len(FM), len(FN)
+    EM, EN = M.edges(), N.edges()
+    E6M, E6N = _edge_triples(EM), _edge_triples(EN)
+    VM, VN = M.num_vertices, N.num_vertices
+    T = max(TM, TN)
+    rotN = np.stack([FN[:, [(k + s) % 3 for k in range(3)]] for s in range(3)], 1)  # (TN,3,3)
+
+    parts = []  # (m, n, kind, face_m, face_n, colour)
+    # tri-tri: M face f in stored rotation, N face g rotated by s
+    f, g, s = np.meshgrid(np.arange(TM), np.arange(TN), np.arange(3), indexing="ij")
+    f, g, s = f.ravel(), g.ravel(), s.ravel()
+    parts.append((FM[f], rotN[g, s], TRI_TRI, f, g, 3 * ((f + g) % T) + s))
+    # tri-edge / tri-vertex: M face, N degenerate element
+    f, t = np.meshgrid(np.arange(TM), np.arange(len(E6N)), indexing="ij")
+    f, t = f.ravel(), t.ravel()
+    parts.append((FM[f], E6N[t], TRI_EDGE, f, np.full_like(f, -1), 3 * T + t))
+    f, v = np.meshgrid(np.arange(TM), np.arange(VN), indexing="ij")
+    f, v = f.ravel(), v.ravel()
+    parts.append((FM[f], np.stack([v, v, v], 1), TRI_VERTEX, f, np.full_like(f, -1),
+                  3 * T + len(E6N) + v))
+    # edge-tri / vertex-tri: M degenerate element, N face g in stored rotation
+    t, g = np.meshgrid(np.arange(len(E6M)), np.arange(TN), indexing="ij")
+    t, g = t.ravel(), g.ravel()
+    parts.append((E6M[t], FN[g], EDGE_TRI, np.full_like(g, -1), g, 3 * T + t))
+    v, g = np.meshgrid(np.arange(VM), np.arange(TN), indexing="ij")
+    v, g = v.ravel(), g.ravel()
+    parts.append((np.stack([v, v, v], 1), FN[g], VERTEX_TRI, np.full_like(g, -1), g,
+                  3 * T + len(E6M) + v))
+
+    m = np.concatenate([p[0] for p in parts]).astype(np.int64)
+    n = np.concatenate([p[1] for p in parts]).astype(np.int64)
+    kind = np.concatenate([np.full(len(p[0]), p[2], np.int8) for p in parts])
+    face_m = np.concatenate([p[3] for p in parts]).astype(np.int64)
+    face_n = np.concatenate([p[4] for p in parts]).astype(np.int64)
+    colour = np.concatenate([p[5] for p in parts]).astype(np.int64)
+
+    if allowed is not None:
+        keep = allowed[m, n].all(axis=1)
+        m, n, kind, face_m, face_n, colour = (a[keep] for a in (m, n, kind, face_m, face_n, colour))
+
+    if order == "colour":
+        perm = np.lexsort((np.arange(len(m)), colour))
+    elif order == "natural":
+        perm = np.arange(len(m))
+    else:
+        raise ValueError(f"unknown order {order!r}")
+    m, n, kind, face_m, face_n = m[perm], n[perm], kind[perm], face_m[perm], face_n[perm]
+    m, n = _canonical_rotation(m, n)
+    P = len(m)
+
+    # Eq. (2) costs, summed corner by corner on the canonical rotation
+    area_m, area_n = mixed_vertex_areas(M), mixed_vertex_areas(N)
+    costs = np.zeros(P)
+    for k in range(3):
+        dist = np.linalg.norm(feat_m[m[:, k]] - feat_n[n[:, k]], axis=1)
+        costs = costs + (area_m[m[:, k]] + area_n[n[:, k]]) * dist
+
+    # boundary rows: group the 3P oriented product-edge incidences
+    pid = m * VN + n  # vertex-pair ids
+    src = pid.ravel()
+    dst = pid[:, [1, 2, 0]].ravel()
+    var = np.repeat(np.arange(P, dtype=np.int64), 3)
+    lo_, hi_ = np.minimum(src, dst), np.maximum(src, dst)
+    sign = np.where(src < dst, 1, -1).astype(np.int64)
+    key = lo_ * (VM * VN) + hi_
+    o = np.lexsort((var, key))
+    key, var_s, sign_s = key[o], var[o], sign[o]
+    starts = np.flatnonzero(np.concatenate([[True], key[1:] != key[:-1]]))
+    nb = len(starts)
+    b_ptr = np.concatenate([starts, [len(key)]]).astype(np.int64)
+
+    # projection rows
+    def proj(face, nf):
+        sel = np.flatnonzero(face >= 0)
+        oo = np.lexsort((sel, face[sel]))
+        sel = sel[oo]
+        cnt = np.bincount(face[sel], minlength=nf)
+        return sel, np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+
+    am_var, am_ptr = proj(face_m, TM)
+    an_var, an_ptr = proj(face_n, TN)
+    row_var = np.concatenate([var_s, am_var, an_var]).astype(np.int64)
+    row_coef = np.concatenate([sign_s, np.ones(len(am_var) + len(an_var), np.int64)])
+    row_ptr = np.concatenate([b_ptr[:-1], am_ptr[:-1] + len(var_s),
+                              an_ptr + len(var_s) + len(am_var)]).astype(np.int64)
+    row_rhs = np.concatenate([np.zeros(nb, np.int64), np.ones(TM + TN, np.int64)])
+    return ProductSpace(m, n, kind, face_m, face_n, costs, row_ptr, row_var, row_coef, row_rhs,
+                        nb, VM, VN)
+
+
+def verify_solution(ps: ProductSpace, x: np.ndarray) -> list[int]:
+    """Exact integer check of all rows; returns violated rows."""
+    x = np.asarray(x, dtype=np.int64)
+    lhs = np.add.reduceat(ps.row_coef * x[ps.row_var], ps.row_ptr[:-1]) if ps.num_rows else []
+    empty = ps.row_ptr[1:] == ps.row_ptr[:-1]
+    lhs = np.where(empty, 0, lhs)
+    return np.flatnonzero(lhs != ps.row_rhs).tolist()
+
+
+def synthetic_pair(config: str, seed: int = 0):
+    """Mesh pairs and descriptors of the BASELINE configs.
+
+    'tetra' / 'icosa'  — SPEC acceptance anchors (|P| = 368, ratio ~22);
+    'c1'  — icosphere subdiv-1 pair (80 x 80), random 16-D descriptors;
+    'c2'  — deformed icosphere subdiv-2 pair (320 x 320), smooth descriptors.
+    """
+    if config == "tetra":
+        v = np.array([[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]], np.float64)
+        f = np.array([[0, 1, 2], [0, 3, 1], [0, 2, 3], [1, 3, 2]], np.int64)
+        M = N = Mesh(v, f)
+        fm, fn = random_features(4, 8, seed), random_features(4, 8, seed + 1)
+    elif config == "icosa":
+        M = N = icosphere(0)
+        fm, fn = random_features(12, 8, seed), random_features(12, 8, seed + 1)
+    elif config == "c1":
+        M = icosphere(1)
+        N = icosphere(1)
+        fm, fn = random_features(M.num_vertices, 16, seed), random_features(N.num_vertices, 16, seed + 1)
+    elif config == "c2":
+        base = icosphere(2)
+        M = deform(base, seed * 2 + 1)
+        N = deform(base, seed * 2 + 2)
+        fm = smooth_features(base, 16, seed, noise=0.3, noise_seed=seed * 2 + 1)
+        fn = smooth_features(base, 16, seed, noise=0.3, noise_seed=seed * 2 + 2)
+    else:
+        raise ValueError(f"unknown config {config!r}")
+    return M, N, fm, fn
