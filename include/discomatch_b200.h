@@ -112,6 +112,14 @@ typedef struct {
 
 int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out);
 int dm_flat_get_info(const dm_flat *flat, dm_flat_info *info);
+/* Synchronises the stream and reports whether an exact pass since the last
+ * call was aborted by its watchdog (DM_ERR_CUDA) — resets the word. */
+int dm_flat_status(dm_flat *flat, void *stream);
+/* Launch shape of the exact passes: block size (multiple of 32, <= 256),
+ * resident blocks per SM (<= 0: as many as fit) and the back-off between
+ * unsuccessful polls.  Defaults come from DM_MMA_THREADS /
+ * DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS at creation. */
+int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns);
 void dm_flat_destroy(dm_flat *flat);
 
 /* --- sweep kernels: one per reference kernel ---------------------------- */

@@ -108,6 +108,8 @@ class OracleInstance:
         return pos
 
     def counts(self) -> np.ndarray:
+        if self.bdds is None:  # built from a flat table (see from_flat_table)
+            return self._counts
         cnt = np.zeros(self.num_variables, np.int64)
         for v, _, _ in self.bdds:
             cnt[v] += 1
@@ -207,3 +209,16 @@ def flatten(inst: OracleInstance) -> OracleFlat:
         bdd_layer_lo, layer_node_lo, layer_var, layer_bdd, zero_t, one_t, proc_ptr,
         proc_layers, int(cnt.max()) if len(cnt) else 0,
     )
+
+
+def from_flat_table(costs, order, counts, arrays: dict):
+    """Wrap an already-lowered flat table (int64 arrays keyed like FlatBdds)
+    so the oracle kernels can run on it; used for full-size checks where
+    the Python diagram builder would be slow.  Parity of the lowering itself
+    is established separately against the reference's golden hashes."""
+    inst = OracleInstance(np.asarray(costs, np.float64), None, np.asarray(order, np.int64))
+    inst._counts = np.asarray(counts, np.int64)
+    a = {k: np.ascontiguousarray(arrays[k], dtype=np.int64) for k in (
+        "bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd", "zero_t", "one_t", "proc_ptr", "proc_layers")}
+    deg = int(np.diff(a["proc_ptr"]).max()) if len(a["proc_ptr"]) > 1 else 0
+    return inst, OracleFlat(max_degree=deg, **a)

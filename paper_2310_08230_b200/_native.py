@@ -56,6 +56,8 @@ SIGNATURES = {
     "dm_instance_free": ([_P], None),
     "dm_flat_create": ([ctypes.POINTER(FlatDesc), _INT, _P, ctypes.POINTER(_P)], _INT),
     "dm_flat_get_info": ([_P, ctypes.POINTER(FlatInfo)], _INT),
+    "dm_flat_status": ([_P, _P], _INT),
+    "dm_flat_set_mma_config": ([_P, _INT, _INT, _INT], _INT),
     "dm_flat_destroy": ([_P], None),
     "dm_k_backward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_backward_trial": ([_P, _P, _P, _D, _P, _P, _P], _INT),
@@ -117,5 +119,17 @@ def check(rc: int, what: str = "") -> None:
     raise ProdmatchError(msg)
 
 
+# kernels each entry point launches (for the bench's gpu_launches claim)
+LAUNCHES = {"dm_k_mma_forward": 3, "dm_k_mma_backward": 2, "dm_sum": 2, "dm_dot": 2}
+KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_mma_forward",
+                  "dm_k_mma_backward", "dm_k_min_marginals", "dm_k_argmin", "dm_init_duals",
+                  "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
+                  "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub"}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     check(getattr(load(), name)(*args), name)
+    if name in KERNEL_ENTRIES:
+        launch_count += LAUNCHES.get(name, 1)

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <cstdio>
 #include <map>
@@ -50,6 +51,15 @@ __device__ __forceinline__ void st_relaxed(double *p, double x) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(x))
                  : "memory");
 }
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// A lane waits at most this long for its inputs; past it the pass aborts
+// (status word set, every warp drains) instead of hanging the device.
+constexpr uint64_t kWaitLimitNs = 4000000000ull;
+
 __device__ __forceinline__ bool is_sentinel(double x) {
     return (unsigned long long)__double_as_longlong(x) == kSentinel;
 }
@@ -196,6 +206,7 @@ __global__ void lambda_sums_kernel(int32_t P, const int32_t *__restrict__ proc_p
                                    double *__restrict__ out) {
     const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
+    if (pos_var[p] < 0) return;  // unconstrained: the host fills its cost
     double s = 0.0;
     for (int32_t t = proc_ptr[p]; t < proc_ptr[p + 1]; ++t) s = __dadd_rn(s, lam[proc_layers[t]]);
     out[pos_var[p]] = s;
@@ -207,7 +218,7 @@ __global__ void agreement_kernel(int32_t P, const int32_t *__restrict__ proc_ptr
                                  int8_t *__restrict__ agrees, double *__restrict__ score,
                                  int8_t *__restrict__ preferred) {
     const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
+    if (p >= P || pos_var[p] < 0) return;  // unconstrained: host defaults (no vote)
     double vmax = -2.0, vmin = 2.0, total = 0.0;
     const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
     for (int32_t t = lo; t < hi; ++t) {
@@ -339,16 +350,35 @@ struct MmaArgs {
     const int32_t *task_layer, *task_meta;
     const int32_t *lnl, *zero_t, *one_t, *layer_bdd;
     double *lam, *F, *B, *bounds;
+    int *status;        // 0 ok, 1 watchdog fired
+    unsigned sleep_ns;  // back-off between unsuccessful polls
 };
+
+// true when this warp must abandon the pass (own timeout or another's)
+__device__ __forceinline__ bool watchdog(const MmaArgs &a, uint64_t t_start, unsigned &spins) {
+    if ((++spins & 63u) != 0) return false;
+    if (*(volatile int *)a.status) return true;
+    if (global_ns() - t_start > kWaitLimitNs) {
+        atomicExch(a.status, 1);
+        return true;
+    }
+    return false;
+}
+
+// Lanes [gbase, gbase+gcnt) hold the copies of one variable in copy order.
+__device__ __forceinline__ unsigned group_mask(int32_t meta) {
+    const int gbase = meta & 0xff, gcnt = (meta >> 8) & 0xff;
+    return (gcnt >= 32 ? 0xffffffffu : ((1u << gcnt) - 1u)) << gbase;
+}
 
 // Sum of the finite min-marginal differences of the lane's variable, in copy
 // order (kernels.py:200-233), then the lane's new dual (kernels.py:234-240).
-__device__ __forceinline__ double average_in_group(bool act, int32_t meta, double m0, double m1,
-                                                   double lam_l) {
-    const bool fin = act && m0 != DM_INF && m1 != DM_INF;
+// Executed by the whole warp; only lanes with `go` use the result.
+__device__ __forceinline__ double average_in_group(bool go, int32_t meta, double m0, double m1, double lam_l) {
+    const bool fin = go && m0 != DM_INF && m1 != DM_INF;
     const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
     const int gbase = meta & 0xff, gcnt = (meta >> 8) & 0xff;
-    const int maxc = __reduce_max_sync(kFull, act ? gcnt : 0);
+    const int maxc = __reduce_max_sync(kFull, go ? gcnt : 0);
     double fsum = 0.0;
     int fcnt = 0;
     for (int k = 0; k < maxc; ++k) {
@@ -366,6 +396,32 @@ __device__ __forceinline__ double average_in_group(bool act, int32_t meta, doubl
     return lam_l;
 }
 
+// Min-marginals of one layer from its forward distances f and the distances
+// to TRUE of its arc targets (kernels.py:205-230).
+template <int W>
+__device__ __forceinline__ void layer_marginals(int32_t w, const double (&f)[W], const int32_t (&z)[W],
+                                                const int32_t (&o)[W], const double (&bz)[W],
+                                                const double (&bo)[W], double lam_l, double &m0, double &m1) {
+    m0 = DM_INF;
+    m1 = DM_INF;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (i < w && f[i] != DM_INF) {
+            const double fv = f[i];
+            const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
+            if (c0 < m0) m0 = c0;
+            const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
+                                                : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
+            if (c1 < m1) m1 = c1;
+        }
+    }
+}
+
+// Forward pass.  Warp w takes tasks w, w+W, ... (level order).  Inside a task
+// each variable (lane group) proceeds as soon as its own inputs are
+// published, independently of the other groups in the warp.  A lane first
+// polls a single probe word — the last forward distance its producer writes
+// — and only then reads the whole layer.
 template <int W>
 __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
@@ -374,13 +430,17 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         const int32_t l = a.task_layer[task * 32 + lane];
         const int32_t meta = a.task_meta[task * 32 + lane];
         const bool act = l >= 0;
-        int32_t nlo = 0, w = 0;
+        int32_t nlo = 0, w = 0, n0 = 0, wn = 0;
         double lam_l = 0.0;
         int32_t z[W], o[W];
         double bz[W], bo[W], f[W];
         if (act) {
             nlo = a.lnl[l];
             w = a.lnl[l + 1] - nlo;
+            if (!(meta & (1 << 17))) {
+                n0 = a.lnl[l + 1];
+                wn = a.lnl[l + 2] - n0;
+            }
             lam_l = a.lam[l];
         }
         // static inputs: topology and the backward distances (valid all pass)
@@ -393,66 +453,78 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
                 bo[i] = o[i] >= 0 ? a.B[o[i]] : 0.0;
             }
         }
-        // wait until the producer of this layer's forward distances published them
-        bool ready;
-        do {
-            ready = true;
+        const unsigned gmask = act ? group_mask(meta) : 0u;
+        bool have = !act;
+        unsigned pending = __ballot_sync(kFull, act);
+        unsigned spins = 0;
+        const uint64_t t_wait = global_ns();
+        while (pending) {
+            if (!have && ((pending >> lane) & 1u)) {
+                if (!is_sentinel(ld_relaxed(a.F + nlo + w - 1))) {
+                    bool ok = true;
 #pragma unroll
-            for (int i = 0; i < W; ++i)
-                if (i < w) {
-                    f[i] = ld_relaxed(a.F + nlo + i);
-                    ready &= !is_sentinel(f[i]);
+                    for (int i = 0; i < W; ++i)
+                        if (i < w) {
+                            f[i] = ld_relaxed(a.F + nlo + i);
+                            ok &= !is_sentinel(f[i]);
+                        }
+                    have = ok;
                 }
-        } while (!__all_sync(kFull, ready));
-        // min-marginals (kernels.py:205-230)
-        double m0 = DM_INF, m1 = DM_INF;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w && f[i] != DM_INF) {
-                const double fv = f[i];
-                const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
-                if (c0 < m0) m0 = c0;
-                const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
-                                                    : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
-                if (c1 < m1) m1 = c1;
             }
-        }
-        lam_l = average_in_group(act, meta, m0, m1, lam_l);
-        if (!act) continue;
-        a.lam[l] = lam_l;
-        // propagate to the next layer (kernels.py:241-269), gather form with the
-        // reference's scatter order: first strict minimum over (v asc, zero, one)
-        if (!(meta & (1 << 17))) {
-            const int32_t n0 = a.lnl[l + 1];
-            const int32_t wn = a.lnl[l + 2] - n0;
-            for (int32_t u = 0; u < wn; ++u) {
-                double best = DM_INF;
-                const int32_t tgt = n0 + u;
+            const unsigned hm = __ballot_sync(kFull, have);
+            const bool go = act && ((pending >> lane) & 1u) && ((hm & gmask) == gmask);
+            const unsigned gom = __ballot_sync(kFull, go);
+            if (gom == 0u) {
+                if (watchdog(a, t_wait, spins)) {
+                    __syncwarp();
+                    return;
+                }
+                if (a.sleep_ns) __nanosleep(a.sleep_ns);
+                continue;
+            }
+            pending &= ~gom;
+            double m0, m1;
+            layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
+            const double lam_new = average_in_group(go, meta, m0, m1, lam_l);
+            if (!go) continue;
+            lam_l = lam_new;
+            a.lam[l] = lam_l;
+            // propagate to the next layer (kernels.py:241-269), gather form with
+            // the reference's scatter order: first strict minimum over
+            // (v ascending, zero-arc, one-arc)
+            if (!(meta & (1 << 17))) {
+                for (int32_t u = 0; u < wn; ++u) {
+                    double best = DM_INF;
+                    const int32_t tgt = n0 + u;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        if (i < w && f[i] != DM_INF) {
+                            if (z[i] == tgt && f[i] < best) best = f[i];
+                            const double c = __dadd_rn(f[i], lam_l);
+                            if (o[i] == tgt && c < best) best = c;
+                        }
+                    }
+                    st_relaxed(a.F + tgt, best);
+                }
+            } else {
+                double tb = DM_INF;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
                     if (i < w && f[i] != DM_INF) {
-                        if (z[i] == tgt && f[i] < best) best = f[i];
+                        if (z[i] == dm::kTrue && f[i] < tb) tb = f[i];
                         const double c = __dadd_rn(f[i], lam_l);
-                        if (o[i] == tgt && c < best) best = c;
+                        if (o[i] == dm::kTrue && c < tb) tb = c;
                     }
                 }
-                st_relaxed(a.F + tgt, best);
+                a.bounds[a.layer_bdd[l]] = tb;
             }
-        } else {
-            double tb = DM_INF;
-#pragma unroll
-            for (int i = 0; i < W; ++i) {
-                if (i < w && f[i] != DM_INF) {
-                    if (z[i] == dm::kTrue && f[i] < tb) tb = f[i];
-                    const double c = __dadd_rn(f[i], lam_l);
-                    if (o[i] == dm::kTrue && c < tb) tb = c;
-                }
-            }
-            a.bounds[a.layer_bdd[l]] = tb;
         }
     }
 }
 
+// Backward pass: mirror image; a lane waits for the distances to TRUE of the
+// next layer (probe = that layer's last node, written last by its producer)
+// and rebuilds its own layer's distances with the updated dual.
 template <int W>
 __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
@@ -461,13 +533,15 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
         const int32_t l = a.task_layer[task * 32 + lane];
         const int32_t meta = a.task_meta[task * 32 + lane];
         const bool act = l >= 0;
-        int32_t nlo = 0, w = 0;
+        const bool last = meta & (1 << 17);
+        int32_t nlo = 0, w = 0, probe = -1;
         double lam_l = 0.0;
         int32_t z[W], o[W];
         double bz[W], bo[W], f[W];
         if (act) {
             nlo = a.lnl[l];
             w = a.lnl[l + 1] - nlo;
+            if (!last) probe = a.lnl[l + 2] - 1;
             lam_l = a.lam[l];
         }
 #pragma unroll
@@ -476,52 +550,66 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
                 z[i] = a.zero_t[nlo + i];
                 o[i] = a.one_t[nlo + i];
                 f[i] = a.F[nlo + i];
+                bz[i] = 0.0;
+                bo[i] = 0.0;
             }
         }
-        bool ready;
-        do {
-            ready = true;
+        const unsigned gmask = act ? group_mask(meta) : 0u;
+        bool have = !act || last;
+        unsigned pending = __ballot_sync(kFull, act);
+        unsigned spins = 0;
+        const uint64_t t_wait = global_ns();
+        while (pending) {
+            if (!have && ((pending >> lane) & 1u)) {
+                if (!is_sentinel(ld_relaxed(a.B + probe))) {
+                    bool ok = true;
 #pragma unroll
-            for (int i = 0; i < W; ++i)
-                if (i < w) {
-                    if (z[i] >= 0) {
-                        bz[i] = ld_relaxed(a.B + z[i]);
-                        ready &= !is_sentinel(bz[i]);
-                    }
-                    if (o[i] >= 0) {
-                        bo[i] = ld_relaxed(a.B + o[i]);
-                        ready &= !is_sentinel(bo[i]);
-                    }
+                    for (int i = 0; i < W; ++i)
+                        if (i < w) {
+                            if (z[i] >= 0) {
+                                bz[i] = ld_relaxed(a.B + z[i]);
+                                ok &= !is_sentinel(bz[i]);
+                            }
+                            if (o[i] >= 0) {
+                                bo[i] = ld_relaxed(a.B + o[i]);
+                                ok &= !is_sentinel(bo[i]);
+                            }
+                        }
+                    have = ok;
                 }
-        } while (!__all_sync(kFull, ready));
-        double m0 = DM_INF, m1 = DM_INF;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w && f[i] != DM_INF) {
-                const double fv = f[i];
-                const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
-                if (c0 < m0) m0 = c0;
-                const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
-                                                    : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
-                if (c1 < m1) m1 = c1;
             }
-        }
-        lam_l = average_in_group(act, meta, m0, m1, lam_l);
-        if (!act) continue;
-        a.lam[l] = lam_l;
-        // rebuild this layer's distances to TRUE with the new dual (kernels.py:340-358)
-        double first = 0.0;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w) {
-                const double c0 = z[i] == dm::kTrue ? 0.0 : (z[i] == dm::kFalse ? DM_INF : bz[i]);
-                const double c1 = o[i] == dm::kTrue ? lam_l : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo[i]));
-                const double bv = (c0 <= c1) ? c0 : c1;
-                st_relaxed(a.B + nlo + i, bv);
-                if (i == 0) first = bv;
+            const unsigned hm = __ballot_sync(kFull, have);
+            const bool go = act && ((pending >> lane) & 1u) && ((hm & gmask) == gmask);
+            const unsigned gom = __ballot_sync(kFull, go);
+            if (gom == 0u) {
+                if (watchdog(a, t_wait, spins)) {
+                    __syncwarp();
+                    return;
+                }
+                if (a.sleep_ns) __nanosleep(a.sleep_ns);
+                continue;
             }
+            pending &= ~gom;
+            double m0, m1;
+            layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
+            const double lam_new = average_in_group(go, meta, m0, m1, lam_l);
+            if (!go) continue;
+            lam_l = lam_new;
+            a.lam[l] = lam_l;
+            // rebuild this layer's distances to TRUE (kernels.py:340-358)
+            double first = 0.0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                if (i < w) {
+                    const double c0 = z[i] == dm::kTrue ? 0.0 : (z[i] == dm::kFalse ? DM_INF : bz[i]);
+                    const double c1 = o[i] == dm::kTrue ? lam_l : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo[i]));
+                    const double bv = (c0 <= c1) ? c0 : c1;
+                    st_relaxed(a.B + nlo + i, bv);
+                    if (i == 0) first = bv;
+                }
+            }
+            if (meta & (1 << 16)) a.bounds[a.layer_bdd[l]] = first;  // kernels.py:359-361
         }
-        if (meta & (1 << 16)) a.bounds[a.layer_bdd[l]] = first;  // kernels.py:359-361
     }
 }
 
@@ -547,7 +635,10 @@ struct dm_flat {
     int32_t *fw_layer = nullptr, *fw_meta = nullptr, *bw_layer = nullptr, *bw_meta = nullptr;
     int64_t fw_tasks = 0, bw_tasks = 0, fw_depth = 0, bw_depth = 0;
     int64_t max_width = 0, max_degree = 0;
+    int *status = nullptr;  // device watchdog word of the exact passes
     int mma_w = 8;
+    int mma_threads = 256, mma_blocks_per_sm = 0;
+    unsigned mma_sleep_ns = 0;
     int mma_grid_fw = 0, mma_grid_bw = 0;
     int64_t bytes = 0;
     std::vector<void *> allocs;
@@ -627,23 +718,52 @@ int launch_mma(const dm_flat *f, bool forward, MmaArgs &args, cudaStream_t s) {
     void *params[] = {&args};
     const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
     const int grid = forward ? f->mma_grid_fw : f->mma_grid_bw;
-    DM_CUDA(cudaLaunchCooperativeKernel(fn, grid, 256, params, 0, s));
+    DM_CUDA(cudaLaunchCooperativeKernel(fn, grid, f->mma_threads, params, 0, s));
     return DM_OK;
 }
 
+// Persistent grid: min(requested, resident) blocks per SM x SM count.
 template <int W>
-int mma_grid_for(bool forward, int *grid) {
+int mma_grid_for(bool forward, int threads, int want_per_sm, int *grid) {
     int dev, sms, per;
     DM_CUDA(cudaGetDevice(&dev));
     DM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
-    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0));
+    DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0));
     if (per < 1) {
         dm::set_error("exact averaging kernel cannot be resident");
         return DM_ERR_CUDA;
     }
+    if (want_per_sm > 0) per = std::min(per, want_per_sm);
     *grid = sms * per;
     return DM_OK;
+}
+
+}  // namespace
+
+static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sleep_ns) {
+    if (threads < 32 || threads > 256 || threads % 32) {
+        dm::set_error("exact-pass block size must be a multiple of 32 in [32, 256]");
+        return DM_ERR_INVALID;
+    }
+    int rc;
+    switch (f->mma_w) {
+        case 8: rc = mma_grid_for<8>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<8>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
+        case 16: rc = mma_grid_for<16>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<16>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
+        default: rc = mma_grid_for<32>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<32>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
+    }
+    if (rc) return rc;
+    f->mma_threads = threads;
+    f->mma_blocks_per_sm = blocks_per_sm;
+    f->mma_sleep_ns = sleep_ns;
+    return DM_OK;
+}
+
+namespace {
+
+int env_int(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
 }
 
 int check_stream_error(const char *what) {
@@ -763,12 +883,10 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = up(&f->fw_meta, std::move(fw.task_meta)))) return rc;
     if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
     if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
+    if ((rc = up(&f->status, std::vector<int32_t>(1, 0)))) return rc;
     f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
-    switch (f->mma_w) {
-        case 8: rc = mma_grid_for<8>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<8>(false, &f->mma_grid_bw); break;
-        case 16: rc = mma_grid_for<16>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<16>(false, &f->mma_grid_bw); break;
-        default: rc = mma_grid_for<32>(true, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<32>(false, &f->mma_grid_bw); break;
-    }
+    rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 2),
+                       (unsigned)env_int("DM_MMA_SLEEP_NS", 0));
     if (rc) return rc;
     DevPlan *dummy;
     if ((rc = get_plan(nb, &dummy))) return rc;
@@ -788,10 +906,38 @@ int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
     info->fw_tasks = f->fw_tasks;
     info->bw_tasks = f->bw_tasks;
     info->mma_grid = f->mma_grid_fw;
-    info->mma_block = 256;
+    info->mma_block = f->mma_threads;
     info->max_width = f->max_width;
     info->max_degree = f->max_degree;
     info->device_bytes = f->bytes;
+    return DM_OK;
+}
+
+#define DM_CHECK_FLAT(f)                        \
+    if (!(f)) {                                 \
+        dm::set_error("null flat handle");      \
+        return DM_ERR_INVALID;                  \
+    }
+
+int dm_flat_set_mma_config(dm_flat *f, int threads, int blocks_per_sm, int sleep_ns) {
+    if (!f) {
+        dm::set_error("null flat handle");
+        return DM_ERR_INVALID;
+    }
+    return configure_mma(f, threads, blocks_per_sm, (unsigned)std::max(0, sleep_ns));
+}
+
+int dm_flat_status(dm_flat *f, void *stream) {
+    DM_CHECK_FLAT(f);
+    int v = 0;
+    DM_CUDA(cudaMemcpyAsync(&v, f->status, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    DM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (v != 0) {
+        const int zero = 0;
+        cudaMemcpy(f->status, &zero, sizeof(int), cudaMemcpyHostToDevice);
+        dm::set_error("exact averaging pass aborted by its watchdog (a lane waited > 4 s for its inputs)");
+        return DM_ERR_CUDA;
+    }
     return DM_OK;
 }
 
@@ -800,12 +946,6 @@ void dm_flat_destroy(dm_flat *f) {
     for (void *p : f->allocs) cudaFree(p);
     delete f;
 }
-
-#define DM_CHECK_FLAT(f)                        \
-    if (!(f)) {                                 \
-        dm::set_error("null flat handle");      \
-        return DM_ERR_INVALID;                  \
-    }
 
 int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
@@ -857,6 +997,8 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.F = F;
     args.B = B;
     args.bounds = bounds;
+    args.status = f->status;
+    args.sleep_ns = f->mma_sleep_ns;
     switch (f->mma_w) {
         case 8: return launch_mma<8>(f, forward, args, s);
         case 16: return launch_mma<16>(f, forward, args, s);
@@ -925,7 +1067,7 @@ int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, in
 }
 
 static int pairwise(const double *a, const double *b, int64_t n, double *out, cudaStream_t s) {
-    if (n < 0 || n >= INT32_MAX || !a || !out) {
+    if (n < 0 || n >= INT32_MAX || (n > 0 && !a) || !out) {
         dm::set_error("invalid reduction arguments");
         return DM_ERR_INVALID;
     }

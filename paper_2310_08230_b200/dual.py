@@ -28,6 +28,33 @@ def as_device(x, device) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=device)
 
 
+class KernelTimer:
+    """CUDA-event timing of individual kernel launches on the launching
+    (current torch) stream; used by bench.py for the roofline numbers."""
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+
+    def begin(self, name):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        return (name, a, b)
+
+    def end(self, ev):
+        name, a, b = ev
+        b.record()
+        self.events.setdefault(name, []).append((a, b))
+
+    def summary(self) -> dict[str, dict]:
+        torch.cuda.synchronize()
+        out = {}
+        for name, evs in self.events.items():
+            ms = [a.elapsed_time(b) for a, b in evs]
+            out[name] = {"launches": len(ms), "total_ms": float(sum(ms)), "avg_ms": float(sum(ms) / len(ms))}
+        return out
+
+
 class DualState:
     """Per-constraint duals plus cached sweep distances, resident on a GPU."""
 
@@ -50,6 +77,7 @@ class DualState:
         self.bound = -np.inf
         self.best_bound = -np.inf
         self.sweeps = 0  # full-table sweep equivalents (2 arcs per node each)
+        self.pass_timer: KernelTimer | None = None
         free = instance.unconstrained_variables()
         self.free_values = {int(v): (0 if instance.costs[v] >= 0 else 1) for v in free}
         self.free_contribution = float(np.minimum(instance.costs[free], 0.0).sum()) if len(free) else 0.0
@@ -119,7 +147,10 @@ class DualState:
 
     def eval_step(self, d: torch.Tensor, gamma: float) -> float:
         """Objective at lam + gamma*d without materialising it (fused trial)."""
+        ev = self.pass_timer.begin("backward_trial") if self.pass_timer else None
         self.dev.k_backward_trial(self.lam_d, d, gamma, self._scratch(), self._scratch_bounds)
+        if ev:
+            self.pass_timer.end(ev)
         self.sweeps += 1
         return self._sum_bounds(self._scratch_bounds)
 
@@ -171,22 +202,30 @@ def dual_objective(state: DualState) -> float:
 
 def mma_pass(state: DualState, direction: str) -> DualState:
     """One exact averaging pass over all variables (dual.py:154-186)."""
+    timer = state.pass_timer
     if direction == FORWARD:
         if not state.b_valid:
             state.refresh_backward()
+        ev = timer.begin("mma_forward") if timer else None
         state.dev.k_mma_forward(state.lam_d, state.F, state.B, state._bounds)
+        if ev:
+            timer.end(ev)
         state.f_valid = True
         state.b_valid = False
     elif direction == BACKWARD:
         if not state.f_valid:
             state.refresh_forward()
+        ev = timer.begin("mma_backward") if timer else None
         state.dev.k_mma_backward(state.lam_d, state.F, state.B, state._bounds)
+        if ev:
+            timer.end(ev)
         state.b_valid = True
         state.f_valid = False
     else:
         raise ValueError(f"unknown pass direction {direction!r}")
     state.sweeps += 2
     state._set_bound()
+    state.dev.check_status()  # fail loudly if the pass's watchdog fired
     return state
 
 

@@ -101,6 +101,17 @@ class DeviceFlat:
     def k_mma_backward(self, lam, F, B, bounds):
         _native.call("dm_k_mma_backward", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(bounds), self._s())
 
+    def set_mma_config(self, threads: int = 256, blocks_per_sm: int = 2, sleep_ns: int = 0):
+        """Launch shape of the exact passes (see dm_flat_set_mma_config)."""
+        _native.call("dm_flat_set_mma_config", self._h, int(threads), int(blocks_per_sm), int(sleep_ns))
+        info = _native.FlatInfo()
+        _native.check(_native.load().dm_flat_get_info(self._h, ctypes.byref(info)), "dm_flat_get_info")
+        self.info = {k: getattr(info, k) for k, _ in _native.FlatInfo._fields_}
+
+    def check_status(self):
+        """Raise if an exact pass was aborted by its watchdog (synchronises)."""
+        _native.call("dm_flat_status", self._h, self._s())
+
     def k_min_marginals(self, lam, F, B, m0, m1):
         _native.call("dm_k_min_marginals", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(m0), _ptr(m1), self._s())
 

@@ -1,0 +1,229 @@
+"""B200 path == reference, through the C-ABI library (pytest -m gpu).
+
+* every golden case (real-reference outputs): init duals, each exact pass,
+  min-marginal table, subgradient, agreement scores and the mma-only
+  trajectory bit-for-bit; hybrid trajectories bit-for-bit against the
+  oracle in pairwise-dot mode and within 1e-9 of the reference's BLAS run;
+* kernel-level checks on random duals against the C oracle;
+* numpy-order reductions, L-BFGS pieces and projection.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model, solver
+from paper_2310_08230_b200 import qn
+from paper_2310_08230_b200.config import SolveConfig
+from paper_2310_08230_b200.dual import BACKWARD, FORWARD, dual_objective, init_duals, mma_pass, subgradient
+from paper_2310_08230_b200.errors import EmptyHistory
+from paper_2310_08230_b200.ilp import IlpInstance, make_row
+from paper_2310_08230_b200.kernels import dev_dot, dev_sum
+from paper_2310_08230_b200.primal import agreement_scores
+from tests.golden_util import case_inputs, h, load_cases
+
+pytestmark = pytest.mark.gpu
+CASES = load_cases()
+
+
+def product_instance(case):
+    costs, rows, chunk = case_inputs(case)
+    if isinstance(rows, list):
+        return IlpInstance.from_rows(costs, [make_row(*r) for r in rows], chunk_size=chunk)
+    return IlpInstance.from_csr(rows.costs, rows.row_ptr, rows.row_var, rows.row_coef, rows.row_rhs, chunk)
+
+
+def oracle_twin(inst):
+    f = inst.flat
+    arrays = {k: getattr(f, k) for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd", "zero_t",
+                                          "one_t", "proc_ptr", "proc_layers")}
+    return model.from_flat_table(inst.costs, inst.variable_order, f.constraint_counts, arrays)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_exact_passes_match_reference(case):
+    inst = product_instance(case)
+    st = init_duals(inst)
+    assert st.bound == case["init"]["bound"]
+    assert h(st.lam) == case["init"]["lam"]
+    mma_pass(st, FORWARD)
+    g = case["after_forward"]
+    assert st.bound == g["bound"]
+    assert h(st.lam) == g["lam"]
+    assert h(st.F.cpu().numpy()) == g["F"]
+    m0, m1 = st.min_marginal_table()
+    assert (h(m0), h(m1)) == (g["m0"], g["m1"])
+    assert h(st.B.cpu().numpy()) == g["B"]
+    mma_pass(st, BACKWARD)
+    g = case["after_backward"]
+    assert (st.bound, h(st.lam), h(st.B.cpu().numpy())) == (g["bound"], g["lam"], g["B"])
+    assert h(subgradient(st)) == g["subgradient"]
+    sc = agreement_scores(st)
+    assert (h(sc.agrees), h(sc.score), h(sc.preferred)) == tuple(
+        case["agreement"][k] for k in ("agrees", "score", "preferred"))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_mma_only_solve_matches_reference(case):
+    inst = product_instance(case)
+    g = case["mma-only"]
+    iters = len(g["bounds"]) - 1 if g["stop"] == "max_iterations" else 10_000
+    res = qn.solve(inst, SolveConfig(mode="mma-only", max_iterations=iters))
+    assert res.bounds == g["bounds"]
+    assert [r.kind for r in res.records] == g["kinds"]
+    assert res.stop_reason == g["stop"]
+    assert h(res.state.lam) == g["lam"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_hybrid_solve_matches_oracle_and_reference(case):
+    inst = product_instance(case)
+    g = case["hybrid"]
+    iters = len(g["bounds"]) - 1 if g["stop"] == "max_iterations" else 10_000
+    res = qn.solve(inst, SolveConfig(mode="hybrid", max_iterations=iters))
+    oi, of = oracle_twin(inst)
+    ost, orec, ostop = solver.solve(oi, mode="hybrid", max_iterations=iters, dot="pairwise", flat=of)
+    assert res.bounds == [r[2] for r in orec]  # bitwise, same reduction order
+    assert [r.kind for r in res.records] == [r[1] for r in orec]
+    assert res.stop_reason == ostop
+    assert res.state.lam.tobytes() == ost.lam.tobytes()
+    ref = np.array(g["bounds"])
+    got = np.array(res.bounds)
+    n = min(len(ref), len(got))
+    assert np.allclose(got[:n], ref[:n], rtol=1e-9, atol=1e-9)  # OpenBLAS ddot order
+
+
+@pytest.mark.parametrize("name", ["random3_c3", "random7_c0", "ps_tetra", "ps_icosa", "ps_c1"])
+def test_sweep_kernels_on_random_duals(name):
+    case = next(c for c in CASES if c["name"] == name)
+    inst = product_instance(case)
+    oi, of = oracle_twin(inst)
+    rng = np.random.default_rng(1)
+    for trial in range(3):
+        lam = rng.standard_normal(of.num_layers) * (10.0 ** trial)
+        ost = solver.OracleDual(oi, of)
+        ost.lam[:] = lam
+        ost.refresh_backward()
+        ost.refresh_forward()
+        st = init_duals(inst)
+        st.set_lambda(lam)
+        assert st.B.cpu().numpy().tobytes() == ost.B.tobytes()
+        st.refresh_forward()
+        assert st.F.cpu().numpy().tobytes() == ost.F.tobytes()
+        assert st.bound == ost.bound
+        m0, m1 = st.min_marginal_table()
+        om0, om1 = ost.min_marginals()
+        assert m0.tobytes() == om0.tobytes() and m1.tobytes() == om1.tobytes()
+        assert subgradient(st).tobytes() == ost.subgradient().tobytes()
+        d = rng.standard_normal(of.num_layers)
+        dd = torch.as_tensor(d, device=st.device)
+        for gamma in (0.0, 0.37, 3.1):
+            assert st.eval_step(dd, gamma) == ost.eval_trial(d, gamma)
+        # exact passes from arbitrary duals
+        mma_pass(st, FORWARD)
+        ost.mma(True)
+        assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
+        mma_pass(st, BACKWARD)
+        ost.mma(False)
+        assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
+
+
+@pytest.mark.parametrize("n", [0, 1, 5, 7, 8, 9, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 4097, 65537, 636_800,
+                               2_000_003])
+def test_pairwise_sum_and_dot_match_numpy(n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)
+    b = rng.standard_normal(n)
+    ta, tb = torch.as_tensor(a, device="cuda"), torch.as_tensor(b, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    dev_sum(ta, out[0:1])
+    dev_dot(ta, tb, out[1:2])
+    got = out.cpu().numpy()
+    assert got[0].tobytes() == np.sum(a).tobytes()
+    assert got[1].tobytes() == np.sum(a * b).tobytes()
+
+
+def kinked():
+    return IlpInstance.from_rows(np.array([4.0, 1.0, 3.0]), [make_row([0, 1], [1, 1], 1), make_row([0, 2], [1, 1], 1)])
+
+
+def test_project_direction_reference_example():  # reference test_qn.py:40-44
+    st = init_duals(kinked())
+    d = qn.project_direction(np.array([3.0, 7.0, 1.0, -2.0]), st)
+    assert d.tolist() == [1.0, 0.0, -1.0, 0.0]
+
+
+def test_lbfgs_direction_requires_history():
+    with pytest.raises(EmptyHistory):
+        qn.lbfgs_direction(np.zeros(3), qn.LbfgsHistory(5))
+
+
+def test_lbfgs_direction_matches_dense_oracle_and_pairwise_oracle():  # test_qn.py:62-75
+    rng = np.random.default_rng(42)
+    n = 12
+    history = qn.LbfgsHistory(10)
+    cfg = qn.StepConfig()
+    pairs = []
+    while len(history) < 7:
+        s = rng.standard_normal(n)
+        y = rng.standard_normal(n)
+        if s @ y >= cfg.curvature_eps:
+            qn.update_history(s, y, history, cfg)
+            sy = float(np.sum(s * y))
+            pairs.insert(0, (s, y, 1.0 / sy, sy))
+            pairs = pairs[:10]
+        g = rng.standard_normal(n)
+        d = qn.lbfgs_direction(g, history)
+        ps = list(history.newest_first())
+        s0, y0, _ = ps[0]
+        s0, y0 = s0.cpu().numpy(), y0.cpu().numpy()
+        H = np.eye(n) * (s0 @ y0) / (y0 @ y0)
+        for s, y, rho in reversed(ps):
+            s, y = s.cpu().numpy(), y.cpu().numpy()
+            V = np.eye(n) - rho * np.outer(s, y)
+            H = V @ H @ V.T + rho * np.outer(s, s)
+        ref = H @ g
+        assert np.abs(d - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+        assert d.tobytes() == solver.lbfgs(g, pairs, solver._dot_pairwise).tobytes()
+
+
+def test_find_step_size_kinked():  # test_qn.py:104-114
+    st = init_duals(kinked())
+    assert dual_objective(st) == pytest.approx(3.0)
+    g = subgradient(st)
+    assert g.tolist() == [0.0, 1.0, 1.0, 0.0]
+    d = qn.project_direction(g, st)
+    gamma, improved = qn.find_step_size(st, d, 1.0, qn.StepConfig(min_ascent=1e-3))
+    assert improved
+    assert st.eval_lambda(st.lam + gamma * d) == pytest.approx(3.5)
+
+
+def test_find_step_size_counts():  # test_qn.py:117-137
+    st = init_duals(kinked())
+    calls = []
+    orig = st.eval_step
+    st.eval_step = lambda d, gm: (calls.append(1), orig(d, gm))[1]
+    gamma, improved = qn.find_step_size(st, np.zeros(4), 1.0, qn.StepConfig(min_ascent=1e-3, max_trials=5))
+    assert not improved and len(calls) == 6
+    calls.clear()
+    d = qn.project_direction(subgradient(st), st)
+    qn.find_step_size(st, d, 1.0, qn.StepConfig(min_ascent=-10.0))
+    assert len(calls) == 2
+
+
+def test_solver_iteration_empty_history_is_averaging():  # test_qn.py:140-146
+    st = init_duals(kinked())
+    gamma, used = qn.solver_iteration(st, qn.LbfgsHistory(5), 1.0, qn.StepConfig())
+    assert not used and gamma == 1.0
+    assert dual_objective(st) == pytest.approx(4.0)
+
+
+def test_free_variables_clamped():  # test_dual.py:84-90
+    inst = IlpInstance.from_rows(np.array([-2.0, 1.0, 3.0]), [make_row([1], [1], 1)])
+    st = init_duals(inst)
+    assert st.free_values == {0: 1, 2: 0}
+    assert dual_objective(st) == pytest.approx(-1.0)
+    sums = st.lambda_sums()
+    assert sums.tolist() == [-2.0, 1.0, 3.0]
+    sc = agreement_scores(st)
+    assert not sc.agrees[0] and not sc.agrees[2]
