@@ -203,8 +203,9 @@ def algorithmic_bytes(flat):
         # arcs 8 + own distance read 8 + target distance read 8 + produced distance 8 + sentinel prime 8
         # per node; lam r/w 16 + task slot 8 + layer offset 4 per layer; bound 8 per diagram
         "mma": 40 * N + 28 * L + 8 * nb,
-        # arcs 8 + B write 8 + target B read 8 per node; lam 8 + d 8 + offset 4 per layer; bound/offsets 12 per diagram
-        "backward_trial": 24 * N + 20 * L + 12 * nb,
+        # interleaved arcs 8 per node (next-layer distances stay in shared memory, trial writes no table);
+        # lam 8 + d 8 per layer; bound 8 + offsets 8 per diagram
+        "backward_trial": 8 * N + 16 * L + 16 * nb,
     }
 
 

@@ -116,10 +116,22 @@ int dm_flat_get_info(const dm_flat *flat, dm_flat_info *info);
  * call was aborted by its watchdog (DM_ERR_CUDA) — resets the word. */
 int dm_flat_status(dm_flat *flat, void *stream);
 /* Launch shape of the exact passes: block size (multiple of 32, <= 256),
- * resident blocks per SM (<= 0: as many as fit) and the back-off between
- * unsuccessful polls.  Defaults come from DM_MMA_THREADS /
- * DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS at creation. */
-int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns);
+ * resident blocks per SM (<= 0: as many as fit), the back-off between
+ * unsuccessful polls, the poll mode (probe != 0: poll one probe word
+ * before reading the inputs; 0: poll all inputs) and the progress lookahead
+ * (a warp polls its inputs only once a task within `lookahead` levels of its
+ * own has finished; 0 disables the gating).  Defaults come from
+ * DM_MMA_THREADS / DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS / DM_MMA_PROBE /
+ * DM_MMA_LOOKAHEAD. */
+int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns, int probe,
+                           int lookahead);
+/* Profiling hooks: a device buffer of tasks*32*5 u64 receives, per lane,
+ * %globaltimer stamps (task start, own inputs seen, group go, dual updated, outputs published) of the
+ * following exact passes (NULL disables); dm_flat_task_levels copies the
+ * DAG level of every task (and optionally the 32 lane layers per task) of
+ * the forward/backward schedule. */
+int dm_flat_set_trace(dm_flat *flat, unsigned long long *trace);
+int dm_flat_task_levels(const dm_flat *flat, int forward, int32_t *levels, int32_t *lane_layers);
 void dm_flat_destroy(dm_flat *flat);
 
 /* --- sweep kernels: one per reference kernel ---------------------------- */

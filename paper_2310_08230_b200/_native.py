@@ -57,7 +57,9 @@ SIGNATURES = {
     "dm_flat_create": ([ctypes.POINTER(FlatDesc), _INT, _P, ctypes.POINTER(_P)], _INT),
     "dm_flat_get_info": ([_P, ctypes.POINTER(FlatInfo)], _INT),
     "dm_flat_status": ([_P, _P], _INT),
-    "dm_flat_set_mma_config": ([_P, _INT, _INT, _INT], _INT),
+    "dm_flat_set_mma_config": ([_P, _INT, _INT, _INT, _INT, _INT], _INT),
+    "dm_flat_set_trace": ([_P, _P], _INT),
+    "dm_flat_task_levels": ([_P, _INT, _P, _P], _INT),
     "dm_flat_destroy": ([_P], None),
     "dm_k_backward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_backward_trial": ([_P, _P, _P, _D, _P, _P, _P], _INT),

@@ -350,9 +350,30 @@ struct MmaArgs {
     const int32_t *task_layer, *task_meta;
     const int32_t *lnl, *zero_t, *one_t, *layer_bdd;
     double *lam, *F, *B, *bounds;
-    int *status;        // 0 ok, 1 watchdog fired
-    unsigned sleep_ns;  // back-off between unsuccessful polls
+    int *status;                // 0 ok, 1 watchdog fired
+    unsigned sleep_ns;          // back-off between unsuccessful polls
+    int probe;                  // 1: poll one probe word before reading the layer; 0: poll all inputs
+    unsigned long long *trace;  // optional [task*32+lane][5]: start, own inputs seen, group go, dual updated, published
+    const int32_t *task_level;  // DAG level of each task
+    int *progress;              // highest level of a finished task (monotone hint)
+    int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
+    int warm;                   // prefetch the polled lines into L2 at task start
 };
+
+// Progress gating: a warp whose task is far ahead of the wavefront watches a
+// single word (one L2 line for all warps) instead of polling its inputs, so
+// the SM's load queue stays free for the warps on the critical path.  Safe
+// for lookahead >= 1: the lowest unfinished level m always sees
+// progress >= m - 1.
+__device__ __forceinline__ bool wait_progress(const MmaArgs &a, int64_t task, uint64_t t_start, unsigned &spins);
+__device__ __forceinline__ void publish_progress(const MmaArgs &a, int64_t task, int lane) {
+    if (a.lookahead > 0 && lane == 0)
+        asm volatile("red.relaxed.gpu.global.max.s32 [%0], %1;" ::"l"(a.progress), "r"(a.task_level[task]) : "memory");
+}
+
+__device__ __forceinline__ void trace_mark(const MmaArgs &a, int64_t task, int lane, int slot, uint64_t t) {
+    if (a.trace) a.trace[(task * 32 + lane) * 5 + slot] = t;
+}
 
 // true when this warp must abandon the pass (own timeout or another's)
 __device__ __forceinline__ bool watchdog(const MmaArgs &a, uint64_t t_start, unsigned &spins) {
@@ -365,27 +386,60 @@ __device__ __forceinline__ bool watchdog(const MmaArgs &a, uint64_t t_start, uns
     return false;
 }
 
+__device__ __forceinline__ bool wait_progress(const MmaArgs &a, int64_t task, uint64_t t_start, unsigned &spins) {
+    if (a.lookahead <= 0) return true;
+    const int need = a.task_level[task] - a.lookahead;
+    if (need < 0) return true;
+    while (true) {
+        int p;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(p) : "l"(a.progress) : "memory");
+        if (p >= need) return true;
+        if (watchdog(a, t_start, spins)) return false;
+        __nanosleep(a.sleep_ns ? a.sleep_ns : 64);
+    }
+}
+
 // Lanes [gbase, gbase+gcnt) hold the copies of one variable in copy order.
 __device__ __forceinline__ unsigned group_mask(int32_t meta) {
     const int gbase = meta & 0xff, gcnt = (meta >> 8) & 0xff;
     return (gcnt >= 32 ? 0xffffffffu : ((1u << gcnt) - 1u)) << gbase;
 }
 
-// Sum of the finite min-marginal differences of the lane's variable, in copy
-// order (kernels.py:200-233), then the lane's new dual (kernels.py:234-240).
-// Executed by the whole warp; only lanes with `go` use the result.
+// Leftmost minimum: keeps `a` unless `b` is strictly smaller.  Folding a
+// sequence with it in any left-to-right tree returns exactly what the
+// reference's sequential `if c < m: m = c` loop returns (the first element
+// of minimal value), so tree reductions stay bit-identical.
+__device__ __forceinline__ double lmin(double a, double b) { return (b < a) ? b : a; }
+
+template <int N>
+__device__ __forceinline__ double tree_lmin(double (&v)[N]) {
+#pragma unroll
+    for (int s = 1; s < N; s *= 2)
+#pragma unroll
+        for (int i = 0; i + s < N; i += 2 * s) v[i] = lmin(v[i], v[i + s]);
+    return v[0];
+}
+
+// Sum of the finite min-marginal differences of the lane's variable in copy
+// order (kernels.py:200-233) and the lane's new dual (kernels.py:234-240).
+// Whole warp executes it; only lanes with `go` use the result.  The group's
+// deltas are gathered with independent shuffles, then summed sequentially.
+template <int K>
 __device__ __forceinline__ double average_in_group(bool go, int32_t meta, double m0, double m1, double lam_l) {
     const bool fin = go && m0 != DM_INF && m1 != DM_INF;
     const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
+    const unsigned finmask = __ballot_sync(kFull, fin);
     const int gbase = meta & 0xff, gcnt = (meta >> 8) & 0xff;
-    const int maxc = __reduce_max_sync(kFull, go ? gcnt : 0);
+    double dk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) dk[k] = __shfl_sync(kFull, dlt, (gbase + k) & 31);
     double fsum = 0.0;
     int fcnt = 0;
-    for (int k = 0; k < maxc; ++k) {
-        const double dk = __shfl_sync(kFull, dlt, (gbase + k) & 31);
-        const int fk = __shfl_sync(kFull, (int)fin, (gbase + k) & 31);
-        if (k < gcnt && fk) {
-            fsum = __dadd_rn(fsum, dk);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (k >= gcnt) break;
+        if ((finmask >> (gbase + k)) & 1u) {
+            fsum = __dadd_rn(fsum, dk[k]);
             ++fcnt;
         }
     }
@@ -396,33 +450,29 @@ __device__ __forceinline__ double average_in_group(bool go, int32_t meta, double
     return lam_l;
 }
 
-// Min-marginals of one layer from its forward distances f and the distances
-// to TRUE of its arc targets (kernels.py:205-230).
+// Min-marginals of one layer (kernels.py:205-230), as two leftmost-min trees.
+// Nodes with F == INF contribute INF candidates, which never win — the same
+// as the reference's `continue`.
 template <int W>
 __device__ __forceinline__ void layer_marginals(int32_t w, const double (&f)[W], const int32_t (&z)[W],
                                                 const int32_t (&o)[W], const double (&bz)[W],
                                                 const double (&bo)[W], double lam_l, double &m0, double &m1) {
-    m0 = DM_INF;
-    m1 = DM_INF;
+    double c0[W], c1[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-        if (i < w && f[i] != DM_INF) {
-            const double fv = f[i];
-            const double c0 = z[i] == dm::kTrue ? fv : (z[i] == dm::kFalse ? DM_INF : __dadd_rn(fv, bz[i]));
-            if (c0 < m0) m0 = c0;
-            const double c1 = o[i] == dm::kTrue ? __dadd_rn(fv, lam_l)
-                                                : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(__dadd_rn(fv, lam_l), bo[i]));
-            if (c1 < m1) m1 = c1;
-        }
+        const double fv = f[i];
+        const double fl = __dadd_rn(fv, lam_l);
+        c0[i] = (i >= w || z[i] == dm::kFalse) ? DM_INF : (z[i] == dm::kTrue ? fv : __dadd_rn(fv, bz[i]));
+        c1[i] = (i >= w || o[i] == dm::kFalse) ? DM_INF : (o[i] == dm::kTrue ? fl : __dadd_rn(fl, bo[i]));
     }
+    m0 = tree_lmin<W>(c0);
+    m1 = tree_lmin<W>(c1);
 }
 
 // Forward pass.  Warp w takes tasks w, w+W, ... (level order).  Inside a task
 // each variable (lane group) proceeds as soon as its own inputs are
-// published, independently of the other groups in the warp.  A lane first
-// polls a single probe word — the last forward distance its producer writes
-// — and only then reads the whole layer.
-template <int W>
+// published, independently of the other groups in the warp.
+template <int W, int K>
 __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -430,6 +480,7 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         const int32_t l = a.task_layer[task * 32 + lane];
         const int32_t meta = a.task_meta[task * 32 + lane];
         const bool act = l >= 0;
+        const bool last = meta & (1 << 17);
         int32_t nlo = 0, w = 0, n0 = 0, wn = 0;
         double lam_l = 0.0;
         int32_t z[W], o[W];
@@ -437,7 +488,7 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         if (act) {
             nlo = a.lnl[l];
             w = a.lnl[l + 1] - nlo;
-            if (!(meta & (1 << 17))) {
+            if (!last) {
                 n0 = a.lnl[l + 1];
                 wn = a.lnl[l + 2] - n0;
             }
@@ -446,21 +497,30 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         // static inputs: topology and the backward distances (valid all pass)
 #pragma unroll
         for (int i = 0; i < W; ++i) {
+            z[i] = o[i] = dm::kFalse;
+            bz[i] = bo[i] = f[i] = DM_INF;
             if (i < w) {
                 z[i] = a.zero_t[nlo + i];
                 o[i] = a.one_t[nlo + i];
-                bz[i] = z[i] >= 0 ? a.B[z[i]] : 0.0;
-                bo[i] = o[i] >= 0 ? a.B[o[i]] : 0.0;
+                if (z[i] >= 0) bz[i] = a.B[z[i]];
+                if (o[i] >= 0) bo[i] = a.B[o[i]];
             }
+        }
+        // pull the lines this lane will poll into L2 while it waits
+        if (a.warm && act) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.F + nlo));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.F + nlo + w - 1));
         }
         const unsigned gmask = act ? group_mask(meta) : 0u;
         bool have = !act;
         unsigned pending = __ballot_sync(kFull, act);
         unsigned spins = 0;
         const uint64_t t_wait = global_ns();
+        if (act) trace_mark(a, task, lane, 0, t_wait);
+        if (!wait_progress(a, task, t_wait, spins)) return;
         while (pending) {
             if (!have && ((pending >> lane) & 1u)) {
-                if (!is_sentinel(ld_relaxed(a.F + nlo + w - 1))) {
+                if (!a.probe || !is_sentinel(ld_relaxed(a.F + nlo + w - 1))) {
                     bool ok = true;
 #pragma unroll
                     for (int i = 0; i < W; ++i)
@@ -469,6 +529,7 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
                             ok &= !is_sentinel(f[i]);
                         }
                     have = ok;
+                    if (ok && a.trace) trace_mark(a, task, lane, 1, global_ns());
                 }
             }
             const unsigned hm = __ballot_sync(kFull, have);
@@ -483,49 +544,53 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
                 continue;
             }
             pending &= ~gom;
+            if (go && a.trace) trace_mark(a, task, lane, 2, global_ns());
             double m0, m1;
             layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
-            const double lam_new = average_in_group(go, meta, m0, m1, lam_l);
+            const double lam_new = average_in_group<K>(go, meta, m0, m1, lam_l);
             if (!go) continue;
             lam_l = lam_new;
             a.lam[l] = lam_l;
-            // propagate to the next layer (kernels.py:241-269), gather form with
-            // the reference's scatter order: first strict minimum over
-            // (v ascending, zero-arc, one-arc)
-            if (!(meta & (1 << 17))) {
-                for (int32_t u = 0; u < wn; ++u) {
-                    double best = DM_INF;
-                    const int32_t tgt = n0 + u;
+            if (a.trace) trace_mark(a, task, lane, 3, global_ns());
+            // propagate to the next layer (kernels.py:241-269): every target's
+            // value is the leftmost minimum over (v ascending, zero-arc,
+            // one-arc) of the reference's scatter, computed for all targets
+            // at once.
+            double c[W];
 #pragma unroll
-                    for (int i = 0; i < W; ++i) {
-                        if (i < w && f[i] != DM_INF) {
-                            if (z[i] == tgt && f[i] < best) best = f[i];
-                            const double c = __dadd_rn(f[i], lam_l);
-                            if (o[i] == tgt && c < best) best = c;
+            for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
+            if (!last) {
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < wn) {
+                        const int32_t tgt = n0 + u;
+                        double cand[2 * W];
+#pragma unroll
+                        for (int i = 0; i < W; ++i) {
+                            cand[2 * i] = z[i] == tgt ? f[i] : DM_INF;
+                            cand[2 * i + 1] = o[i] == tgt ? c[i] : DM_INF;
                         }
+                        st_relaxed(a.F + tgt, tree_lmin<2 * W>(cand));
                     }
-                    st_relaxed(a.F + tgt, best);
                 }
             } else {
-                double tb = DM_INF;
+                double cand[2 * W];
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    if (i < w && f[i] != DM_INF) {
-                        if (z[i] == dm::kTrue && f[i] < tb) tb = f[i];
-                        const double c = __dadd_rn(f[i], lam_l);
-                        if (o[i] == dm::kTrue && c < tb) tb = c;
-                    }
+                    cand[2 * i] = z[i] == dm::kTrue ? f[i] : DM_INF;
+                    cand[2 * i + 1] = o[i] == dm::kTrue ? c[i] : DM_INF;
                 }
-                a.bounds[a.layer_bdd[l]] = tb;
+                a.bounds[a.layer_bdd[l]] = tree_lmin<2 * W>(cand);
             }
+            if (a.trace) trace_mark(a, task, lane, 4, global_ns());
         }
+        publish_progress(a, task, lane);
     }
 }
 
 // Backward pass: mirror image; a lane waits for the distances to TRUE of the
-// next layer (probe = that layer's last node, written last by its producer)
-// and rebuilds its own layer's distances with the updated dual.
-template <int W>
+// next layer and rebuilds its own layer's distances with the updated dual.
+template <int W, int K>
 __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -534,48 +599,68 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
         const int32_t meta = a.task_meta[task * 32 + lane];
         const bool act = l >= 0;
         const bool last = meta & (1 << 17);
-        int32_t nlo = 0, w = 0, probe = -1;
+        int32_t nlo = 0, w = 0, probe = -1, wnext = 0;
         double lam_l = 0.0;
         int32_t z[W], o[W];
         double bz[W], bo[W], f[W];
         if (act) {
             nlo = a.lnl[l];
             w = a.lnl[l + 1] - nlo;
-            if (!last) probe = a.lnl[l + 2] - 1;
+            if (!last) {
+                probe = a.lnl[l + 2] - 1;
+                wnext = probe + 1 - a.lnl[l + 1];
+            }
             lam_l = a.lam[l];
         }
 #pragma unroll
         for (int i = 0; i < W; ++i) {
+            z[i] = o[i] = dm::kFalse;
+            f[i] = DM_INF;
+            bz[i] = bo[i] = 0.0;
             if (i < w) {
                 z[i] = a.zero_t[nlo + i];
                 o[i] = a.one_t[nlo + i];
                 f[i] = a.F[nlo + i];
-                bz[i] = 0.0;
-                bo[i] = 0.0;
             }
+        }
+        if (a.warm && act && !last) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + a.lnl[l + 1]));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.B + probe));
         }
         const unsigned gmask = act ? group_mask(meta) : 0u;
         bool have = !act || last;
         unsigned pending = __ballot_sync(kFull, act);
         unsigned spins = 0;
         const uint64_t t_wait = global_ns();
+        if (act) trace_mark(a, task, lane, 0, t_wait);
+        if (!wait_progress(a, task, t_wait, spins)) return;
         while (pending) {
             if (!have && ((pending >> lane) & 1u)) {
-                if (!is_sentinel(ld_relaxed(a.B + probe))) {
+                if (!a.probe || !is_sentinel(ld_relaxed(a.B + probe))) {
+                    // read the next layer contiguously (like the forward pass reads
+                    // its own layer), then route values to the arc targets
+                    const int32_t n0 = probe + 1 - wnext;
+                    double nbv[W];
                     bool ok = true;
 #pragma unroll
-                    for (int i = 0; i < W; ++i)
-                        if (i < w) {
-                            if (z[i] >= 0) {
-                                bz[i] = ld_relaxed(a.B + z[i]);
-                                ok &= !is_sentinel(bz[i]);
-                            }
-                            if (o[i] >= 0) {
-                                bo[i] = ld_relaxed(a.B + o[i]);
-                                ok &= !is_sentinel(bo[i]);
-                            }
+                    for (int u = 0; u < W; ++u)
+                        if (u < wnext) {
+                            nbv[u] = ld_relaxed(a.B + n0 + u);
+                            ok &= !is_sentinel(nbv[u]);
                         }
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        double vz = 0.0, vo = 0.0;
+#pragma unroll
+                        for (int u = 0; u < W; ++u) {
+                            if (z[i] == n0 + u) vz = nbv[u];
+                            if (o[i] == n0 + u) vo = nbv[u];
+                        }
+                        bz[i] = vz;
+                        bo[i] = vo;
+                    }
                     have = ok;
+                    if (ok && a.trace) trace_mark(a, task, lane, 1, global_ns());
                 }
             }
             const unsigned hm = __ballot_sync(kFull, have);
@@ -590,12 +675,14 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
                 continue;
             }
             pending &= ~gom;
+            if (go && a.trace) trace_mark(a, task, lane, 2, global_ns());
             double m0, m1;
             layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
-            const double lam_new = average_in_group(go, meta, m0, m1, lam_l);
+            const double lam_new = average_in_group<K>(go, meta, m0, m1, lam_l);
             if (!go) continue;
             lam_l = lam_new;
             a.lam[l] = lam_l;
+            if (a.trace) trace_mark(a, task, lane, 3, global_ns());
             // rebuild this layer's distances to TRUE (kernels.py:340-358)
             double first = 0.0;
 #pragma unroll
@@ -609,7 +696,9 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
                 }
             }
             if (meta & (1 << 16)) a.bounds[a.layer_bdd[l]] = first;  // kernels.py:359-361
+            if (a.trace) trace_mark(a, task, lane, 4, global_ns());
         }
+        publish_progress(a, task, lane);
     }
 }
 
@@ -636,11 +725,20 @@ struct dm_flat {
     int64_t fw_tasks = 0, bw_tasks = 0, fw_depth = 0, bw_depth = 0;
     int64_t max_width = 0, max_degree = 0;
     int *status = nullptr;  // device watchdog word of the exact passes
-    int mma_w = 8;
+    int *progress = nullptr;  // progress hint word of the exact passes
+    int32_t *fw_task_level = nullptr, *bw_task_level = nullptr;
+    int mma_lookahead = 0;
+    int mma_warm = 1;
+    int mma_w = 8, mma_k = 8;
     int mma_threads = 256, mma_blocks_per_sm = 0;
     unsigned mma_sleep_ns = 0;
+    int mma_probe = 0;
+    unsigned long long *trace = nullptr;
+    std::vector<int32_t> fw_level, bw_level;  // host copy: DAG level of each task
+    std::vector<int32_t> fw_layer_h, bw_layer_h;  // host copy of the lane layers (profiling)
     int mma_grid_fw = 0, mma_grid_bw = 0;
     int64_t bytes = 0;
+    dm::SweepDev sweep;  // interleaved layout for the full-table sweeps
     std::vector<void *> allocs;
 };
 
@@ -713,22 +811,22 @@ int get_plan(int64_t n, DevPlan **out) {
 inline int blocks_for(int64_t n, int threads) { return (int)std::max<int64_t>(1, (n + threads - 1) / threads); }
 inline int grid_stride_blocks(int64_t n) { return (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 255) / 256)); }
 
-template <int W>
+template <int W, int K>
 int launch_mma(const dm_flat *f, bool forward, MmaArgs &args, cudaStream_t s) {
     void *params[] = {&args};
-    const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
+    const void *fn = forward ? (const void *)mma_forward_kernel<W, K> : (const void *)mma_backward_kernel<W, K>;
     const int grid = forward ? f->mma_grid_fw : f->mma_grid_bw;
     DM_CUDA(cudaLaunchCooperativeKernel(fn, grid, f->mma_threads, params, 0, s));
     return DM_OK;
 }
 
 // Persistent grid: min(requested, resident) blocks per SM x SM count.
-template <int W>
+template <int W, int K>
 int mma_grid_for(bool forward, int threads, int want_per_sm, int *grid) {
     int dev, sms, per;
     DM_CUDA(cudaGetDevice(&dev));
     DM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const void *fn = forward ? (const void *)mma_forward_kernel<W> : (const void *)mma_backward_kernel<W>;
+    const void *fn = forward ? (const void *)mma_forward_kernel<W, K> : (const void *)mma_backward_kernel<W, K>;
     DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0));
     if (per < 1) {
         dm::set_error("exact averaging kernel cannot be resident");
@@ -741,21 +839,27 @@ int mma_grid_for(bool forward, int threads, int want_per_sm, int *grid) {
 
 }  // namespace
 
-static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sleep_ns) {
+// Instantiations: W = widest layer (8/16/32), K = most copies per variable (8/32).
+#define DM_MMA_DISPATCH(f, CALL)                                  \
+    (f->mma_k <= 8 ? (f->mma_w == 8 ? CALL(8, 8) : f->mma_w == 16 ? CALL(16, 8) : CALL(32, 8)) \
+                   : (f->mma_w == 8 ? CALL(8, 32) : f->mma_w == 16 ? CALL(16, 32) : CALL(32, 32)))
+
+static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sleep_ns, int probe, int lookahead) {
+    f->mma_lookahead = lookahead < 0 ? 0 : (lookahead & 0xffff);
+    f->mma_warm = (lookahead >> 16) & 1;  // bit 16 of the lookahead word: L2 warming
     if (threads < 32 || threads > 256 || threads % 32) {
         dm::set_error("exact-pass block size must be a multiple of 32 in [32, 256]");
         return DM_ERR_INVALID;
     }
-    int rc;
-    switch (f->mma_w) {
-        case 8: rc = mma_grid_for<8>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<8>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
-        case 16: rc = mma_grid_for<16>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<16>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
-        default: rc = mma_grid_for<32>(true, threads, blocks_per_sm, &f->mma_grid_fw); if (!rc) rc = mma_grid_for<32>(false, threads, blocks_per_sm, &f->mma_grid_bw); break;
-    }
-    if (rc) return rc;
+#define DM_GRID(W, K)                                                          \
+    (mma_grid_for<W, K>(true, threads, blocks_per_sm, &f->mma_grid_fw) ||      \
+     mma_grid_for<W, K>(false, threads, blocks_per_sm, &f->mma_grid_bw))
+    if (DM_MMA_DISPATCH(f, DM_GRID)) return DM_ERR_CUDA;
+#undef DM_GRID
     f->mma_threads = threads;
     f->mma_blocks_per_sm = blocks_per_sm;
     f->mma_sleep_ns = sleep_ns;
+    f->mma_probe = probe ? 1 : 0;
     return DM_OK;
 }
 
@@ -879,14 +983,48 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = up(&f->layer_bdd, std::move(layer_bdd)))) return rc;
     if ((rc = up(&f->pos_var, std::move(pos_var)))) return rc;
     if ((rc = up(&f->var_count, std::move(var_count)))) return rc;
+    if ((rc = up(&f->fw_task_level, fw.task_level))) return rc;
+    if ((rc = up(&f->bw_task_level, bw.task_level))) return rc;
+    if ((rc = up(&f->progress, std::vector<int32_t>(1, -1)))) return rc;
+    f->fw_level = fw.task_level;
+    f->bw_level = bw.task_level;
+    f->fw_layer_h = fw.task_layer;
+    f->bw_layer_h = bw.task_layer;
     if ((rc = up(&f->fw_layer, std::move(fw.task_layer)))) return rc;
     if ((rc = up(&f->fw_meta, std::move(fw.task_meta)))) return rc;
     if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
     if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
     if ((rc = up(&f->status, std::vector<int32_t>(1, 0)))) return rc;
+    {
+        dm::SweepLayout sl;
+        if ((rc = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl))) return rc;
+        int32_t *gb, *gn, *pw, *zl, *ol;
+        int64_t *gp, *ps;
+        if ((rc = up(&gb, std::move(sl.grp_bdd)))) return rc;
+        if ((rc = up(&gn, std::move(sl.grp_npos)))) return rc;
+        if ((rc = up(&pw, std::move(sl.pos_width)))) return rc;
+        if ((rc = up(&zl, std::move(sl.zl)))) return rc;
+        if ((rc = up(&ol, std::move(sl.ol)))) return rc;
+        if ((rc = upload(f.get(), &gp, sl.grp_pos_lo.data(), (int64_t)sl.grp_pos_lo.size(), s))) return rc;
+        if ((rc = upload(f.get(), &ps, sl.pos_slot.data(), (int64_t)sl.pos_slot.size(), s))) return rc;
+        DM_CUDA(cudaStreamSynchronize(s));  // sl's int64 vectors die with this scope
+        f->sweep.groups = sl.groups;
+        f->sweep.max_width = (int32_t)sl.max_width;
+        f->sweep.grp_bdd = gb;
+        f->sweep.grp_npos = gn;
+        f->sweep.pos_width = pw;
+        f->sweep.grp_pos_lo = gp;
+        f->sweep.pos_slot = ps;
+        f->sweep.zl = zl;
+        f->sweep.ol = ol;
+        f->sweep.bdd_layer_lo = f->bdd_layer_lo;
+        f->sweep.lnl = f->lnl;
+    }
     f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
+    f->mma_k = max_degree <= 8 ? 8 : 32;
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 2),
-                       (unsigned)env_int("DM_MMA_SLEEP_NS", 0));
+                       (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
+                       env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16));
     if (rc) return rc;
     DevPlan *dummy;
     if ((rc = get_plan(nb, &dummy))) return rc;
@@ -919,12 +1057,33 @@ int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
         return DM_ERR_INVALID;                  \
     }
 
-int dm_flat_set_mma_config(dm_flat *f, int threads, int blocks_per_sm, int sleep_ns) {
+int dm_flat_set_mma_config(dm_flat *f, int threads, int blocks_per_sm, int sleep_ns, int probe, int lookahead) {
     if (!f) {
         dm::set_error("null flat handle");
         return DM_ERR_INVALID;
     }
-    return configure_mma(f, threads, blocks_per_sm, (unsigned)std::max(0, sleep_ns));
+    return configure_mma(f, threads, blocks_per_sm, (unsigned)std::max(0, sleep_ns), probe, lookahead);
+}
+
+int dm_flat_set_trace(dm_flat *f, unsigned long long *trace) {
+    if (!f) {
+        dm::set_error("null flat handle");
+        return DM_ERR_INVALID;
+    }
+    f->trace = trace;
+    return DM_OK;
+}
+
+int dm_flat_task_levels(const dm_flat *f, int forward, int32_t *levels, int32_t *lane_layers) {
+    if (!f) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    const auto &v = forward ? f->fw_level : f->bw_level;
+    const auto &w = forward ? f->fw_layer_h : f->bw_layer_h;
+    if (levels) std::memcpy(levels, v.data(), v.size() * sizeof(int32_t));
+    if (lane_layers) std::memcpy(lane_layers, w.data(), w.size() * sizeof(int32_t));
+    return DM_OK;
 }
 
 int dm_flat_status(dm_flat *f, void *stream) {
@@ -950,26 +1109,24 @@ void dm_flat_destroy(dm_flat *f) {
 int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
     if (f->nb == 0) return DM_OK;
-    k_backward_kernel<false><<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
-        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, nullptr, 0.0, B, bounds);
-    return check_stream_error("k_backward");
+    if (!B) {
+        dm::set_error("k_backward needs B");
+        return DM_ERR_INVALID;
+    }
+    return dm::sweep_backward(f->sweep, lam, nullptr, 0.0, B, bounds, stream);
 }
 
 int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, double gamma, double *B,
                         double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
     if (f->nb == 0) return DM_OK;
-    k_backward_kernel<true><<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
-        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, d, gamma, B, bounds);
-    return check_stream_error("k_backward_trial");
+    return dm::sweep_backward(f->sweep, lam, d, gamma, B, bounds, stream);
 }
 
 int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
     if (f->nb == 0) return DM_OK;
-    k_forward_kernel<<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
-        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, F, bounds);
-    return check_stream_error("k_forward");
+    return dm::sweep_forward(f->sweep, lam, F, bounds, stream);
 }
 
 static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, double *B, double *bounds,
@@ -999,11 +1156,16 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.bounds = bounds;
     args.status = f->status;
     args.sleep_ns = f->mma_sleep_ns;
-    switch (f->mma_w) {
-        case 8: return launch_mma<8>(f, forward, args, s);
-        case 16: return launch_mma<16>(f, forward, args, s);
-        default: return launch_mma<32>(f, forward, args, s);
-    }
+    args.probe = f->mma_probe;
+    args.trace = f->trace;
+    args.task_level = forward ? f->fw_task_level : f->bw_task_level;
+    args.progress = f->progress;
+    args.lookahead = f->mma_lookahead;
+    args.warm = f->mma_warm;
+    DM_CUDA(cudaMemsetAsync(f->progress, 0xff, sizeof(int), s));  // -1: nothing finished
+#define DM_LAUNCH(W, K) launch_mma<W, K>(f, forward, args, s)
+    return DM_MMA_DISPATCH(f, DM_LAUNCH);
+#undef DM_LAUNCH
 }
 
 int dm_k_mma_forward(const dm_flat *f, double *lam, double *F, const double *B, double *bounds, void *stream) {
@@ -1087,7 +1249,7 @@ int dm_sum(const double *x, int64_t n, double *out, void *stream) {
 }
 
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream) {
-    if (!b) {
+    if (!b && n > 0) {
         dm::set_error("dm_dot needs two vectors");
         return DM_ERR_INVALID;
     }

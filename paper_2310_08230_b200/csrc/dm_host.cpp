@@ -352,6 +352,7 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
     s.depth = depth;
     int used = 32;  // lanes used in the open task (32 = none open)
     int32_t open_level = -1;
+    s.task_level.clear();
     auto open_task = [&]() {
         s.task_layer.insert(s.task_layer.end(), 32, -1);
         s.task_meta.insert(s.task_meta.end(), 32, 0);
@@ -364,6 +365,7 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
         if (pos_level[p] != open_level || used + c > 32) {
             open_task();
             open_level = pos_level[p];
+            s.task_level.push_back(open_level);
         }
         const size_t base = s.task_layer.size() - 32;
         for (int k = 0; k < c; ++k) {

@@ -60,11 +60,42 @@ PairwisePlan plan_pairwise(int64_t n);
 // lane's group base lane (bits 0-7), group size (8-15), first-layer flag
 // (bit 16) and last-layer flag (bit 17).
 struct MmaSchedule {
-    std::vector<int32_t> task_layer, task_meta;
+    std::vector<int32_t> task_layer, task_meta, task_level;
     int64_t depth = 0, tasks = 0;
 };
 int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_bdd_or_null,
                        const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,
                        const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &out);
+
+// Interleaved sweep layout (dm_layout.cpp): 32 diagrams per warp group,
+// layers aligned at the last layer (position 0), node slots interleaved by
+// lane, arc targets as local indices into the next layer.
+struct SweepLayout {
+    int64_t groups = 0, slots = 0, max_width = 0;
+    std::vector<int32_t> grp_bdd;     // [groups*32] diagram of each lane, -1 = idle
+    std::vector<int32_t> grp_npos;    // [groups] positions (max layers in the group)
+    std::vector<int64_t> grp_pos_lo;  // [groups+1] into pos_width / pos_slot
+    std::vector<int32_t> pos_width;   // widest layer at each position of each group
+    std::vector<int64_t> pos_slot;    // first node slot of each position
+    std::vector<int32_t> zl, ol;      // [slots*32] local targets, -1 FALSE, -2 TRUE
+};
+int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_node_lo,
+                       const int64_t *zero_t, const int64_t *one_t, SweepLayout &out);
+
+// Device view of a SweepLayout plus the reference-layout offsets the sweeps
+// need to read duals and write distances (dm_sweep.cu).
+struct SweepDev {
+    int64_t groups = 0;
+    int32_t max_width = 0;
+    const int32_t *grp_bdd = nullptr, *grp_npos = nullptr, *pos_width = nullptr;
+    const int64_t *grp_pos_lo = nullptr, *pos_slot = nullptr;
+    const int32_t *zl = nullptr, *ol = nullptr;
+    const int32_t *bdd_layer_lo = nullptr, *lnl = nullptr;
+};
+// kernels.py:95-120 (B may be null: trial evaluation, bounds only; d null: plain duals)
+int sweep_backward(const SweepDev &s, const double *lam, const double *d, double gamma, double *B,
+                   double *bounds, void *stream);
+// kernels.py:123-159
+int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream);
 
 }  // namespace dm

@@ -1,0 +1,92 @@
+// Interleaved "sweep layout" of the diagram table for the full-table sweeps
+// (k_backward, the step-search trials, k_forward).
+//
+// The reference layout (FlatBdds) stores each diagram contiguously, which
+// makes a thread-per-diagram sweep read 32 unrelated cache lines per warp
+// instruction.  Here diagrams of similar shape are grouped 32 to a warp
+// (sorted by layer count, then node count), their layers are aligned at the
+// LAST layer (position k = 0 is every lane's last layer), and the node slots
+// of one position are interleaved by lane: slot (k, i) of lane t lives at
+// element (pos_slot[k] + i) * 32 + t.  A warp instruction then reads 128
+// contiguous bytes.  Arc targets are stored as LOCAL indices into the next
+// layer (position k - 1), so a sweep keeps the neighbouring layer's
+// distances in shared memory instead of re-reading them from L2.
+// Padded slots (lanes whose diagram is shorter / narrower) have both arcs
+// to FALSE and never feed a real node.
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "dm_internal.h"
+
+namespace dm {
+
+int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *lnl, const int64_t *zero_t,
+                       const int64_t *one_t, SweepLayout &s) {
+    std::vector<int64_t> order(nb);
+    std::iota(order.begin(), order.end(), 0);
+    auto nlay = [&](int64_t j) { return bdd_layer_lo[j + 1] - bdd_layer_lo[j]; };
+    auto nnod = [&](int64_t j) { return lnl[bdd_layer_lo[j + 1]] - lnl[bdd_layer_lo[j]]; };
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        if (nlay(a) != nlay(b)) return nlay(a) > nlay(b);
+        return nnod(a) > nnod(b);
+    });
+    s.groups = (nb + 31) / 32;
+    s.grp_bdd.assign(s.groups * 32, -1);
+    s.grp_npos.assign(s.groups, 0);
+    s.grp_pos_lo.assign(s.groups + 1, 0);
+    s.pos_width.clear();
+    s.pos_slot.clear();
+    s.max_width = 0;
+    int64_t slots = 0;
+    for (int64_t g = 0; g < s.groups; ++g) {
+        int64_t K = 0;
+        for (int t = 0; t < 32 && g * 32 + t < nb; ++t) {
+            const int64_t j = order[g * 32 + t];
+            s.grp_bdd[g * 32 + t] = (int32_t)j;
+            K = std::max(K, nlay(j));
+        }
+        s.grp_npos[g] = (int32_t)K;
+        for (int64_t k = 0; k < K; ++k) {
+            int64_t w = 0;
+            for (int t = 0; t < 32; ++t) {
+                const int32_t j = s.grp_bdd[g * 32 + t];
+                if (j < 0 || k >= nlay(j)) continue;
+                const int64_t l = bdd_layer_lo[j + 1] - 1 - k;
+                w = std::max(w, lnl[l + 1] - lnl[l]);
+            }
+            s.pos_width.push_back((int32_t)w);
+            s.pos_slot.push_back(slots);
+            slots += w;
+            s.max_width = std::max<int64_t>(s.max_width, w);
+        }
+        s.grp_pos_lo[g + 1] = (int64_t)s.pos_width.size();
+    }
+    if (slots * 32 >= INT32_MAX) {
+        set_error("sweep layout exceeds the int32 element range");
+        return DM_ERR_UNSUPPORTED;
+    }
+    s.slots = slots;
+    s.zl.assign(slots * 32, kFalse);
+    s.ol.assign(slots * 32, kFalse);
+    for (int64_t g = 0; g < s.groups; ++g) {
+        const int64_t p0 = s.grp_pos_lo[g];
+        for (int t = 0; t < 32; ++t) {
+            const int32_t j = s.grp_bdd[g * 32 + t];
+            if (j < 0) continue;
+            for (int64_t k = 0; k < nlay(j); ++k) {
+                const int64_t l = bdd_layer_lo[j + 1] - 1 - k;
+                const int64_t next0 = lnl[l + 1];
+                for (int64_t v = lnl[l]; v < lnl[l + 1]; ++v) {
+                    const int64_t at = (s.pos_slot[p0 + k] + (v - lnl[l])) * 32 + t;
+                    const int64_t a = zero_t[v], b = one_t[v];
+                    s.zl[at] = (int32_t)(a >= 0 ? a - next0 : a);
+                    s.ol[at] = (int32_t)(b >= 0 ? b - next0 : b);
+                }
+            }
+        }
+    }
+    return DM_OK;
+}
+
+}  // namespace dm

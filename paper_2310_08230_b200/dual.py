@@ -148,7 +148,9 @@ class DualState:
     def eval_step(self, d: torch.Tensor, gamma: float) -> float:
         """Objective at lam + gamma*d without materialising it (fused trial)."""
         ev = self.pass_timer.begin("backward_trial") if self.pass_timer else None
-        self.dev.k_backward_trial(self.lam_d, d, gamma, self._scratch(), self._scratch_bounds)
+        # trial distances are scratch in the reference (dual.py:99-106): only
+        # the per-diagram optima are produced, no distance table is written
+        self.dev.k_backward_trial(self.lam_d, d, gamma, None, self._scratch_bounds)
         if ev:
             self.pass_timer.end(ev)
         self.sweeps += 1

@@ -101,9 +101,11 @@ class DeviceFlat:
     def k_mma_backward(self, lam, F, B, bounds):
         _native.call("dm_k_mma_backward", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(bounds), self._s())
 
-    def set_mma_config(self, threads: int = 256, blocks_per_sm: int = 2, sleep_ns: int = 0):
+    def set_mma_config(self, threads: int = 256, blocks_per_sm: int = 2, sleep_ns: int = 0, probe: bool = False,
+                       lookahead: int = 3):
         """Launch shape of the exact passes (see dm_flat_set_mma_config)."""
-        _native.call("dm_flat_set_mma_config", self._h, int(threads), int(blocks_per_sm), int(sleep_ns))
+        _native.call("dm_flat_set_mma_config", self._h, int(threads), int(blocks_per_sm), int(sleep_ns), int(probe),
+                     int(lookahead))
         info = _native.FlatInfo()
         _native.check(_native.load().dm_flat_get_info(self._h, ctypes.byref(info)), "dm_flat_get_info")
         self.info = {k: getattr(info, k) for k, _ in _native.FlatInfo._fields_}

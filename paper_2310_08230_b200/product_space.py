@@ -219,7 +219,8 @@ def _canonical_rotation(m, n):
 
 
 def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray,
-                        order: str = "colour", allowed: np.ndarray | None = None) -> ProductSpace:
+                        order: str = "colour", allowed: np.ndarray | None = None,
+                        order_seed: int = 2) -> ProductSpace:
     """Enumerate P, order the variables, assemble rows and Eq. (2) costs.
 
     ``allowed`` (optional, bool (|V_M|, |V_N|)) keeps only product triangles
@@ -235,28 +236,36 @@ def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray
     VM, VN = M.num_vertices, N.num_vertices
     T = max(TM, TN)
     rotN = np.stack([FN[:, [(k + s) % 3 for k in range(3)]] for s in range(3)], 1)  # (TN,3,3)
+    # colour shifts: a random Latin square for the face pairs and a per-face
+    # cyclic shift of each degenerate class (a bijection inside every A^M /
+    # A^N row), which keeps boundary rows from chaining same-colour
+    # variables of neighbouring faces
+    rng = np.random.default_rng(order_seed)
+    piM, piN = rng.permutation(T), rng.permutation(T)
+    shift_te, shift_tv = rng.integers(0, len(E6N), TM), rng.integers(0, VN, TM)
+    shift_et, shift_vt = rng.integers(0, len(E6M), TN), rng.integers(0, VM, TN)
 
     parts = []  # (m, n, kind, face_m, face_n, colour)
     # tri-tri: M face f in stored rotation, N face g rotated by s
     f, g, s = np.meshgrid(np.arange(TM), np.arange(TN), np.arange(3), indexing="ij")
     f, g, s = f.ravel(), g.ravel(), s.ravel()
-    parts.append((FM[f], rotN[g, s], TRI_TRI, f, g, 3 * ((f + g) % T) + s))
+    parts.append((FM[f], rotN[g, s], TRI_TRI, f, g, 3 * ((piM[f] + piN[g]) % T) + s))
     # tri-edge / tri-vertex: M face, N degenerate element
     f, t = np.meshgrid(np.arange(TM), np.arange(len(E6N)), indexing="ij")
     f, t = f.ravel(), t.ravel()
-    parts.append((FM[f], E6N[t], TRI_EDGE, f, np.full_like(f, -1), 3 * T + t))
+    parts.append((FM[f], E6N[t], TRI_EDGE, f, np.full_like(f, -1), 3 * T + (t + shift_te[f]) % len(E6N)))
     f, v = np.meshgrid(np.arange(TM), np.arange(VN), indexing="ij")
     f, v = f.ravel(), v.ravel()
     parts.append((FM[f], np.stack([v, v, v], 1), TRI_VERTEX, f, np.full_like(f, -1),
-                  3 * T + len(E6N) + v))
+                  3 * T + len(E6N) + (v + shift_tv[f]) % VN))
     # edge-tri / vertex-tri: M degenerate element, N face g in stored rotation
     t, g = np.meshgrid(np.arange(len(E6M)), np.arange(TN), indexing="ij")
     t, g = t.ravel(), g.ravel()
-    parts.append((E6M[t], FN[g], EDGE_TRI, np.full_like(g, -1), g, 3 * T + t))
+    parts.append((E6M[t], FN[g], EDGE_TRI, np.full_like(g, -1), g, 3 * T + (t + shift_et[g]) % len(E6M)))
     v, g = np.meshgrid(np.arange(VM), np.arange(TN), indexing="ij")
     v, g = v.ravel(), g.ravel()
     parts.append((np.stack([v, v, v], 1), FN[g], VERTEX_TRI, np.full_like(g, -1), g,
-                  3 * T + len(E6M) + v))
+                  3 * T + len(E6M) + (v + shift_vt[g]) % VM))
 
     m = np.concatenate([p[0] for p in parts]).astype(np.int64)
     n = np.concatenate([p[1] for p in parts]).astype(np.int64)

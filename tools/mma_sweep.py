@@ -28,15 +28,15 @@ def main():
     results = []
     ref = None
     configs = []
-    for threads in (256, 128, 64):
-        for bps in (1, 2, 4, 8):
-            for sleep in (0, 64, 256):
-                configs.append((threads, bps, sleep))
-    for threads, bps, sleep in configs:
+    for warm in (0, 1):
+        for probe in (0, 1):
+            for threads, bps in ((128, 1), (256, 2)):
+                configs.append((threads, bps, 0, probe, warm << 16))
+    for threads, bps, sleep, probe, look in configs:
         try:
-            st.dev.set_mma_config(threads, bps, sleep)
+            st.dev.set_mma_config(threads, bps, sleep, probe, look)
         except Exception as exc:  # occupancy limits
-            results.append({"threads": threads, "bps": bps, "sleep": sleep, "error": str(exc)})
+            results.append({"threads": threads, "bps": bps, "sleep": sleep, "probe": probe, "look": look, "error": str(exc)})
             continue
         times = []
         for rep in range(2):
@@ -55,7 +55,7 @@ def main():
         key = h(st.lam_d)
         ref = ref or key
         fw, bw = min(t[0] for t in times), min(t[1] for t in times)
-        r = {"threads": threads, "bps": bps, "sleep": sleep, "grid": st.dev.info["mma_grid"], "fw_ms": fw,
+        r = {"threads": threads, "bps": bps, "sleep": sleep, "probe": probe, "look": look, "grid": st.dev.info["mma_grid"], "fw_ms": fw,
              "bw_ms": bw, "exact": key == ref}
         print(json.dumps(r), flush=True)
         results.append(r)

@@ -1,0 +1,86 @@
+"""Per-level latency breakdown of the exact averaging passes (GPU tool).
+
+Stamps (%globaltimer) per lane: task start, inputs seen, outputs published.
+For every lane we find its producer (the copy at the previous layer of the
+same diagram) and split the critical chain into
+  comm  = inputs seen  - producer published
+  work  = published    - inputs seen
+"""
+
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from bench import build_instance  # noqa: E402
+from paper_2310_08230_b200 import _native  # noqa: E402
+from paper_2310_08230_b200.dual import BACKWARD, FORWARD, init_duals, mma_pass  # noqa: E402
+
+
+def analyse(st, forward, trace, name):
+    ntask = st.dev.info["fw_tasks" if forward else "bw_tasks"]
+    levels = np.zeros(ntask, np.int32)
+    layers = np.zeros(ntask * 32, np.int32)
+    _native.check(_native.load().dm_flat_task_levels(st.dev.handle, int(forward), levels.ctypes.data,
+                                                    layers.ctypes.data))
+    tr = trace.cpu().numpy().reshape(ntask * 32, 5).astype(np.int64)
+    act = layers >= 0
+    t0 = tr[act, 0].min()
+    start, own, seen, upd, done = (tr[:, k] - t0 for k in range(5))
+    own = np.where(tr[:, 1] == 0, seen, own)  # lanes without dependencies
+    lane_level = np.repeat(levels, 32)
+    # producer lane of each lane: layer l-1 (forward) / l+1 (backward) in the same diagram
+    f = st.flat
+    L = f.num_layers
+    slot_of_layer = np.full(L, -1, np.int64)
+    slot_of_layer[layers[act]] = np.flatnonzero(act)
+    layer_bdd = f.layer_bdd
+    lo, hi = f.bdd_layer_lo[layer_bdd], f.bdd_layer_lo[layer_bdd + 1]
+    l = layers.astype(np.int64)
+    has_pred = act.copy()
+    pred_layer = np.where(act, l - 1 if forward else l + 1, 0)
+    if forward:
+        has_pred &= l > lo[np.maximum(l, 0)]
+    else:
+        has_pred &= l + 1 < hi[np.maximum(l, 0)]
+    pslot = np.where(has_pred, slot_of_layer[np.clip(pred_layer, 0, L - 1)], -1)
+    waiting = has_pred.copy()
+    waiting[has_pred] = start[has_pred] < done[pslot[has_pred]]
+    comm = seen[waiting] - done[pslot[waiting]]
+    comm_own = own[waiting] - done[pslot[waiting]]
+    gate = seen[act] - own[act]
+    work = done[act] - seen[act]
+    wait_after_start = seen[act] - start[act]
+    lv_done = np.zeros(levels.max() + 1, np.int64)
+    np.maximum.at(lv_done, lane_level[act], done[act])
+    per_level = np.diff(lv_done)
+    q = lambda x: {k: float(np.percentile(x, p)) for k, p in (("p10", 10), ("p50", 50), ("p90", 90), ("max", 100))}
+    out = {"pass": name, "levels": int(levels.max() + 1), "total_ns": int(done[act].max()),
+           "ns_per_level_mean": float(done[act].max() / (levels.max() + 1)),
+           "level_advance_ns": q(per_level), "comm_waiting_ns": q(comm), "own_visible_ns": q(comm_own), "group_gate_ns": q(gate), "work_ns": q(work),
+           "average_ns": q(upd[act] - seen[act]), "publish_ns": q(done[act] - upd[act]),
+           "seen_minus_start_ns": q(wait_after_start),
+           "late_start_frac": float(np.mean(start[has_pred] > done[pslot[has_pred]]))}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    inst = build_instance(sys.argv[1] if len(sys.argv) > 1 else "c2", 0)
+    st = init_duals(inst, device="cuda:0")
+    for _ in range(2):
+        mma_pass(st, FORWARD)
+        mma_pass(st, BACKWARD)
+    for forward, name in ((True, "forward"), (False, "backward")):
+        ntask = st.dev.info["fw_tasks" if forward else "bw_tasks"]
+        trace = torch.zeros(ntask * 32 * 5, dtype=torch.int64, device=st.device)
+        _native.check(_native.load().dm_flat_set_trace(st.dev.handle, trace.data_ptr()))
+        mma_pass(st, FORWARD if forward else BACKWARD)
+        torch.cuda.synchronize()
+        _native.check(_native.load().dm_flat_set_trace(st.dev.handle, None))
+        analyse(st, forward, trace, name)
+
+
+if __name__ == "__main__":
+    main()
