@@ -196,6 +196,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def aggregate_work_time(work: float, ms: float, world: int, device=None):
+    """Whole-job aggregation over ranks: total work (sum) and the slowest
+    rank's time (max).  Works with the nccl (device tensor) and gloo (CPU)
+    backends; instance sharding needs no other collective."""
+    import torch
+
+    t = torch.tensor([float(work), float(ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        w, m = t[0:1].clone(), t[1:2].clone()
+        torch.distributed.all_reduce(w, op=torch.distributed.ReduceOp.SUM)
+        torch.distributed.all_reduce(m, op=torch.distributed.ReduceOp.MAX)
+        t = torch.cat([w, m])
+    return float(t[0]), float(t[1])
+
+
 def algorithmic_bytes(flat):
     """Per-launch algorithmic HBM bytes."""
     N, L, nb = flat.num_nodes, flat.num_layers, flat.num_bdds
@@ -251,14 +266,7 @@ def run_b200(args, rank, world, local_rank):
     launches = _native.launch_count - l0
     kt = timer.summary()
 
-    # whole-job aggregation: sum of work, max of time over ranks
-    t = torch.tensor([float(arcs), ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        tot = t.clone()
-        torch.distributed.all_reduce(tot[0:1], op=torch.distributed.ReduceOp.SUM)
-        torch.distributed.all_reduce(tot[1:2], op=torch.distributed.ReduceOp.MAX)
-        t = tot
-    total_arcs, max_ms = float(t[0]), float(t[1])
+    total_arcs, max_ms = aggregate_work_time(arcs, ms, world, dev)
     value = total_arcs / (max_ms / 1e3)
 
     result = None

@@ -30,7 +30,9 @@
 #include <map>
 #include <mutex>
 #include <memory>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dm_internal.h"
@@ -40,6 +42,7 @@
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int32_t kRelaxDesc = dm::kRelaxDescBit;
 constexpr unsigned long long kSentinel = 0x7ff4dead0badf00dULL;  // signalling-NaN payload
 
 __device__ __forceinline__ double ld_relaxed(const double *p) {
@@ -288,34 +291,51 @@ __device__ __forceinline__ double pw_elem(const double *__restrict__ a, const do
     return a[i];
 }
 
+// One leaf per 8 lanes: lane q of the octet owns numpy's accumulator r[q]
+// (elements q, q+8, q+16, ... of the leaf, summed in that order), so a warp
+// reads four contiguous 64-byte segments per step; the octet then combines
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with shuffles and lane 0 adds the
+// n % 8 tail sequentially — exactly loops_utils.h.src pairwise_sum's leaf.
 template <bool kDot>
 __global__ void pw_leaf_kernel(int32_t nleaves, const int64_t *__restrict__ leaf_off,
                                const int32_t *__restrict__ leaf_len, const double *__restrict__ a,
                                const double *__restrict__ b, double *__restrict__ vals) {
-    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= nleaves) return;
-    const int64_t off = leaf_off[k];
-    const int32_t n = leaf_len[k];
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t k = t >> 3;
+    const int q = threadIdx.x & 7;
+    const bool live = k < nleaves;
+    int64_t off = 0;
+    int32_t n = 0;
+    if (live) {
+        off = leaf_off[k];
+        n = leaf_len[k];
+    }
     const double *pa = a + off;
     const double *pb = kDot ? b + off : nullptr;
+    const int32_t stop = n - (n % 8);
+    double r = 0.0;
+    if (live && n >= 8) {
+        r = pw_elem<kDot>(pa, pb, q);
+        for (int32_t i = 8; i < stop; i += 8) r = __dadd_rn(r, pw_elem<kDot>(pa, pb, i + q));
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) within the octet
+    const double r1 = __shfl_xor_sync(0xffffffffu, r, 1);
+    const double s01 = (q & 1) ? __dadd_rn(r1, r) : __dadd_rn(r, r1);
+    const double s2 = __shfl_xor_sync(0xffffffffu, s01, 2);
+    const double s03 = (q & 2) ? __dadd_rn(s2, s01) : __dadd_rn(s01, s2);
+    const double s4 = __shfl_xor_sync(0xffffffffu, s03, 4);
+    const double s07 = (q & 4) ? __dadd_rn(s4, s03) : __dadd_rn(s03, s4);
+    if (!live || q != 0) return;
     double res;
+    int32_t i;
     if (n < 8) {
         res = 0.0;
-        for (int32_t i = 0; i < n; ++i) res = __dadd_rn(res, pw_elem<kDot>(pa, pb, i));
+        i = 0;
     } else {
-        double r[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] = pw_elem<kDot>(pa, pb, q);
-        const int32_t stop = n - (n % 8);
-        int32_t i = 8;
-        for (; i < stop; i += 8) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], pw_elem<kDot>(pa, pb, i + q));
-        }
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, pw_elem<kDot>(pa, pb, i));
+        res = s07;
+        i = stop;
     }
+    for (; i < n; ++i) res = __dadd_rn(res, pw_elem<kDot>(pa, pb, i));
     vals[k] = res;
 }
 
@@ -355,6 +375,7 @@ struct MmaArgs {
     int probe;                  // 1: poll one probe word before reading the layer; 0: poll all inputs
     unsigned long long *trace;  // optional [task*32+lane][5]: start, own inputs seen, group go, dual updated, published
     const int32_t *task_level;  // DAG level of each task
+    const uint64_t *task_relax;  // forward: per-lane relax descriptor (see build_relax_desc)
     int *progress;              // highest level of a finished task (monotone hint)
     int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
     int warm;                   // prefetch the polled lines into L2 at task start
@@ -469,6 +490,23 @@ __device__ __forceinline__ void layer_marginals(int32_t w, const double (&f)[W],
     m1 = tree_lmin<W>(c1);
 }
 
+// The reference's scatter for one target, in its order (used only to settle
+// the sign of a zero when a zero-arc and a one-arc candidate tie at 0).
+template <int W>
+__device__ __noinline__ double replay_scatter(int32_t w, const double (&f)[W], const int32_t (&z)[W],
+                                              const int32_t (&o)[W], int32_t tgt, double lam_l) {
+    double best = DM_INF;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (i < w && f[i] != DM_INF) {
+            if (z[i] == tgt && f[i] < best) best = f[i];
+            const double c = __dadd_rn(f[i], lam_l);
+            if (o[i] == tgt && c < best) best = c;
+        }
+    }
+    return best;
+}
+
 // Forward pass.  Warp w takes tasks w, w+W, ... (level order).  Inside a task
 // each variable (lane group) proceeds as soon as its own inputs are
 // published, independently of the other groups in the warp.
@@ -479,6 +517,7 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
     for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
         const int32_t l = a.task_layer[task * 32 + lane];
         const int32_t meta = a.task_meta[task * 32 + lane];
+        const uint64_t relax = a.task_relax[task * 32 + lane];
         const bool act = l >= 0;
         const bool last = meta & (1 << 17);
         int32_t nlo = 0, w = 0, n0 = 0, wn = 0;
@@ -552,35 +591,52 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             lam_l = lam_new;
             a.lam[l] = lam_l;
             if (a.trace) trace_mark(a, task, lane, 3, global_ns());
-            // propagate to the next layer (kernels.py:241-269): every target's
-            // value is the leftmost minimum over (v ascending, zero-arc,
-            // one-arc) of the reference's scatter, computed for all targets
-            // at once.
-            double c[W];
-#pragma unroll
-            for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
-            if (!last) {
+            // propagate to the next layer (kernels.py:241-269)
+            if (meta & kRelaxDesc) {
+                // Each target has at most one zero-arc source and one one-arc
+                // source (host-checked): value = first minimum of the two in
+                // the reference's scatter order (node ascending, zero first).
+                const uint64_t desc = relax;
+                const int nt = last ? 1 : wn;
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
-                    if (u < wn) {
-                        const int32_t tgt = n0 + u;
+                    if (u >= nt) break;
+                    const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
+                    double A = DM_INF, fo = DM_INF;  // register gathers f[zi], f[oi]
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        A = zi == i ? f[i] : A;
+                        fo = oi == i ? f[i] : fo;
+                    }
+                    const double c = __dadd_rn(fo, lam_l);
+                    const double v = (c < A || (c == A && oi < zi)) ? c : A;
+                    if (last)
+                        a.bounds[a.layer_bdd[l]] = v;
+                    else
+                        st_relaxed(a.F + n0 + u, v);
+                }
+            } else {
+                // general diagrams: leftmost-minimum tree over all candidates
+                double c[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < (last ? 1 : wn)) {
+                        const int32_t tgt = last ? dm::kTrue : n0 + u;
                         double cand[2 * W];
 #pragma unroll
                         for (int i = 0; i < W; ++i) {
                             cand[2 * i] = z[i] == tgt ? f[i] : DM_INF;
                             cand[2 * i + 1] = o[i] == tgt ? c[i] : DM_INF;
                         }
-                        st_relaxed(a.F + tgt, tree_lmin<2 * W>(cand));
+                        const double v = tree_lmin<2 * W>(cand);
+                        if (last)
+                            a.bounds[a.layer_bdd[l]] = v;
+                        else
+                            st_relaxed(a.F + tgt, v);
                     }
                 }
-            } else {
-                double cand[2 * W];
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    cand[2 * i] = z[i] == dm::kTrue ? f[i] : DM_INF;
-                    cand[2 * i + 1] = o[i] == dm::kTrue ? c[i] : DM_INF;
-                }
-                a.bounds[a.layer_bdd[l]] = tree_lmin<2 * W>(cand);
             }
             if (a.trace) trace_mark(a, task, lane, 4, global_ns());
         }
@@ -727,6 +783,7 @@ struct dm_flat {
     int *status = nullptr;  // device watchdog word of the exact passes
     int *progress = nullptr;  // progress hint word of the exact passes
     int32_t *fw_task_level = nullptr, *bw_task_level = nullptr;
+    uint64_t *fw_relax = nullptr;
     int mma_lookahead = 0;
     int mma_warm = 1;
     int mma_w = 8, mma_k = 8;
@@ -865,6 +922,10 @@ static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sl
 
 namespace {
 
+double host_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int env_int(const char *name, int dflt) {
     const char *v = std::getenv(name);
     return (v && *v) ? std::atoi(v) : dflt;
@@ -890,6 +951,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         return DM_ERR_INVALID;
     }
     *out = nullptr;
+    const double t_begin = host_seconds();
     const int64_t nb = desc->num_bdds, L = desc->num_layers, N = desc->num_nodes, P = desc->num_positions;
     if (nb < 0 || L < 0 || N < 0 || P < 0 || L >= INT32_MAX || N >= INT32_MAX - 2 || P >= INT32_MAX) {
         dm::set_error("instance sizes outside the int32 device layout");
@@ -943,11 +1005,34 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
             var_count[v] = (int32_t)(hi - lo);
         }
     }
+    const double t_valid = host_seconds();
+    // the two pass schedules and the sweep layout are independent host plans
     dm::MmaSchedule fw, bw;
-    int rc = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P, true, fw);
-    if (rc != DM_OK) return rc;
-    rc = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P, false, bw);
-    if (rc != DM_OK) return rc;
+    dm::SweepLayout sl;
+    int rc_fw = DM_OK, rc_bw = DM_OK, rc_sl = DM_OK;
+    std::string err_fw, err_bw, err_sl;
+    {
+        std::thread t_fw([&] {
+            rc_fw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
+                                           true, fw);
+            if (rc_fw) err_fw = dm_last_error();
+        });
+        std::thread t_bw([&] {
+            rc_bw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
+                                           false, bw);
+            if (rc_bw) err_bw = dm_last_error();
+        });
+        rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
+        if (rc_sl) err_sl = dm_last_error();
+        t_fw.join();
+        t_bw.join();
+    }
+    if (rc_fw) { dm::set_error(err_fw); return rc_fw; }
+    if (rc_bw) { dm::set_error(err_bw); return rc_bw; }
+    if (rc_sl) { dm::set_error(err_sl); return rc_sl; }
+    dm::build_relax_desc(bl, nb, lnl, desc->zero_t, desc->one_t, fw);
+    int rc = DM_OK;
+    const double t_plans = host_seconds();
 
     DM_CUDA(cudaSetDevice(device));
     cudaStream_t s = (cudaStream_t)stream;
@@ -990,14 +1075,14 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     f->bw_level = bw.task_level;
     f->fw_layer_h = fw.task_layer;
     f->bw_layer_h = bw.task_layer;
+    if ((rc = upload(f.get(), &f->fw_relax, fw.task_relax.data(), (int64_t)fw.task_relax.size(), s))) return rc;
+    DM_CUDA(cudaStreamSynchronize(s));
     if ((rc = up(&f->fw_layer, std::move(fw.task_layer)))) return rc;
     if ((rc = up(&f->fw_meta, std::move(fw.task_meta)))) return rc;
     if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
     if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
     if ((rc = up(&f->status, std::vector<int32_t>(1, 0)))) return rc;
     {
-        dm::SweepLayout sl;
-        if ((rc = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl))) return rc;
         int32_t *gb, *gn, *pw, *zl, *ol;
         int64_t *gp, *ps;
         if ((rc = up(&gb, std::move(sl.grp_bdd)))) return rc;
@@ -1030,6 +1115,9 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = get_plan(nb, &dummy))) return rc;
     if ((rc = get_plan(L, &dummy))) return rc;
     DM_CUDA(cudaStreamSynchronize(s));
+    if (env_int("DM_VERBOSE", 0))
+        std::fprintf(stderr, "[dm_flat_create] validate %.3fs, plans %.3fs, upload %.3fs\n", t_valid - t_begin,
+                     t_plans - t_valid, host_seconds() - t_plans);
     *out = f.release();
     return DM_OK;
 }
@@ -1159,6 +1247,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.probe = f->mma_probe;
     args.trace = f->trace;
     args.task_level = forward ? f->fw_task_level : f->bw_task_level;
+    args.task_relax = f->fw_relax;
     args.progress = f->progress;
     args.lookahead = f->mma_lookahead;
     args.warm = f->mma_warm;
@@ -1237,9 +1326,9 @@ static int pairwise(const double *a, const double *b, int64_t n, double *out, cu
     int rc = get_plan(n, &p);
     if (rc) return rc;
     if (b)
-        pw_leaf_kernel<true><<<blocks_for(p->nleaves, 128), 128, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, b, p->vals);
+        pw_leaf_kernel<true><<<blocks_for((int64_t)p->nleaves * 8, 256), 256, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, b, p->vals);
     else
-        pw_leaf_kernel<false><<<blocks_for(p->nleaves, 128), 128, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, nullptr, p->vals);
+        pw_leaf_kernel<false><<<blocks_for((int64_t)p->nleaves * 8, 256), 256, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, nullptr, p->vals);
     pw_combine_kernel<<<1, 1024, 0, s>>>(p->nleaves, p->maxh, p->height_lo, p->left, p->right, p->root, p->vals, out);
     return check_stream_error("pairwise sum");
 }

@@ -301,19 +301,19 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
                        const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,
                        const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &s) {
     (void)layer_var;
-    std::vector<int64_t> lbdd;
-    if (!layer_bdd) {
-        lbdd.resize(L);
-        for (int64_t j = 0; j < nb; ++j)
-            for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) lbdd[l] = j;
-        layer_bdd = lbdd.data();
-    }
+    (void)layer_bdd;
     // level of each position along the dependency DAG: a copy at layer l
     // depends on the copy at layer l-1 (forward) / l+1 (backward) of its
     // diagram, which the visitation order processes earlier.
     std::vector<int32_t> layer_level(L, 0);
     std::vector<int32_t> pos_level(npos, -1);
     int32_t depth = 0;
+    // first/last-layer flags packed above the level bits, filled in memory order
+    constexpr int32_t kFirstFlag = 1 << 29, kLastFlag = 1 << 30, kLevelMask = (1 << 29) - 1;
+    for (int64_t j = 0; j < nb; ++j) {
+        layer_level[bdd_layer_lo[j]] |= kFirstFlag;
+        layer_level[bdd_layer_lo[j + 1] - 1] |= kLastFlag;
+    }
     for (int64_t k = 0; k < npos; ++k) {
         const int64_t p = forward ? k : npos - 1 - k;
         const int64_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
@@ -326,11 +326,14 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
         int32_t lev = 0;
         for (int64_t t = lo; t < hi; ++t) {
             const int64_t l = proc_layers[t];
-            const int64_t j = layer_bdd[l];
-            if (forward && l > bdd_layer_lo[j]) lev = std::max(lev, layer_level[l - 1] + 1);
-            if (!forward && l + 1 < bdd_layer_lo[j + 1]) lev = std::max(lev, layer_level[l + 1] + 1);
+            // one cache line: the flags of l and the level of its neighbour
+            if (forward && !(layer_level[l] & kFirstFlag)) lev = std::max(lev, (layer_level[l - 1] & kLevelMask) + 1);
+            if (!forward && !(layer_level[l] & kLastFlag)) lev = std::max(lev, (layer_level[l + 1] & kLevelMask) + 1);
         }
-        for (int64_t t = lo; t < hi; ++t) layer_level[proc_layers[t]] = lev;
+        for (int64_t t = lo; t < hi; ++t) {
+            int32_t &slot = layer_level[proc_layers[t]];
+            slot = (slot & ~kLevelMask) | lev;
+        }
         pos_level[p] = lev;
         depth = std::max(depth, lev + 1);
     }
@@ -370,10 +373,9 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
         const size_t base = s.task_layer.size() - 32;
         for (int k = 0; k < c; ++k) {
             const int64_t l = proc_layers[lo + k];
-            const int64_t j = layer_bdd[l];
             int32_t meta = used | (c << 8);
-            if (l == bdd_layer_lo[j]) meta |= 1 << 16;
-            if (l + 1 == bdd_layer_lo[j + 1]) meta |= 1 << 17;
+            if (layer_level[l] & kFirstFlag) meta |= 1 << 16;
+            if (layer_level[l] & kLastFlag) meta |= 1 << 17;
             s.task_layer[base + used + k] = (int32_t)l;
             s.task_meta[base + used + k] = meta;
         }

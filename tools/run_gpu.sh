@@ -7,6 +7,7 @@ for step in "$@"; do
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log ;;
     sweep) timeout 900 python tools/mma_sweep.py c2 > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err; echo "sweep rc=$?" >> gpurun_out/sweep.err ;;
     pingpong) ./tools/pingpong > gpurun_out/pingpong.txt 2>&1 ;;
+    latency) ./tools/latency > gpurun_out/latency.txt 2>&1 ;;
     trace) timeout 600 python tools/mma_trace.py c2 > gpurun_out/trace.jsonl 2> gpurun_out/trace.err; echo "trace rc=$?" >> gpurun_out/trace.err ;;
     bench) timeout 900 python bench.py --steps 5 --warmup 2 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err ;;
   esac
