@@ -13,7 +13,7 @@ import os
 from .errors import EmptyFeasibleSet, NativeLibraryError, ProdmatchError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdiscomatch_b200.so")
+LIB_PATH = os.environ.get("DM_LIB_PATH") or os.path.join(_HERE, "libdiscomatch_b200.so")
 
 DM_OK = 0
 DM_ERR_INVALID = -1

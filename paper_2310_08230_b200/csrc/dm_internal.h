@@ -61,12 +61,8 @@ PairwisePlan plan_pairwise(int64_t n);
 // (bit 16) and last-layer flag (bit 17).
 struct MmaSchedule {
     std::vector<int32_t> task_layer, task_meta, task_level;
-    std::vector<uint64_t> task_relax;  // forward pass: per-lane relax descriptor
     int64_t depth = 0, tasks = 0;
 };
-constexpr int32_t kRelaxDescBit = 1 << 18;  // task_meta: lane has a relax descriptor
-void build_relax_desc(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_node_lo, const int64_t *zero_t,
-                      const int64_t *one_t, MmaSchedule &fw);
 int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_bdd_or_null,
                        const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,
                        const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &out);

@@ -91,65 +91,6 @@ int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
 
 }  // namespace dm
 
-namespace dm {
-
-// Relax descriptors of the forward exact pass: for every lane (one diagram
-// layer l) and every target u of layer l+1 (or the TRUE terminal of a last
-// layer, u = 0), the local index of its zero-arc source (bits 8u..8u+3) and
-// one-arc source (bits 8u+4..8u+7), 15 = none.  Lanes whose targets have
-// more than one source of a kind, or layers wider than 8, keep the general
-// path (meta bit kRelaxDescBit cleared).
-void build_relax_desc(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *lnl, const int64_t *zero_t,
-                      const int64_t *one_t, MmaSchedule &fw) {
-    // descriptors per layer, computed in memory order (the task order is by
-    // DAG level, i.e. random over the node table)
-    const int64_t L = nb ? bdd_layer_lo[nb] : 0;
-    std::vector<uint64_t> by_layer(L, ~0ull);
-    std::vector<uint8_t> valid(L, 0);
-    for (int64_t j = 0; j < nb; ++j)
-        for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
-            const bool last = l + 1 == bdd_layer_lo[j + 1];
-            const int64_t v0 = lnl[l], w = lnl[l + 1] - v0;
-            const int64_t n0 = lnl[l + 1];
-            const int64_t wn = last ? 1 : lnl[l + 2] - n0;
-            if (w > 8 || wn > 8) continue;
-            uint64_t desc = ~0ull;
-            bool ok = true;
-            auto put = [&](int64_t u, int shift, int64_t i) {
-                if (((desc >> (8 * u + shift)) & 15) != 15) {
-                    ok = false;
-                    return;
-                }
-                desc &= ~(15ull << (8 * u + shift));
-                desc |= (uint64_t)i << (8 * u + shift);
-            };
-            for (int64_t i = 0; i < w && ok; ++i) {
-                const int64_t a = zero_t[v0 + i], b = one_t[v0 + i];
-                if (last) {
-                    if (a == kTrue) put(0, 0, i);
-                    if (b == kTrue) put(0, 4, i);
-                } else {
-                    if (a >= 0) put(a - n0, 0, i);
-                    if (b >= 0) put(b - n0, 4, i);
-                }
-            }
-            if (ok) {
-                by_layer[l] = desc;
-                valid[l] = 1;
-            }
-        }
-    const size_t n = fw.task_layer.size();
-    fw.task_relax.assign(n, ~0ull);
-    for (size_t s = 0; s < n; ++s) {
-        const int64_t l = fw.task_layer[s];
-        if (l < 0 || !valid[l]) continue;
-        fw.task_relax[s] = by_layer[l];
-        fw.task_meta[s] |= kRelaxDescBit;
-    }
-}
-
-}  // namespace dm
-
 // Host-only timing of the plans dm_flat_create builds (test/profiling hook).
 #include <chrono>
 extern "C" int dm_debug_time_plans(const dm_flat_desc *d, double *seconds3) {
@@ -160,11 +101,13 @@ extern "C" int dm_debug_time_plans(const dm_flat_desc *d, double *seconds3) {
                                     d->proc_layers, d->num_positions, true, fw);
     if (rc) return rc;
     auto t1 = clk::now();
+    rc = dm::build_mma_schedule(d->bdd_layer_lo, d->num_bdds, nullptr, d->layer_var, d->num_layers, d->proc_ptr,
+                                d->proc_layers, d->num_positions, false, bw);
+    if (rc) return rc;
+    auto t2 = clk::now();
     dm::SweepLayout sl;
     rc = dm::build_sweep_layout(d->bdd_layer_lo, d->num_bdds, d->layer_node_lo, d->zero_t, d->one_t, sl);
     if (rc) return rc;
-    auto t2 = clk::now();
-    dm::build_relax_desc(d->bdd_layer_lo, d->num_bdds, d->layer_node_lo, d->zero_t, d->one_t, fw);
     auto t3 = clk::now();
     seconds3[0] = std::chrono::duration<double>(t1 - t0).count();
     seconds3[1] = std::chrono::duration<double>(t2 - t1).count();

@@ -1,0 +1,35 @@
+"""A/B timing of the exact passes across library builds (GPU tool).
+
+usage: python tools/ab_mma.py <lib.so> [<lib.so> ...]   (each in a fresh process)
+"""
+import json
+import os
+import subprocess
+import sys
+
+CHILD = r'''
+import os, sys, json, torch
+sys.path.insert(0, ".")
+from bench import build_instance
+from paper_2310_08230_b200 import _native
+from paper_2310_08230_b200.dual import init_duals, mma_pass, FORWARD, BACKWARD
+inst = build_instance("c2", 0)
+st = init_duals(inst, device="cuda:0")
+for _ in range(2):
+    mma_pass(st, FORWARD); mma_pass(st, BACKWARD)
+res = []
+for rep in range(3):
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize(); e[0].record()
+    st.dev.k_mma_forward(st.lam_d, st.F, st.B, st._bounds); e[1].record()
+    st.dev.k_mma_backward(st.lam_d, st.F, st.B, st._bounds); e[2].record()
+    torch.cuda.synchronize()
+    res.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])))
+print(json.dumps({"lib": os.environ["DM_LIB_PATH"], "fw_ms": min(r[0] for r in res), "bw_ms": min(r[1] for r in res),
+                  "lam_hash": __import__("hashlib").sha256(st.lam.tobytes()).hexdigest()[:16]}))
+'''
+
+for lib in sys.argv[1:]:
+    env = dict(os.environ, DM_LIB_PATH=os.path.abspath(lib))
+    out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+    print(out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:], flush=True)

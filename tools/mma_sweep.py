@@ -28,10 +28,11 @@ def main():
     results = []
     ref = None
     configs = []
-    for warm in (0, 1):
-        for probe in (0, 1):
-            for threads, bps in ((128, 1), (256, 2)):
-                configs.append((threads, bps, 0, probe, warm << 16))
+    for rep in range(2):
+        for relax in (0, 1):
+            for warm in (0, 1):
+                for threads, bps in ((128, 1), (256, 1)):
+                    configs.append((threads, bps, 0, 0, (warm << 16) | (relax << 17)))
     for threads, bps, sleep, probe, look in configs:
         try:
             st.dev.set_mma_config(threads, bps, sleep, probe, look)

@@ -63,6 +63,11 @@ def analyse(st, forward, trace, name):
            "average_ns": q(upd[act] - seen[act]), "publish_ns": q(done[act] - upd[act]),
            "seen_minus_start_ns": q(wait_after_start),
            "late_start_frac": float(np.mean(start[has_pred] > done[pslot[has_pred]]))}
+    late = has_pred.copy()
+    late[has_pred] = start[has_pred] > done[pslot[has_pred]]
+    if late.any():
+        out["late_by_ns"] = q(start[late] - done[pslot[late]])
+        out["late_seen_after_start_ns"] = q(own[late] - start[late])
     print(json.dumps(out), flush=True)
 
 

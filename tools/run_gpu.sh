@@ -10,5 +10,21 @@ for step in "$@"; do
     latency) ./tools/latency > gpurun_out/latency.txt 2>&1 ;;
     trace) timeout 600 python tools/mma_trace.py c2 > gpurun_out/trace.jsonl 2> gpurun_out/trace.err; echo "trace rc=$?" >> gpurun_out/trace.err ;;
     bench) timeout 900 python bench.py --steps 5 --warmup 2 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err ;;
+    ncu_list)
+      B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
+      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
+      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+          --log-file gpurun_out/launches.csv $B > gpurun_out/ncu.log 2>&1; echo "ncu_list rc=$?" >> gpurun_out/ncu.log ;;
+    ncu_full)
+      B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
+      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_forward -s 1 -c 1 \
+          -o gpurun_out/prof_mma_fw $B > gpurun_out/ncu_full.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:sweep_backward -s 3 -c 1 \
+          -o gpurun_out/prof_sweep $B >> gpurun_out/ncu_full.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:pw_leaf -s 20 -c 1 \
+          -o gpurun_out/prof_pwleaf $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full rc=$?" >> gpurun_out/ncu_full.log ;;
+    ab) timeout 1200 python tools/ab_mma.py tools/ab/*.so tools/ab/*.so > gpurun_out/ab.jsonl 2> gpurun_out/ab.err ;;
+    prof) timeout 900 python tools/step_profile.py > gpurun_out/step_profile.txt 2>&1 ;;
   esac
 done
