@@ -156,31 +156,47 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.samples = []  # (host time, line)
+        self.marks = []
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+
+        def reader():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self.samples.append((time.time(), line))
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
         return self
 
+    def mark(self):
+        self.marks.append(time.time())
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.thread.join(timeout=5)
 
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in getattr(self, "lines", []):
+        lo, hi = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0.0, float("inf"))
+        window = [l for t, l in self.samples if lo <= t <= hi + 0.2] or [l for _, l in self.samples]
+        for line in window:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -241,23 +257,33 @@ def run_b200(args, rank, world, local_rank):
     info = st.dev.info
     log(f"[bench] rank {rank}: exact-pass DAG depth fw {info['fw_depth']} bw {info['bw_depth']}, "
         f"tasks {info['fw_tasks']}, grid {info['mma_grid']}x{info['mma_block']}")
-    for _ in range(args.warmup):
-        run.step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    timer = KernelTimer()
-    st.pass_timer = timer
-    s0 = st.sweeps
-    l0 = _native.launch_count
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the clock sampler (nvidia-smi) starts before the warm-up: its start-up
+    # touches the driver and must not fall inside the timed region
     with ClockSampler(local_rank) as clk:
+        time.sleep(1.0)
+        for _ in range(args.warmup):
+            run.step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        timer = KernelTimer()
+        st.pass_timer = timer
+        s0 = st.sweeps
+        l0 = _native.launch_count
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clk.mark()
         torch.cuda.synchronize()
         start.record()
+        step_wall = []
         for _ in range(args.steps):
+            t_s = time.perf_counter()
+            sw0 = st.sweeps
             run.step()
+            step_wall.append((round((time.perf_counter() - t_s) * 1e3, 2), st.sweeps - sw0))
         end.record()
         torch.cuda.synchronize()
+        clk.mark()
+        log(f"[bench] per-step host wall ms / sweeps: {step_wall}")
     if world > 1:
         torch.distributed.barrier()
     st.pass_timer = None

@@ -120,9 +120,11 @@ int dm_flat_status(dm_flat *flat, void *stream);
  * unsuccessful polls, the poll mode (probe != 0: poll one probe word
  * before reading the inputs; 0: poll all inputs) and the progress lookahead
  * (a warp polls its inputs only once a task within `lookahead` levels of its
- * own has finished; 0 disables the gating).  Defaults come from
- * DM_MMA_THREADS / DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS / DM_MMA_PROBE /
- * DM_MMA_LOOKAHEAD. */
+ * own has finished; 0 disables the gating) in bits 0-15 of `lookahead`;
+ * bit 16 enables L2 warming of the polled lines, bit 17 forces the generic
+ * tree publish in the forward pass instead of the per-layer descriptors.
+ * Defaults come from DM_MMA_THREADS / DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS /
+ * DM_MMA_PROBE / DM_MMA_LOOKAHEAD / DM_MMA_WARM / DM_MMA_DESC. */
 int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns, int probe,
                            int lookahead);
 /* Profiling hooks: a device buffer of tasks*32*5 u64 receives, per lane,
@@ -166,14 +168,26 @@ int dm_lambda_sums(const dm_flat *f, const double *lam, double *sums_by_var, voi
 int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, int8_t *agrees,
                         double *score, int8_t *preferred, void *stream);
 
-/* numpy pairwise summation order (np.add.reduce on contiguous float64):
- * out[0] = 0.0 + pairwise(x[0:n]).  dm_dot uses the same tree on the
- * elementwise products, i.e. exactly np.sum(a * b).  Results land in device
+/* dm_sum: numpy pairwise summation order (np.add.reduce on contiguous
+ * float64): out[0] = 0.0 + pairwise(x[0:n]) — bit-identical to the
+ * reference's bound sums.  dm_dot: the fixed inner-product order of the
+ * L-BFGS path — numpy pairwise over each 4096-element chunk of a*b, then
+ * over the chunk totals (n <= 4096^2); the reference's OpenBLAS ddot order
+ * is host-dependent, so any fixed order is parity-equivalent.  Results land in device
  * memory.  Reduction trees are planned once per (device, length) and cached
  * for the process; reductions of the same length must not run concurrently
  * on two streams of one device. */
 int dm_sum(const double *x, int64_t n, double *out, void *stream);
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream);
+
+/* L-BFGS two-loop recursion (reference qn.py:95-115, lbfgs_direction):
+ * d = H*g from m curvature pairs, newest first — s[i], y[i] device vectors of
+ * length n, rho[i] = 1/sy[i] and sy[i] = s[i].y[i] host scalars.  Each launch
+ * fuses one update with the next inner product (dm_dot order), so d is
+ * bit-identical to the dm_dot / dm_axpy_dev / dm_scale_dev / dm_lbfgs_up
+ * sequence; 2m+2 launches, m <= 64.  Shares dm_dot's per-length scratch. */
+int dm_lbfgs_direction(const double *g, const double *const *s, const double *const *y, const double *rho,
+                       const double *sy, int m, int64_t n, double *d, void *stream);
 
 /* Elementwise updates with numpy's rounding (no contraction):
  *   dm_axpy_dev : x[i] = x[i] - (alpha_host * dot_dev[0]) * y[i]            (qn.py:108-109)

@@ -8,9 +8,9 @@ Reductions: the reference sums per-diagram optima with ``ndarray.sum``
 (numpy pairwise summation, dual.py:67,106) — reused here unchanged.  Its
 inner products go through OpenBLAS ``ddot`` (qn.py:89,107,111,113), whose
 summation order depends on the host's thread count; ``dot="blas"`` keeps
-that (used to pin against the reference), ``dot="pairwise"`` uses
-``np.sum(a * b)`` — the order the B200 path implements — so GPU and oracle
-agree bit-for-bit in hybrid mode too.
+that (used to pin against the reference), ``dot="chunked"`` uses the
+B200 path's fixed order (numpy pairwise per 4096-element chunk, then over
+the chunk totals) so GPU and oracle agree bit-for-bit in hybrid mode too.
 """
 
 from __future__ import annotations
@@ -30,8 +30,25 @@ def _dot_blas(a, b):
     return float(a @ b)
 
 
-def _dot_pairwise(a, b):
-    return float(np.sum(a * b))
+DOT_CHUNK = 4096
+
+
+def _dot_chunked(a, b):
+    """The B200 path's inner-product order (csrc/dm_sweep.cu chunk_dot):
+    numpy pairwise over 4096-element chunks of a*b, then numpy pairwise over
+    the chunk totals."""
+    p = a * b
+    n = len(p)
+    if n == 0:
+        return 0.0
+    full = n // DOT_CHUNK
+    sums = list(np.sum(p[: full * DOT_CHUNK].reshape(-1, DOT_CHUNK), axis=1)) if full else []
+    if n % DOT_CHUNK:
+        sums.append(np.sum(p[full * DOT_CHUNK:]))
+    return float(np.sum(np.asarray(sums, dtype=np.float64)))
+
+
+_dot_pairwise = _dot_chunked  # name kept for callers of the previous order
 
 
 class OracleDual:
@@ -213,7 +230,7 @@ def solve(inst: OracleInstance, mode="hybrid", max_iterations=2000, dual_toleran
     """qn.py:184-259; returns (state, records[(it, kind, bound, t)], stop_reason)."""
     if threads is not None:
         lib.oracle_set_threads(int(threads))
-    dotf = _dot_blas if dot == "blas" else _dot_pairwise
+    dotf = _dot_blas if dot == "blas" else _dot_chunked
     hybrid = mode == "hybrid"
     t0 = clock()
     st = init_duals(inst, flat)

@@ -319,6 +319,7 @@ struct MmaArgs {
     int *progress;              // highest level of a finished task (monotone hint)
     int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
     int warm;                   // prefetch the polled lines into L2 at task start
+    const uint64_t *relax_layer;  // per-layer source nibbles (forward, W == 8 only)
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -433,7 +434,7 @@ __device__ __forceinline__ void layer_marginals(int32_t w, const double (&f)[W],
 // Forward pass.  Warp w takes tasks w, w+W, ... (level order).  Inside a task
 // each variable (lane group) proceeds as soon as its own inputs are
 // published, independently of the other groups in the warp.
-template <int W, int K>
+template <int W, int K, bool D = false>
 __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         const int32_t meta = a.task_meta[task * 32 + lane];
         const bool act = l >= 0;
         const bool last = meta & (1 << 17);
+        const uint64_t desc = (D && act) ? a.relax_layer[l] : 0ull;
         int32_t nlo = 0, w = 0, n0 = 0, wn = 0;
         double lam_l = 0.0;
         int32_t z[W], o[W];
@@ -520,7 +522,23 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             double c[W];
 #pragma unroll
             for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
-            if (!last) {
+            if (!last && D) {
+                // host-built per-layer source nibbles (dm_layout.cpp
+                // build_relax_by_layer): at most one zero- and one one-arc
+                // source per target, so the leftmost minimum is one compare.
+                double fl[W], cl[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) fl[i] = f[i], cl[i] = c[i];
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if (u < wn) {
+                        const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
+                        const double A = zi < W ? fl[zi] : DM_INF;
+                        const double C = oi < W ? cl[oi] : DM_INF;
+                        st_relaxed(a.F + n0 + u, (C < A || (C == A && oi < zi)) ? C : A);
+                    }
+                }
+            } else if (!last) {
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     if (u < wn) {
@@ -691,6 +709,9 @@ struct dm_flat {
     int32_t *fw_task_level = nullptr, *bw_task_level = nullptr;
     int mma_lookahead = 0;
     int mma_warm = 1;
+    uint64_t *relax_layer = nullptr;  // forward publish descriptors (W == 8 instances)
+    bool relax_ok = false;
+    bool mma_desc = true;
     int mma_w = 8, mma_k = 8;
     int mma_threads = 256, mma_blocks_per_sm = 0;
     unsigned mma_sleep_ns = 0;
@@ -773,10 +794,21 @@ int get_plan(int64_t n, DevPlan **out) {
 inline int blocks_for(int64_t n, int threads) { return (int)std::max<int64_t>(1, (n + threads - 1) / threads); }
 inline int grid_stride_blocks(int64_t n) { return (int)std::min<int64_t>(148 * 16, std::max<int64_t>(1, (n + 255) / 256)); }
 
+// The descriptor-driven forward publish is a separate instantiation, used only
+// when every non-final layer of the instance has one source per arc kind.
+template <int W, int K>
+const void *mma_fn(const dm_flat *f, bool forward) {
+    if (!forward) return (const void *)mma_backward_kernel<W, K>;
+    if constexpr (W == 8) {
+        if (f->relax_ok && f->mma_desc) return (const void *)mma_forward_kernel<8, K, true>;
+    }
+    return (const void *)mma_forward_kernel<W, K, false>;
+}
+
 template <int W, int K>
 int launch_mma(const dm_flat *f, bool forward, MmaArgs &args, cudaStream_t s) {
     void *params[] = {&args};
-    const void *fn = forward ? (const void *)mma_forward_kernel<W, K> : (const void *)mma_backward_kernel<W, K>;
+    const void *fn = mma_fn<W, K>(f, forward);
     const int grid = forward ? f->mma_grid_fw : f->mma_grid_bw;
     DM_CUDA(cudaLaunchCooperativeKernel(fn, grid, f->mma_threads, params, 0, s));
     return DM_OK;
@@ -784,11 +816,11 @@ int launch_mma(const dm_flat *f, bool forward, MmaArgs &args, cudaStream_t s) {
 
 // Persistent grid: min(requested, resident) blocks per SM x SM count.
 template <int W, int K>
-int mma_grid_for(bool forward, int threads, int want_per_sm, int *grid) {
+int mma_grid_for(const dm_flat *f, bool forward, int threads, int want_per_sm, int *grid) {
     int dev, sms, per;
     DM_CUDA(cudaGetDevice(&dev));
     DM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const void *fn = forward ? (const void *)mma_forward_kernel<W, K> : (const void *)mma_backward_kernel<W, K>;
+    const void *fn = mma_fn<W, K>(f, forward);
     DM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0));
     if (per < 1) {
         dm::set_error("exact averaging kernel cannot be resident");
@@ -809,13 +841,14 @@ int mma_grid_for(bool forward, int threads, int want_per_sm, int *grid) {
 static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sleep_ns, int probe, int lookahead) {
     f->mma_lookahead = lookahead < 0 ? 0 : (lookahead & 0xffff);
     f->mma_warm = (lookahead >> 16) & 1;   // bit 16 of the lookahead word: L2 warming
+    f->mma_desc = !((lookahead >> 17) & 1);  // bit 17: force the tree publish
     if (threads < 32 || threads > 256 || threads % 32) {
         dm::set_error("exact-pass block size must be a multiple of 32 in [32, 256]");
         return DM_ERR_INVALID;
     }
 #define DM_GRID(W, K)                                                          \
-    (mma_grid_for<W, K>(true, threads, blocks_per_sm, &f->mma_grid_fw) ||      \
-     mma_grid_for<W, K>(false, threads, blocks_per_sm, &f->mma_grid_bw))
+    (mma_grid_for<W, K>(f, true, threads, blocks_per_sm, &f->mma_grid_fw) ||      \
+     mma_grid_for<W, K>(f, false, threads, blocks_per_sm, &f->mma_grid_bw))
     if (DM_MMA_DISPATCH(f, DM_GRID)) return DM_ERR_CUDA;
 #undef DM_GRID
     f->mma_threads = threads;
@@ -914,6 +947,8 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     // the two pass schedules and the sweep layout are independent host plans
     dm::MmaSchedule fw, bw;
     dm::SweepLayout sl;
+    std::vector<uint64_t> relax;
+    bool relax_ok = false;
     int rc_fw = DM_OK, rc_bw = DM_OK, rc_sl = DM_OK;
     std::string err_fw, err_bw, err_sl;
     {
@@ -929,6 +964,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         });
         rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
         if (rc_sl) err_sl = dm_last_error();
+        relax_ok = max_width <= 8 && dm::build_relax_by_layer(bl, nb, lnl, desc->zero_t, desc->one_t, relax);
         t_fw.join();
         t_bw.join();
     }
@@ -984,6 +1020,10 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
     if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
     if ((rc = up(&f->status, std::vector<int32_t>(1, 0)))) return rc;
+    if (relax_ok) {
+        if ((rc = upload(f.get(), &f->relax_layer, relax.data(), L, s))) return rc;
+        f->relax_ok = true;
+    }
     {
         int32_t *gb, *gn, *pw, *zl, *ol;
         int64_t *gp, *ps;
@@ -1011,7 +1051,8 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     f->mma_k = max_degree <= 8 ? 8 : 32;
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 2),
                        (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
-                       env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16));
+                       env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16) |
+                           ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17));
     if (rc) return rc;
     DevPlan *dummy;
     if ((rc = get_plan(nb, &dummy))) return rc;
@@ -1152,6 +1193,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.progress = f->progress;
     args.lookahead = f->mma_lookahead;
     args.warm = f->mma_warm;
+    args.relax_layer = f->relax_layer;
     DM_CUDA(cudaMemsetAsync(f->progress, 0xff, sizeof(int), s));  // -1: nothing finished
 #define DM_LAUNCH(W, K) launch_mma<W, K>(f, forward, args, s)
     return DM_MMA_DISPATCH(f, DM_LAUNCH);
@@ -1238,12 +1280,73 @@ int dm_sum(const double *x, int64_t n, double *out, void *stream) {
     return pairwise(x, nullptr, n, out, (cudaStream_t)stream);
 }
 
+// Per-(device, length) scratch of the chunked dot: chunk totals and the
+// two-loop scalars (same single-stream contract as the pairwise plans).
+struct DotScratch {
+    double *partial = nullptr;  // chunk totals
+    double *slots = nullptr;    // two-loop scalars (dm_lbfgs_direction)
+};
+static std::map<std::pair<int, int64_t>, DotScratch> g_dot;
+constexpr int kMaxPairs = 64;
+
+static int dot_scratch(int64_t n, bool slots, DotScratch **out) {
+    const int64_t nch = (n + dm::kDotChunk - 1) / dm::kDotChunk;
+    int dev;
+    DM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    auto key = std::make_pair(dev, n);
+    auto it = g_dot.find(key);
+    if (it == g_dot.end()) {
+        DotScratch d;
+        DM_CUDA(cudaMalloc((void **)&d.partial, nch * sizeof(double)));
+        it = g_dot.emplace(key, d).first;
+    }
+    if (slots && !it->second.slots) DM_CUDA(cudaMalloc((void **)&it->second.slots, (3 * kMaxPairs + 1) * sizeof(double)));
+    *out = &it->second;
+    return DM_OK;
+}
+
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream) {
-    if (!b && n > 0) {
-        dm::set_error("dm_dot needs two vectors");
+    if (!a || !b || !out || n < 0) {
+        if (n == 0 && out) {
+            cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream);  // empty dot = 0.0
+            return check_stream_error("dm_dot");
+        }
+        dm::set_error("dm_dot needs two vectors and an output");
         return DM_ERR_INVALID;
     }
-    return pairwise(a, b, n, out, (cudaStream_t)stream);
+    if (n == 0) {
+        DM_CUDA(cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream));
+        return DM_OK;
+    }
+    const int64_t nch = (n + dm::kDotChunk - 1) / dm::kDotChunk;
+    if (nch > dm::kDotChunk) {
+        dm::set_error("dm_dot: length above 4096*4096 not supported");
+        return DM_ERR_UNSUPPORTED;
+    }
+    DotScratch *sc;
+    if (int rc = dot_scratch(n, false, &sc)) return rc;
+    return dm::chunk_dot(a, b, n, sc->partial, out, stream);
+}
+
+int dm_lbfgs_direction(const double *g, const double *const *s, const double *const *y, const double *rho,
+                       const double *sy, int m, int64_t n, double *d, void *stream) {
+    if (!g || !s || !y || !rho || !sy || !d || m < 1 || m > kMaxPairs || n < 1) {
+        dm::set_error("dm_lbfgs_direction: needs g, d, 1 <= m <= 64 pairs and n >= 1");
+        return DM_ERR_INVALID;
+    }
+    if ((n + dm::kDotChunk - 1) / dm::kDotChunk > dm::kDotChunk) {
+        dm::set_error("dm_lbfgs_direction: length above 4096*4096 not supported");
+        return DM_ERR_UNSUPPORTED;
+    }
+    for (int i = 0; i < m; ++i)
+        if (!s[i] || !y[i]) {
+            dm::set_error("dm_lbfgs_direction: null pair vector");
+            return DM_ERR_INVALID;
+        }
+    DotScratch *sc;
+    if (int rc = dot_scratch(n, true, &sc)) return rc;
+    return dm::lbfgs_two_loop(g, s, y, rho, sy, m, n, d, sc->slots, sc->partial, stream);
 }
 
 int dm_axpy_dev(double *x, const double *y, double alpha_host, const double *dot_dev, double *alpha_out, int64_t n,

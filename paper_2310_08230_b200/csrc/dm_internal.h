@@ -82,6 +82,13 @@ struct SweepLayout {
 int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_node_lo,
                        const int64_t *zero_t, const int64_t *one_t, SweepLayout &out);
 
+// Per-layer forward publish descriptors: for each non-final layer, nibble
+// 8u (8u+4) names the node whose zero (one) arc enters target u of the next
+// layer, 15 = none.  False when a layer is wider than 8 or a target has two
+// sources of one arc kind (the tree publish handles those instances).
+bool build_relax_by_layer(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_node_lo,
+                          const int64_t *zero_t, const int64_t *one_t, std::vector<uint64_t> &desc_out);
+
 // Device view of a SweepLayout plus the reference-layout offsets the sweeps
 // need to read duals and write distances (dm_sweep.cu).
 struct SweepDev {
@@ -97,5 +104,13 @@ int sweep_backward(const SweepDev &s, const double *lam, const double *d, double
                    double *bounds, void *stream);
 // kernels.py:123-159
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream);
+// Chunked inner product (dm_sweep.cu): partial[nchunks] scratch, counter a
+// zeroed device word; requires nchunks = ceil(n / 4096) <= 4096.
+int chunk_dot(const double *a, const double *b, int64_t n, double *partial, double *out, void *stream);
+constexpr int64_t kDotChunk = 4096;
+// L-BFGS two-loop direction (qn.py:95-115) in 2m+2 fused launches; s/y are
+// host arrays of m device pointers (newest first), slots >= 3m+1 doubles.
+int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
+                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
 
 }  // namespace dm

@@ -114,3 +114,41 @@ extern "C" int dm_debug_time_plans(const dm_flat_desc *d, double *seconds3) {
     seconds3[2] = std::chrono::duration<double>(t3 - t2).count();
     return DM_OK;
 }
+
+namespace dm {
+
+// Forward relax descriptors, one per layer l (targets in layer l+1, or the
+// TRUE terminal for a last layer at u = 0): bits 8u..8u+3 = local index of
+// the zero-arc source of target u, bits 8u+4..8u+7 = its one-arc source,
+// 15 = none.  Returns false when some layer is wider than 8 or has a target
+// with two sources of one kind (then the tree-min kernel is used).
+bool build_relax_by_layer(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *lnl, const int64_t *zero_t,
+                          const int64_t *one_t, std::vector<uint64_t> &desc_out) {
+    const int64_t L = nb ? bdd_layer_lo[nb] : 0;
+    desc_out.assign(L, ~0ull);
+    for (int64_t j = 0; j < nb; ++j)
+        for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
+            if (l + 1 == bdd_layer_lo[j + 1]) continue;  // last layers keep the tree path
+            const int64_t v0 = lnl[l], w = lnl[l + 1] - v0;
+            const int64_t n0 = lnl[l + 1];
+            const int64_t wn = lnl[l + 2] - n0;
+            if (w > 8 || wn > 8) return false;
+            uint64_t desc = ~0ull;
+            for (int64_t i = 0; i < w; ++i) {
+                const int64_t t[2] = {zero_t[v0 + i], one_t[v0 + i]};
+                for (int k = 0; k < 2; ++k) {
+                    if (t[k] < 0) continue;  // terminal
+                    const int64_t u = t[k] - n0;
+                    if (u < 0 || u >= wn) return false;
+                    const int sh = 8 * (int)u + 4 * k;
+                    if (((desc >> sh) & 15) != 15) return false;
+                    desc &= ~(15ull << sh);
+                    desc |= (uint64_t)i << sh;
+                }
+            }
+            desc_out[l] = desc;
+        }
+    return true;
+}
+
+}  // namespace dm

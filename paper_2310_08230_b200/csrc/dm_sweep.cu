@@ -41,30 +41,58 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
     const int64_t p0 = s.grp_pos_lo[g];
     double *nb = sm + threadIdx.x;                       // distances of position k-1 (next layer)
     double *cur = sm + W * kSweepThreads + threadIdx.x;  // distances of position k
+    // Register double buffer: the arc targets and dual of position k+1 are
+    // loaded while position k is computed, so each step waits on shared
+    // memory only (the sweep is otherwise one DRAM round trip per layer).
+    int32_t za[W], oa[W];
+    double lam_n = 0.0, d_n = 0.0;
+    auto fetch = [&](int32_t k, int32_t &w, int64_t &slot) {
+        w = s.pos_width[p0 + k];
+        slot = s.pos_slot[p0 + k];
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w) {
+                za[i] = s.zl[(slot + i) * 32 + lane];
+                oa[i] = s.ol[(slot + i) * 32 + lane];
+            }
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            lam_n = lam[l];
+            if (kTrial) d_n = d[l];
+        }
+    };
+    int32_t w_n;
+    int64_t slot_n;
+    if (K > 0) fetch(0, w_n, slot_n);
     for (int32_t k = 0; k < K; ++k) {
-        const int32_t w = s.pos_width[p0 + k];
-        const int64_t slot = s.pos_slot[p0 + k];
+        const int32_t w = w_n;
+        int32_t z[W], o[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            z[i] = za[i];
+            o[i] = oa[i];
+        }
         const bool act = k < nj;
         const int32_t l = l0 + nj - 1 - k;
-        double lam_l = 0.0;
+        double lam_l = act ? lam_n : 0.0;
+        if (kTrial && act) lam_l = __dadd_rn(lam_l, __dmul_rn(gamma, d_n));
+        if (k + 1 < K) fetch(k + 1, w_n, slot_n);
         int32_t vbase = 0, wl = 0;
-        if (act) {
-            lam_l = lam[l];
-            if (kTrial) lam_l = __dadd_rn(lam_l, __dmul_rn(gamma, d[l]));
-            if (kStore) {
-                vbase = s.lnl[l];
-                wl = s.lnl[l + 1] - vbase;
-            }
+        if (kStore && act) {
+            vbase = s.lnl[l];
+            wl = s.lnl[l + 1] - vbase;
         }
-#pragma unroll 4
-        for (int32_t i = 0; i < w; ++i) {
-            const int32_t a = s.zl[(slot + i) * 32 + lane];
-            const int32_t b = s.ol[(slot + i) * 32 + lane];
-            const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nb[a * kSweepThreads]);
-            const double c1 = b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[b * kSweepThreads]));
-            const double v = (c0 <= c1) ? c0 : c1;
-            cur[i * kSweepThreads] = v;
-            if (kStore && i < wl) B[vbase + i] = v;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (i < w) {
+                const int32_t a = z[i], b = o[i];
+                const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nb[a * kSweepThreads]);
+                const double c1 =
+                    b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[b * kSweepThreads]));
+                const double v = (c0 <= c1) ? c0 : c1;
+                cur[i * kSweepThreads] = v;
+                if (kStore && i < wl) B[vbase + i] = v;
+            }
         }
         double *t = nb;
         nb = cur;
@@ -189,6 +217,313 @@ int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bound
     if (s.max_width <= 8) return launch_forward<8>(s, lam, F, bounds, st);
     if (s.max_width <= 16) return launch_forward<16>(s, lam, F, bounds, st);
     return launch_forward<32>(s, lam, F, bounds, st);
+}
+
+}  // namespace dm
+
+// ===========================================================================
+// Chunked inner product (the dot order of the L-BFGS path):
+//   dot(a, b) = pairwise(c_0, ..., c_{m-1}),  c_k = pairwise(a*b over chunk k)
+// with chunks of 4096 elements (the last one shorter) and numpy's pairwise
+// order inside each sum — restated by oracle/solver.py:_dot_chunked.
+// Two launches: chunk_step_kernel takes one 128-thread block per FULL chunk —
+// a perfect tree over 32 leaves of 128 elements (numpy's 8-accumulator leaf);
+// thread (leaf o, pair p) owns accumulators 2p and 2p+1 of leaf o, read as
+// 16-byte pairs, and the leaf and tree combines are shuffles — and writes the
+// chunk total; chunk_finish_kernel (one block) handles the short tail chunk by
+// replaying numpy's recursion from shared memory, then reduces the chunk
+// totals the same way.  The stream orders the two, so no atomics or fences.
+//
+// The fused L-BFGS two-loop (qn.py:95-115) rides on the same pair of kernels:
+// each step applies one update of the recursion to x and takes the next inner
+// product on the updated values in the same pass.  Rounding and reduction
+// order equal dm_axpy_dev / dm_scale_dev / dm_lbfgs_up / dm_dot, so the
+// direction is bit-identical to the unfused sequence.
+//   kDot   : no update, dot_out = dot(v, x)
+//   kCopy  : x = u                                  (q = g.copy())
+//   kFirst : a = rho*dot_in; x = x - a*u; alpha_out = a
+//   kScale : like kFirst, then x = (sy0 / yy) * x   (last first-loop step)
+//   kSecond: x = x + u * (alpha - rho*dot_in)
+// then dot_out = chunked_dot(v, x) when v != nullptr.
+// ===========================================================================
+namespace {
+
+constexpr int kChunk = 4096;
+constexpr int kChunkThreads = 128;
+constexpr int kFinishThreads = 1024;
+
+enum { kDot = 0, kCopy = 1, kFirst = 2, kScale = 3, kSecond = 4 };
+
+struct ChunkStep {
+    double *x;
+    const double *u, *v;
+    double rho, sy0;
+    const double *dot_in, *yy, *alpha_in;
+    double *alpha_out, *dot_out;
+};
+
+struct StepCoef {
+    double coef, r;
+};
+
+template <int kMode>
+__device__ __forceinline__ StepCoef step_coef(const ChunkStep &a) {
+    StepCoef c{0.0, 0.0};
+    if (kMode == kFirst || kMode == kScale) c.coef = __dmul_rn(a.rho, a.dot_in[0]);
+    if (kMode == kScale) c.r = __ddiv_rn(a.sy0, a.yy[0]);
+    if (kMode == kSecond) c.coef = __dsub_rn(a.alpha_in[0], __dmul_rn(a.rho, a.dot_in[0]));
+    return c;
+}
+
+template <int kMode>
+__device__ __forceinline__ double step_update(const StepCoef &c, double xo, double uo) {
+    if (kMode == kDot) return xo;
+    if (kMode == kCopy) return uo;
+    if (kMode == kSecond) return __dadd_rn(xo, __dmul_rn(uo, c.coef));
+    const double xi = __dsub_rn(xo, __dmul_rn(c.coef, uo));
+    return kMode == kScale ? __dmul_rn(c.r, xi) : xi;
+}
+
+// numpy's pairwise recursion for one length n <= kChunk, planned on the host:
+// the leaves (<= 32 runs of <= 128 elements, left to right) and the combine
+// order as a postfix program (0 = push the next leaf sum, 1 = add the top two).
+struct SumPlan {
+    int32_t nleaves, nops;
+    uint16_t off[32];
+    uint8_t len[32];
+    uint8_t ops[64];
+};
+
+void plan_rec(SumPlan &p, int off, int len) {
+    if (len <= 128) {
+        p.off[p.nleaves] = (uint16_t)off;
+        p.len[p.nleaves++] = (uint8_t)len;
+        p.ops[p.nops++] = 0;
+        return;
+    }
+    int n2 = len / 2;
+    n2 -= n2 % 8;
+    plan_rec(p, off, n2);
+    plan_rec(p, off + n2, len - n2);
+    p.ops[p.nops++] = 1;
+}
+
+SumPlan make_sum_plan(int n) {
+    SumPlan p{};
+    if (n > 0) plan_rec(p, 0, n);
+    return p;
+}
+
+// 0.0 + numpy pairwise_sum(sm[0:n]) of shared-memory values, by a block of
+// >= 256 threads (one octet per leaf, numpy's 8 accumulators); thread 0 runs
+// the combine program.  Result on thread 0.
+__device__ double smem_pairwise(const double *sm, const SumPlan &p) {
+    __shared__ double leaf_val[32];
+    const int oct = threadIdx.x >> 3, q = threadIdx.x & 7;
+    if (oct < 32) {  // whole warps: 256 threads
+        const bool live = oct < p.nleaves;
+        const int off = live ? p.off[oct] : 0, len = live ? p.len[oct] : 0;
+        const int stop = len - (len % 8);
+        double r = 0.0;
+        if (len >= 8) {
+            r = sm[off + q];
+            for (int i = 8; i < stop; i += 8) r = __dadd_rn(r, sm[off + i + q]);
+        }
+#pragma unroll
+        for (int w = 1; w < 8; w <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, w));  // a+b == b+a exactly
+        if (live && q == 0) {
+            double res = len < 8 ? 0.0 : r;
+            for (int i = len < 8 ? 0 : stop; i < len; ++i) res = __dadd_rn(res, sm[off + i]);
+            leaf_val[oct] = res;
+        }
+    }
+    __syncthreads();
+    double total = 0.0;
+    if (threadIdx.x == 0 && p.nops > 0) {
+        double st[8];
+        int sp = 0, k = 0;
+        for (int i = 0; i < p.nops; ++i) {
+            if (p.ops[i] == 0) {
+                st[sp++] = leaf_val[k++];
+            } else {
+                --sp;
+                st[sp - 1] = __dadd_rn(st[sp - 1], st[sp]);
+            }
+        }
+        total = __dadd_rn(0.0, st[0]);
+    }
+    return total;
+}
+
+struct FinishPlans {
+    SumPlan chunk, tail, totals;
+};
+
+// element pair (2p, 2p+1) of row i of leaf o, as a double2 index
+__device__ __forceinline__ int pair_index(int i) { return (threadIdx.x >> 2) * 64 + (threadIdx.x & 3) + 4 * i; }
+
+template <int kMode>
+__global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, double *__restrict__ partial) {
+    const StepCoef c = step_coef<kMode>(a);
+    const int64_t off = (int64_t)blockIdx.x * kChunk;
+    double2 *x2 = reinterpret_cast<double2 *>(a.x + off);
+    const double2 *u2 = reinterpret_cast<const double2 *>((kMode == kDot ? a.x : a.u) + off);
+    const double2 *v2 = reinterpret_cast<const double2 *>((a.v ? a.v : a.x) + off);
+    const bool dot = a.v != nullptr;
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int i0 = 0; i0 < 16; i0 += 4) {
+        double2 xv[4], uv[4], vv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = pair_index(i0 + k);
+            if (kMode != kDot) uv[k] = u2[j];
+            if (kMode != kCopy) xv[k] = x2[j];
+            if (dot) vv[k] = v2[j];
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double2 xn;
+            xn.x = step_update<kMode>(c, kMode == kCopy ? 0.0 : xv[k].x, kMode == kDot ? 0.0 : uv[k].x);
+            xn.y = step_update<kMode>(c, kMode == kCopy ? 0.0 : xv[k].y, kMode == kDot ? 0.0 : uv[k].y);
+            if (kMode != kDot) x2[pair_index(i0 + k)] = xn;
+            if (dot) {
+                const double p0 = __dmul_rn(vv[k].x, xn.x), p1 = __dmul_rn(vv[k].y, xn.y);
+                r0 = (i0 + k == 0) ? p0 : __dadd_rn(r0, p0);
+                r1 = (i0 + k == 0) ? p1 : __dadd_rn(r1, p1);
+            }
+        }
+    }
+    if (!dot) return;
+    const unsigned m = 0xffffffffu;
+    double r = __dadd_rn(r0, r1);
+    r = __dadd_rn(r, __shfl_xor_sync(m, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(m, r, 2));
+    __shared__ double leaf_sm[32];
+    if ((threadIdx.x & 3) == 0) leaf_sm[threadIdx.x >> 2] = r;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = leaf_sm[threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < 32; w <<= 1) t = __dadd_rn(t, __shfl_xor_sync(m, t, w));
+        if (threadIdx.x == 0) partial[blockIdx.x] = __dadd_rn(0.0, t);
+    }
+}
+
+// Tail chunk (update + its total) and the reduction of all chunk totals.
+// `full` = 0 also covers unaligned vectors: every chunk is then done here,
+// one at a time.
+template <int kMode>
+__global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep a, int64_t n, int64_t full,
+                                                                      double *__restrict__ partial,
+                                                                      const __grid_constant__ FinishPlans plans) {
+    __shared__ double buf[kChunk];
+    const StepCoef c = step_coef<kMode>(a);
+    if ((kMode == kFirst || kMode == kScale) && threadIdx.x == 0 && a.alpha_out) a.alpha_out[0] = c.coef;
+    const bool dot = a.v != nullptr;
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    for (int64_t ch = full; ch < nch; ++ch) {
+        const int64_t off = ch * kChunk;
+        const int len = (int)((n - off) < kChunk ? (n - off) : kChunk);
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            const double xi = step_update<kMode>(c, kMode == kCopy ? 0.0 : a.x[off + i],
+                                                 kMode == kDot ? 0.0 : a.u[off + i]);
+            if (kMode != kDot) a.x[off + i] = xi;
+            if (dot) buf[i] = __dmul_rn(a.v[off + i], xi);
+        }
+        if (!dot) continue;
+        __syncthreads();
+        const double t = smem_pairwise(buf, len == kChunk ? plans.chunk : plans.tail);
+        if (threadIdx.x == 0) partial[ch] = t;
+        __syncthreads();
+    }
+    if (!dot) return;
+    for (int i = threadIdx.x; i < nch; i += blockDim.x) buf[i] = partial[i];
+    __syncthreads();
+    const double t = smem_pairwise(buf, plans.totals);
+    if (threadIdx.x == 0) a.dot_out[0] = t;
+}
+
+inline bool aligned16(const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; }
+
+template <int kMode>
+cudaError_t chunk_step(const ChunkStep &a, int64_t n, double *partial, cudaStream_t st) {
+    const bool vec = aligned16(a.x) && aligned16(a.u) && aligned16(a.v);
+    const int64_t full = vec ? n / kChunk : 0;
+    if (full > 0) chunk_step_kernel<kMode><<<(unsigned)full, kChunkThreads, 0, st>>>(a, partial);
+    FinishPlans plans;
+    plans.chunk = make_sum_plan(kChunk);
+    plans.tail = make_sum_plan((int)(n % kChunk));
+    plans.totals = make_sum_plan((int)((n + kChunk - 1) / kChunk));
+    chunk_finish_kernel<kMode><<<1, kFinishThreads, 0, st>>>(a, n, full, partial, plans);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+namespace dm {
+
+int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
+                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream) {
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    if (n <= 0 || nch > kChunk || m < 1) return DM_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    // slots: [0, m) first-loop dots, [m, 2m) alphas, 2m = y0.y0, [2m+1, 3m+1) second-loop dots
+    double *dot1 = slots, *alpha = slots + m, *yy = slots + 2 * m, *dot2 = slots + 2 * m + 1;
+    if (int rc = dm::chunk_dot(y[0], y[0], n, partial, yy, stream)) return rc;
+    cudaError_t e;
+    ChunkStep a{};
+    a.x = d;
+    a.u = g;
+    a.v = s[0];
+    a.dot_out = dot1;
+    if ((e = chunk_step<kCopy>(a, n, partial, st))) return fail(e, "two_loop copy");
+    for (int i = 0; i < m; ++i) {
+        a = ChunkStep{};
+        a.x = d;
+        a.u = y[i];
+        a.rho = rho[i];
+        a.dot_in = dot1 + i;
+        a.alpha_out = alpha + i;
+        if (i + 1 < m) {
+            a.v = s[i + 1];
+            a.dot_out = dot1 + i + 1;
+            e = chunk_step<kFirst>(a, n, partial, st);
+        } else {  // last step of the first loop carries the scaling and starts the second loop
+            a.sy0 = sy[0];
+            a.yy = yy;
+            a.v = y[m - 1];
+            a.dot_out = dot2;
+            e = chunk_step<kScale>(a, n, partial, st);
+        }
+        if (e) return fail(e, "two_loop first");
+    }
+    for (int k = 0; k < m; ++k) {
+        const int i = m - 1 - k;
+        a = ChunkStep{};
+        a.x = d;
+        a.u = s[i];
+        a.rho = rho[i];
+        a.dot_in = dot2 + k;
+        a.alpha_in = alpha + i;
+        if (i > 0) {
+            a.v = y[i - 1];
+            a.dot_out = dot2 + k + 1;
+        }
+        if ((e = chunk_step<kSecond>(a, n, partial, st))) return fail(e, "two_loop second");
+    }
+    return DM_OK;
+}
+
+int chunk_dot(const double *a, const double *b, int64_t n, double *partial, double *out, void *stream) {
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    if (n <= 0 || nch > kChunk || !b) return DM_ERR_UNSUPPORTED;
+    ChunkStep st{};
+    st.x = const_cast<double *>(a);  // read only in kDot mode
+    st.v = b;
+    st.dot_out = out;
+    cudaError_t e = chunk_step<kDot>(st, n, partial, (cudaStream_t)stream);
+    return e == cudaSuccess ? DM_OK : fail(e, "chunk_dot");
 }
 
 }  // namespace dm

@@ -143,7 +143,13 @@ def dev_sum(x: torch.Tensor, out: torch.Tensor) -> None:
 
 def dev_dot(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> None:
     """out[0] = np.sum(a * b) (pairwise order)."""
-    _native.call("dm_dot", _ptr(a), _ptr(b), a.numel(), _ptr(out), _stream(a.device))
+    _native.call("dm_dot", _ptr(a), _ptr(b), a.numel(), _ptr(out), _stream(a.device),
+                 launches=_chunk_launches(a.numel()))
+
+
+def _chunk_launches(n: int) -> int:
+    """Kernels one chunked-dot step launches: full chunks + the finishing block."""
+    return 2 if n >= 4096 else 1
 
 
 def dev_axpy_dev(x, y, alpha_host, dot_dev, alpha_out=None):
@@ -158,6 +164,18 @@ def dev_scale_dev(x, num_host, den_dev):
 def dev_lbfgs_up(x, s, alpha_dev, rho_host, dot_dev):
     _native.call("dm_lbfgs_up", _ptr(x), _ptr(s), _ptr(alpha_dev), float(rho_host), _ptr(dot_dev), x.numel(),
                  _stream(x.device))
+
+
+def dev_lbfgs_direction(g, pairs, d):
+    """d = two-loop(g) over ``pairs`` [(s, y, rho, sy)] newest first (qn.py:95-115), fused launches."""
+    m = len(pairs)
+    ptrs = (ctypes.c_void_p * m)
+    s_p = ptrs(*[p[0].data_ptr() for p in pairs])
+    y_p = ptrs(*[p[1].data_ptr() for p in pairs])
+    rho = (ctypes.c_double * m)(*[float(p[2]) for p in pairs])
+    sy = (ctypes.c_double * m)(*[float(p[3]) for p in pairs])
+    _native.call("dm_lbfgs_direction", _ptr(g), s_p, y_p, rho, sy, m, g.numel(), _ptr(d), _stream(g.device),
+                 launches=(2 * m + 2) * _chunk_launches(g.numel()))
 
 
 def dev_axpy_host(x, gamma, y):

@@ -3,7 +3,7 @@
 * every golden case (real-reference outputs): init duals, each exact pass,
   min-marginal table, subgradient, agreement scores and the mma-only
   trajectory bit-for-bit; hybrid trajectories bit-for-bit against the
-  oracle in pairwise-dot mode and within 1e-9 of the reference's BLAS run;
+  oracle in chunked-dot mode and within 1e-9 of the reference's BLAS run;
 * kernel-level checks on random duals against the C oracle;
 * numpy-order reductions, L-BFGS pieces and projection.
 """
@@ -82,7 +82,7 @@ def test_hybrid_solve_matches_oracle_and_reference(case):
     iters = len(g["bounds"]) - 1 if g["stop"] == "max_iterations" else 10_000
     res = qn.solve(inst, SolveConfig(mode="hybrid", max_iterations=iters))
     oi, of = oracle_twin(inst)
-    ost, orec, ostop = solver.solve(oi, mode="hybrid", max_iterations=iters, dot="pairwise", flat=of)
+    ost, orec, ostop = solver.solve(oi, mode="hybrid", max_iterations=iters, dot="chunked", flat=of)
     assert res.bounds == [r[2] for r in orec]  # bitwise, same reduction order
     assert [r.kind for r in res.records] == [r[1] for r in orec]
     assert res.stop_reason == ostop
@@ -140,7 +140,7 @@ def test_pairwise_sum_and_dot_match_numpy(n):
     dev_dot(ta, tb, out[1:2])
     got = out.cpu().numpy()
     assert got[0].tobytes() == np.sum(a).tobytes()
-    assert got[1].tobytes() == np.sum(a * b).tobytes()
+    assert got[1].tobytes() == np.float64(solver._dot_chunked(a, b)).tobytes()
 
 
 def kinked():
@@ -169,7 +169,7 @@ def test_lbfgs_direction_matches_dense_oracle_and_pairwise_oracle():  # test_qn.
         y = rng.standard_normal(n)
         if s @ y >= cfg.curvature_eps:
             qn.update_history(s, y, history, cfg)
-            sy = float(np.sum(s * y))
+            sy = solver._dot_chunked(s, y)
             pairs.insert(0, (s, y, 1.0 / sy, sy))
             pairs = pairs[:10]
         g = rng.standard_normal(n)
@@ -184,7 +184,43 @@ def test_lbfgs_direction_matches_dense_oracle_and_pairwise_oracle():  # test_qn.
             H = V @ H @ V.T + rho * np.outer(s, s)
         ref = H @ g
         assert np.abs(d - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
-        assert d.tobytes() == solver.lbfgs(g, pairs, solver._dot_pairwise).tobytes()
+        assert d.tobytes() == solver.lbfgs(g, pairs, solver._dot_chunked).tobytes()
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (4096, 1), (3 * 4096 + 123, 4), (100003, 10)])
+def test_fused_two_loop_matches_unfused_and_oracle(n, m):
+    rng = np.random.default_rng(n + m)
+    history = qn.LbfgsHistory(10)
+    pairs = []
+    while len(history) < m:
+        s = rng.standard_normal(n)
+        y = s * rng.uniform(0.5, 2.0, n) + 0.01 * rng.standard_normal(n)
+        sy = solver._dot_chunked(s, y)
+        if sy >= 1e-8:
+            qn.update_history(s, y, history, qn.StepConfig())
+            pairs.insert(0, (s, y, 1.0 / sy, sy))
+    g = torch.from_numpy(rng.standard_normal(n)).cuda()
+    fused = qn.lbfgs_direction(g, history).cpu().numpy()
+    plain = qn.lbfgs_direction(g, history, fused=False).cpu().numpy()
+    assert fused.tobytes() == plain.tobytes()
+    assert fused.tobytes() == solver.lbfgs(g.cpu().numpy(), pairs, solver._dot_chunked).tobytes()
+
+
+def test_history_pool_reuses_evicted_pairs():
+    h = qn.LbfgsHistory(3)
+    like = torch.zeros(5, dtype=torch.float64, device="cuda")
+    h.preallocate(like)
+    seen = set()
+    for k in range(8):
+        s, y = h.reserve(like)
+        seen.update((id(s), id(y)))
+        s.fill_(k + 1.0)
+        y.fill_(2.0 * (k + 1))
+        if k != 4:  # one rejected pair: its storage stays in the pool
+            h.push(s, y, 1.0, 1.0)
+    assert len(seen) == 8  # memory + 1 pairs, never more
+    assert [float(s[0]) for s, _, _ in h.newest_first()] == [8.0, 7.0, 6.0]
+    assert [float(y[0]) for _, y, _ in h.newest_first()] == [16.0, 14.0, 12.0]
 
 
 def test_find_step_size_kinked():  # test_qn.py:104-114

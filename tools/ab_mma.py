@@ -1,6 +1,7 @@
 """A/B timing of the exact passes across library builds (GPU tool).
 
-usage: python tools/ab_mma.py <lib.so> [<lib.so> ...]   (each in a fresh process)
+usage: python tools/ab_mma.py <lib.so | KEY=VAL[,KEY=VAL]> ...   (each in a fresh process;
+       KEY=VAL arguments run the in-tree library with those environment settings)
 """
 import json
 import os
@@ -25,11 +26,14 @@ for rep in range(3):
     st.dev.k_mma_backward(st.lam_d, st.F, st.B, st._bounds); e[2].record()
     torch.cuda.synchronize()
     res.append((e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])))
-print(json.dumps({"lib": os.environ["DM_LIB_PATH"], "fw_ms": min(r[0] for r in res), "bw_ms": min(r[1] for r in res),
+print(json.dumps({"lib": os.environ.get("DM_LIB_PATH", os.environ.get("AB_SPEC")), "fw_ms": min(r[0] for r in res), "bw_ms": min(r[1] for r in res),
                   "lam_hash": __import__("hashlib").sha256(st.lam.tobytes()).hexdigest()[:16]}))
 '''
 
 for lib in sys.argv[1:]:
-    env = dict(os.environ, DM_LIB_PATH=os.path.abspath(lib))
+    if "=" in lib:
+        env = dict(os.environ, AB_SPEC=lib, **dict(kv.split("=", 1) for kv in lib.split(",")))
+    else:
+        env = dict(os.environ, DM_LIB_PATH=os.path.abspath(lib))
     out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     print(out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:], flush=True)

@@ -28,11 +28,9 @@ def main():
     results = []
     ref = None
     configs = []
-    for rep in range(2):
-        for relax in (0, 1):
-            for warm in (0, 1):
-                for threads, bps in ((128, 1), (256, 1)):
-                    configs.append((threads, bps, 0, 0, (warm << 16) | (relax << 17)))
+    for sleep in (0, 20, 50, 100, 200, 400):
+        for threads, bps in ((256, 1), (128, 1), (128, 2)):
+            configs.append((threads, bps, sleep, 0, 1 << 16))
     for threads, bps, sleep, probe, look in configs:
         try:
             st.dev.set_mma_config(threads, bps, sleep, probe, look)

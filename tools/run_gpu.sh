@@ -25,6 +25,12 @@ for step in "$@"; do
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:pw_leaf -s 20 -c 1 \
           -o gpurun_out/prof_pwleaf $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full rc=$?" >> gpurun_out/ncu_full.log ;;
     ab) timeout 1200 python tools/ab_mma.py tools/ab/*.so tools/ab/*.so > gpurun_out/ab.jsonl 2> gpurun_out/ab.err ;;
+    abdesc) timeout 1200 python tools/ab_mma.py DM_MMA_DESC=0 DM_MMA_DESC=1 DM_MMA_DESC=0 DM_MMA_DESC=1 > gpurun_out/abdesc.jsonl 2> gpurun_out/abdesc.err ;;
+    phases) timeout 900 python tools/step_phases.py 12 > gpurun_out/phases.jsonl 2> gpurun_out/phases.err ;;
+    vec) timeout 300 python tools/vec_bench.py > gpurun_out/vec.json 2> gpurun_out/vec.err && \
+      timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -c 400 --csv \
+          --log-file gpurun_out/vec_launches.csv python tools/vec_bench.py > gpurun_out/vec_ncu.log 2>&1 ;;
     prof) timeout 900 python tools/step_profile.py > gpurun_out/step_profile.txt 2>&1 ;;
+    sampler) timeout 900 python tools/sampler_cost.py > gpurun_out/sampler.txt 2>&1 ;;
   esac
 done
