@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <vector>
 
 #include "dm_internal.h"
 
@@ -285,40 +286,57 @@ __device__ __forceinline__ double step_update(const StepCoef &c, double xo, doub
 }
 
 // numpy's pairwise recursion for one length n <= kChunk, planned on the host:
-// the leaves (<= 32 runs of <= 128 elements, left to right) and the combine
-// order as a postfix program (0 = push the next leaf sum, 1 = add the top two).
+// the leaves (<= 32 runs of <= 128 elements, left to right) are nodes
+// 0..nleaves-1; the additions are nodes nleaves.. in post-order (the root
+// last), each with its two children and its height above the leaves.
 struct SumPlan {
-    int32_t nleaves, nops;
+    int32_t nleaves, nint, height;
     uint16_t off[32];
     uint8_t len[32];
-    uint8_t ops[64];
+    uint8_t left[31], right[31], h[31];
 };
 
-void plan_rec(SumPlan &p, int off, int len) {
+int plan_rec(SumPlan &p, int off, int len, int &height, std::vector<int> &post) {
     if (len <= 128) {
         p.off[p.nleaves] = (uint16_t)off;
-        p.len[p.nleaves++] = (uint8_t)len;
-        p.ops[p.nops++] = 0;
-        return;
+        p.len[p.nleaves] = (uint8_t)len;
+        height = 0;
+        return p.nleaves++;
     }
     int n2 = len / 2;
     n2 -= n2 % 8;
-    plan_rec(p, off, n2);
-    plan_rec(p, off + n2, len - n2);
-    p.ops[p.nops++] = 1;
+    int hl, hr;
+    const int l = plan_rec(p, off, n2, hl, post);
+    const int r = plan_rec(p, off + n2, len - n2, hr, post);
+    height = 1 + (hl > hr ? hl : hr);
+    post.push_back(l);
+    post.push_back(r);
+    post.push_back(height);
+    return -(int)(post.size() / 3);  // internal node k (1-based) as -k
 }
 
 SumPlan make_sum_plan(int n) {
     SumPlan p{};
-    if (n > 0) plan_rec(p, 0, n);
+    if (n <= 0) return p;
+    std::vector<int> post;
+    int height;
+    plan_rec(p, 0, n, height, post);
+    p.nint = (int)post.size() / 3;
+    p.height = height;
+    auto id = [&](int v) { return v >= 0 ? v : p.nleaves + (-v - 1); };
+    for (int k = 0; k < p.nint; ++k) {
+        p.left[k] = (uint8_t)id(post[3 * k]);
+        p.right[k] = (uint8_t)id(post[3 * k + 1]);
+        p.h[k] = (uint8_t)post[3 * k + 2];
+    }
     return p;
 }
 
 // 0.0 + numpy pairwise_sum(sm[0:n]) of shared-memory values, by a block of
-// >= 256 threads (one octet per leaf, numpy's 8 accumulators); thread 0 runs
-// the combine program.  Result on thread 0.
+// >= 256 threads: one octet per leaf (numpy's 8 accumulators), then warp 0
+// adds the tree level by level.  Result on thread 0.
 __device__ double smem_pairwise(const double *sm, const SumPlan &p) {
-    __shared__ double leaf_val[32];
+    __shared__ double node[64];
     const int oct = threadIdx.x >> 3, q = threadIdx.x & 7;
     if (oct < 32) {  // whole warps: 256 threads
         const bool live = oct < p.nleaves;
@@ -334,23 +352,18 @@ __device__ double smem_pairwise(const double *sm, const SumPlan &p) {
         if (live && q == 0) {
             double res = len < 8 ? 0.0 : r;
             for (int i = len < 8 ? 0 : stop; i < len; ++i) res = __dadd_rn(res, sm[off + i]);
-            leaf_val[oct] = res;
+            node[oct] = res;
         }
     }
     __syncthreads();
     double total = 0.0;
-    if (threadIdx.x == 0 && p.nops > 0) {
-        double st[8];
-        int sp = 0, k = 0;
-        for (int i = 0; i < p.nops; ++i) {
-            if (p.ops[i] == 0) {
-                st[sp++] = leaf_val[k++];
-            } else {
-                --sp;
-                st[sp - 1] = __dadd_rn(st[sp - 1], st[sp]);
-            }
+    if (threadIdx.x < 32 && p.nleaves > 0) {
+        const int k = threadIdx.x;
+        for (int h = 1; h <= p.height; ++h) {
+            if (k < p.nint && p.h[k] == h) node[p.nleaves + k] = __dadd_rn(node[p.left[k]], node[p.right[k]]);
+            __syncwarp();
         }
-        total = __dadd_rn(0.0, st[0]);
+        total = __dadd_rn(0.0, node[p.nleaves + p.nint - 1]);
     }
     return total;
 }
@@ -422,14 +435,25 @@ __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep 
     if ((kMode == kFirst || kMode == kScale) && threadIdx.x == 0 && a.alpha_out) a.alpha_out[0] = c.coef;
     const bool dot = a.v != nullptr;
     const int64_t nch = (n + kChunk - 1) / kChunk;
+    constexpr int kPer = kChunk / kFinishThreads;  // elements per thread, loads issued together
     for (int64_t ch = full; ch < nch; ++ch) {
         const int64_t off = ch * kChunk;
         const int len = (int)((n - off) < kChunk ? (n - off) : kChunk);
-        for (int i = threadIdx.x; i < len; i += blockDim.x) {
-            const double xi = step_update<kMode>(c, kMode == kCopy ? 0.0 : a.x[off + i],
-                                                 kMode == kDot ? 0.0 : a.u[off + i]);
+        double xv[kPer], uv[kPer], vv[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int i = threadIdx.x + k * kFinishThreads;
+            xv[k] = (kMode != kCopy && i < len) ? a.x[off + i] : 0.0;
+            uv[k] = (kMode != kDot && i < len) ? a.u[off + i] : 0.0;
+            vv[k] = (dot && i < len) ? a.v[off + i] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int i = threadIdx.x + k * kFinishThreads;
+            if (i >= len) continue;
+            const double xi = step_update<kMode>(c, xv[k], uv[k]);
             if (kMode != kDot) a.x[off + i] = xi;
-            if (dot) buf[i] = __dmul_rn(a.v[off + i], xi);
+            if (dot) buf[i] = __dmul_rn(vv[k], xi);
         }
         if (!dot) continue;
         __syncthreads();
@@ -438,7 +462,17 @@ __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep 
         __syncthreads();
     }
     if (!dot) return;
-    for (int i = threadIdx.x; i < nch; i += blockDim.x) buf[i] = partial[i];
+    double pv[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x + k * kFinishThreads;
+        pv[k] = i < nch ? __ldcg(partial + i) : 0.0;  // includes this block's own tail total
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x + k * kFinishThreads;
+        if (i < nch) buf[i] = pv[k];
+    }
     __syncthreads();
     const double t = smem_pairwise(buf, plans.totals);
     if (threadIdx.x == 0) a.dot_out[0] = t;
