@@ -127,8 +127,9 @@ int dm_flat_status(dm_flat *flat, void *stream);
  * DM_MMA_PROBE / DM_MMA_LOOKAHEAD / DM_MMA_WARM / DM_MMA_DESC. */
 int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns, int probe,
                            int lookahead);
-/* Profiling hooks: a device buffer of tasks*32*5 u64 receives, per lane,
- * %globaltimer stamps (task start, own inputs seen, group go, dual updated, outputs published) of the
+/* Profiling hooks: a device buffer of tasks*32*6 u64 receives, per lane,
+ * %globaltimer stamps (task start, own inputs seen, group go, dual updated, outputs published,
+ * issue of the successful input poll) of the
  * following exact passes (NULL disables); dm_flat_task_levels copies the
  * DAG level of every task (and optionally the 32 lane layers per task) of
  * the forward/backward schedule. */

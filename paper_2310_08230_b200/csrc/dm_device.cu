@@ -49,6 +49,58 @@ __device__ __forceinline__ double ld_relaxed(const double *p) {
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return __longlong_as_double((long long)v);
 }
+// Loads p[min(i, n-1)] for i < 8 (n >= 1) in ONE asm block of unpredicated
+// loads, so that all of them are in flight before the first sentinel check
+// (separately predicated loads get interleaved with the checks by the
+// scheduler, which serialises the round trips).  Slots i >= n re-read element
+// n-1, a real input, so checking all 8 is exact.
+__device__ __forceinline__ void ld8_relaxed(const double *p, int n, double *v) {
+    unsigned long long r[8];
+    const double *q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = p + (i < n ? i : n - 1);
+    asm volatile(
+        "ld.relaxed.gpu.global.b64 %0, [%8];\n\t"
+        "ld.relaxed.gpu.global.b64 %1, [%9];\n\t"
+        "ld.relaxed.gpu.global.b64 %2, [%10];\n\t"
+        "ld.relaxed.gpu.global.b64 %3, [%11];\n\t"
+        "ld.relaxed.gpu.global.b64 %4, [%12];\n\t"
+        "ld.relaxed.gpu.global.b64 %5, [%13];\n\t"
+        "ld.relaxed.gpu.global.b64 %6, [%14];\n\t"
+        "ld.relaxed.gpu.global.b64 %7, [%15];"
+        : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3]), "=l"(r[4]), "=l"(r[5]), "=l"(r[6]), "=l"(r[7])
+        : "l"(q[0]), "l"(q[1]), "l"(q[2]), "l"(q[3]), "l"(q[4]), "l"(q[5]), "l"(q[6]), "l"(q[7])
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __longlong_as_double((long long)r[i]);
+}
+
+// Polls the n <= W inputs at p into v: true when none is the sentinel.
+// Slots i >= n come back as +INF (padding nodes).  kFence: see below.
+template <int W, bool kFence>
+__device__ __forceinline__ bool poll_inputs(const double *p, int n, double (&v)[W]) {
+    static_assert(W % 8 == 0, "layer width bound must be a multiple of 8");
+    double t[W];
+#pragma unroll
+    for (int g = 0; g < W; g += 8) {
+        if (g == 0 || g < n) ld8_relaxed(p + g, n - g, t + g);
+    }
+    // scheduling fence: keeps ptxas from interleaving the checks with the
+    // loads in the forward kernel (it pairs them there, paying one round trip
+    // per pair; the backward kernel's schedule is fine without it, and the
+    // fence costs it ~5%)
+    if (kFence) __syncwarp(__activemask());
+    unsigned long long bad = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        if (i >= 8 && i >= ((n + 7) & ~7)) t[i] = DM_INF;  // group not loaded
+        bad |= (unsigned long long)(__double_as_longlong(t[i]) == (long long)kSentinel);
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) v[i] = i < n ? t[i] : DM_INF;
+    return bad == 0;
+}
+
 __device__ __forceinline__ void st_relaxed(double *p, double x) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(x))
                  : "memory");
@@ -314,7 +366,8 @@ struct MmaArgs {
     int *status;                // 0 ok, 1 watchdog fired
     unsigned sleep_ns;          // back-off between unsuccessful polls
     int probe;                  // 1: poll one probe word before reading the layer; 0: poll all inputs
-    unsigned long long *trace;  // optional [task*32+lane][5]: start, own inputs seen, group go, dual updated, published
+    unsigned long long *trace;  // optional [task*32+lane][6]: start, own inputs seen, group go, dual updated,
+                                // published, issue of the successful poll
     const int32_t *task_level;  // DAG level of each task
     int *progress;              // highest level of a finished task (monotone hint)
     int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
@@ -334,7 +387,7 @@ __device__ __forceinline__ void publish_progress(const MmaArgs &a, int64_t task,
 }
 
 __device__ __forceinline__ void trace_mark(const MmaArgs &a, int64_t task, int lane, int slot, uint64_t t) {
-    if (a.trace) a.trace[(task * 32 + lane) * 5 + slot] = t;
+    if (a.trace) a.trace[(task * 32 + lane) * 6 + slot] = t;
 }
 
 // true when this warp must abandon the pass (own timeout or another's)
@@ -386,8 +439,16 @@ __device__ __forceinline__ double tree_lmin(double (&v)[N]) {
 // order (kernels.py:200-233) and the lane's new dual (kernels.py:234-240).
 // Whole warp executes it; only lanes with `go` use the result.  The group's
 // deltas are gathered with independent shuffles, then summed sequentially.
+//
+// Non-finite lanes contribute +0.0 instead of being skipped: the running sum
+// starts at +0.0 and binary64 addition never produces -0.0 from it (exact
+// cancellation gives +0.0, sums of nonzero values never round to zero), so
+// adding +0.0 leaves it bit-unchanged.  Division by a power-of-two count is a
+// multiplication by its exact reciprocal (both correctly rounded from the same
+// real quotient); other counts take __ddiv_rn.
 template <int K>
-__device__ __forceinline__ double average_in_group(bool go, int32_t meta, double m0, double m1, double lam_l) {
+__device__ __forceinline__ double average_in_group(bool go, int32_t meta, unsigned gmask, double m0, double m1,
+                                                   double lam_l) {
     const bool fin = go && m0 != DM_INF && m1 != DM_INF;
     const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
     const unsigned finmask = __ballot_sync(kFull, fin);
@@ -396,39 +457,44 @@ __device__ __forceinline__ double average_in_group(bool go, int32_t meta, double
 #pragma unroll
     for (int k = 0; k < K; ++k) dk[k] = __shfl_sync(kFull, dlt, (gbase + k) & 31);
     double fsum = 0.0;
-    int fcnt = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        if (k >= gcnt) break;
-        if ((finmask >> (gbase + k)) & 1u) {
-            fsum = __dadd_rn(fsum, dk[k]);
-            ++fcnt;
-        }
-    }
+    for (int k = 0; k < K; ++k)
+        if (k < gcnt) fsum = __dadd_rn(fsum, dk[k]);
+    const int fcnt = __popc(finmask & gmask);
     if (fin && fcnt > 0) {
-        const double avg = __ddiv_rn(fsum, (double)fcnt);
+        double avg;
+        if ((fcnt & (fcnt - 1)) == 0)
+            avg = __dmul_rn(fsum, fcnt == 1 ? 1.0 : fcnt == 2 ? 0.5 : fcnt == 4 ? 0.25 : fcnt == 8 ? 0.125 : 1.0 / fcnt);
+        else
+            avg = __ddiv_rn(fsum, (double)fcnt);
         lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
     }
     return lam_l;
 }
 
-// Min-marginals of one layer (kernels.py:205-230), as two leftmost-min trees.
-// Nodes with F == INF contribute INF candidates, which never win — the same
-// as the reference's `continue`.
+// Min-marginals of one layer (kernels.py:205-230), as two leftmost-min trees
+// over c0[i] = F[i] + t0[i] and c1[i] = (F[i] + lam) + t1[i].  The arc terms
+// are prepared before the wait: the target's distance for an inner arc,
+// -0.0 for an arc to TRUE (x + -0.0 == x bit for bit, the reference's plain
+// F[i]) and +INF for an arc to FALSE or a padding node (F is never -INF or
+// NaN, so the sum is +INF, a candidate that never wins — the reference's
+// `continue`).
 template <int W>
-__device__ __forceinline__ void layer_marginals(int32_t w, const double (&f)[W], const int32_t (&z)[W],
-                                                const int32_t (&o)[W], const double (&bz)[W],
-                                                const double (&bo)[W], double lam_l, double &m0, double &m1) {
+__device__ __forceinline__ void layer_marginals(const double (&f)[W], const double (&t0)[W],
+                                                const double (&t1)[W], double lam_l, double &m0, double &m1) {
     double c0[W], c1[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-        const double fv = f[i];
-        const double fl = __dadd_rn(fv, lam_l);
-        c0[i] = (i >= w || z[i] == dm::kFalse) ? DM_INF : (z[i] == dm::kTrue ? fv : __dadd_rn(fv, bz[i]));
-        c1[i] = (i >= w || o[i] == dm::kFalse) ? DM_INF : (o[i] == dm::kTrue ? fl : __dadd_rn(fl, bo[i]));
+        c0[i] = __dadd_rn(f[i], t0[i]);
+        c1[i] = __dadd_rn(__dadd_rn(f[i], lam_l), t1[i]);
     }
     m0 = tree_lmin<W>(c0);
     m1 = tree_lmin<W>(c1);
+}
+
+// additive arc term of layer_marginals for an arc to `t` whose distance is `d`
+__device__ __forceinline__ double arc_term(int32_t t, double d) {
+    return t == dm::kFalse ? DM_INF : (t == dm::kTrue ? -0.0 : d);
 }
 
 // Forward pass.  Warp w takes tasks w, w+W, ... (level order).  Inside a task
@@ -457,7 +523,8 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             }
             lam_l = a.lam[l];
         }
-        // static inputs: topology and the backward distances (valid all pass)
+        // static inputs: topology and the backward distances (valid all pass),
+        // folded into the marginal arc terms
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             z[i] = o[i] = dm::kFalse;
@@ -465,8 +532,8 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             if (i < w) {
                 z[i] = a.zero_t[nlo + i];
                 o[i] = a.one_t[nlo + i];
-                if (z[i] >= 0) bz[i] = a.B[z[i]];
-                if (o[i] >= 0) bo[i] = a.B[o[i]];
+                bz[i] = arc_term(z[i], z[i] >= 0 ? a.B[z[i]] : 0.0);
+                bo[i] = arc_term(o[i], o[i] >= 0 ? a.B[o[i]] : 0.0);
             }
         }
         // pull the lines this lane will poll into L2 while it waits
@@ -484,15 +551,13 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
         while (pending) {
             if (!have && ((pending >> lane) & 1u)) {
                 if (!a.probe || !is_sentinel(ld_relaxed(a.F + nlo + w - 1))) {
-                    bool ok = true;
-#pragma unroll
-                    for (int i = 0; i < W; ++i)
-                        if (i < w) {
-                            f[i] = ld_relaxed(a.F + nlo + i);
-                            ok &= !is_sentinel(f[i]);
-                        }
+                    const uint64_t t_issue = a.trace ? global_ns() : 0;
+                    const bool ok = poll_inputs<W, true>(a.F + nlo, w, f);
                     have = ok;
-                    if (ok && a.trace) trace_mark(a, task, lane, 1, global_ns());
+                    if (ok && a.trace) {
+                        trace_mark(a, task, lane, 1, global_ns());
+                        trace_mark(a, task, lane, 5, t_issue);
+                    }
                 }
             }
             const unsigned hm = __ballot_sync(kFull, have);
@@ -509,8 +574,8 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             pending &= ~gom;
             if (go && a.trace) trace_mark(a, task, lane, 2, global_ns());
             double m0, m1;
-            layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
-            const double lam_new = average_in_group<K>(go, meta, m0, m1, lam_l);
+            layer_marginals<W>(f, bz, bo, lam_l, m0, m1);
+            const double lam_new = average_in_group<K>(go, meta, gmask, m0, m1, lam_l);
             if (!go) continue;
             lam_l = lam_new;
             a.lam[l] = lam_l;
@@ -519,26 +584,30 @@ __global__ void __launch_bounds__(256) mma_forward_kernel(MmaArgs a) {
             // value is the leftmost minimum over (v ascending, zero-arc,
             // one-arc) of the reference's scatter, computed for all targets
             // at once.
-            double c[W];
-#pragma unroll
-            for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
             if (!last && D) {
                 // host-built per-layer source nibbles (dm_layout.cpp
                 // build_relax_by_layer): at most one zero- and one one-arc
                 // source per target, so the leftmost minimum is one compare.
-                double fl[W], cl[W];
+                double fl[W + 1];
 #pragma unroll
-                for (int i = 0; i < W; ++i) fl[i] = f[i], cl[i] = c[i];
+                for (int i = 0; i < W; ++i) fl[i] = f[i];
+                fl[W] = DM_INF;
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     if (u < wn) {
                         const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
-                        const double A = zi < W ? fl[zi] : DM_INF;
-                        const double C = oi < W ? cl[oi] : DM_INF;
+                        const double A = fl[zi < W ? zi : W];
+                        const double C = __dadd_rn(fl[oi < W ? oi : W], lam_l);
                         st_relaxed(a.F + n0 + u, (C < A || (C == A && oi < zi)) ? C : A);
                     }
                 }
-            } else if (!last) {
+                if (a.trace) trace_mark(a, task, lane, 4, global_ns());
+                continue;
+            }
+            double c[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) c[i] = __dadd_rn(f[i], lam_l);
+            if (!last) {
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     if (u < wn) {
@@ -580,8 +649,13 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
         const bool last = meta & (1 << 17);
         int32_t nlo = 0, w = 0, probe = -1, wnext = 0, n0n = 0;
         double lam_l = 0.0;
-        int32_t z[W], o[W];
-        double bz[W], bo[W], f[W], nbv[W];
+        // per node: slot of the zero/one arc target in the next layer (W for
+        // TRUE/FALSE/padding, whose slot holds -0.0), the marginal bases
+        // F (zero arc) and F + lam (one arc) — +INF for FALSE arcs and padding
+        // — and the rebuild offsets (see the rebuild below)
+        int32_t iz[W], io[W];
+        double f0[W], f1[W], rz[W], ro[W];
+        double nbv[W];
         if (act) {
             nlo = a.lnl[l];
             w = a.lnl[l + 1] - nlo;
@@ -594,13 +668,19 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
         }
 #pragma unroll
         for (int i = 0; i < W; ++i) {
-            z[i] = o[i] = dm::kFalse;
-            f[i] = DM_INF;
-            bz[i] = bo[i] = 0.0;
+            iz[i] = io[i] = W;
+            f0[i] = f1[i] = DM_INF;
+            rz[i] = ro[i] = DM_INF;
+            nbv[i] = -0.0;
             if (i < w) {
-                z[i] = a.zero_t[nlo + i];
-                o[i] = a.one_t[nlo + i];
-                f[i] = a.F[nlo + i];
+                const int32_t z = a.zero_t[nlo + i], o = a.one_t[nlo + i];
+                const double fv = a.F[nlo + i];
+                iz[i] = z >= 0 ? ((z - n0n) & (W - 1)) : W;
+                io[i] = o >= 0 ? ((o - n0n) & (W - 1)) : W;
+                f0[i] = z == dm::kFalse ? DM_INF : fv;
+                f1[i] = o == dm::kFalse ? DM_INF : __dadd_rn(fv, lam_l);
+                rz[i] = z == dm::kFalse ? DM_INF : (z == dm::kTrue ? 0.0 : -0.0);
+                ro[i] = o == dm::kFalse ? DM_INF : -0.0;
             }
         }
         if (a.warm && act && !last) {
@@ -619,15 +699,13 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
                 if (!a.probe || !is_sentinel(ld_relaxed(a.B + probe))) {
                     // read the next layer contiguously (like the forward pass reads
                     // its own layer); routing to the arc targets happens once, at go
-                    bool ok = true;
-#pragma unroll
-                    for (int u = 0; u < W; ++u)
-                        if (u < wnext) {
-                            nbv[u] = ld_relaxed(a.B + n0n + u);
-                            ok &= !is_sentinel(nbv[u]);
-                        }
+                    const uint64_t t_issue = a.trace ? global_ns() : 0;
+                    const bool ok = poll_inputs<W, false>(a.B + n0n, wnext, nbv);
                     have = ok;
-                    if (ok && a.trace) trace_mark(a, task, lane, 1, global_ns());
+                    if (ok && a.trace) {
+                        trace_mark(a, task, lane, 1, global_ns());
+                        trace_mark(a, task, lane, 5, t_issue);
+                    }
                 }
             }
             const unsigned hm = __ballot_sync(kFull, have);
@@ -645,31 +723,46 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
             if (go && a.trace) trace_mark(a, task, lane, 2, global_ns());
             // route the next layer's distances to the arc targets through a
             // dynamically indexed (local-memory, L1-resident) copy: measured
-            // 20% faster per pass than W x W register selects
+            // 20% faster per pass than W x W register selects.  Slot W holds
+            // -0.0, the term of arcs to a terminal.
+            double tz[W], to[W];
             {
-                double nbl[W];
+                double nbl[W + 1];
 #pragma unroll
                 for (int u = 0; u < W; ++u) nbl[u] = nbv[u];
+                nbl[W] = -0.0;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    bz[i] = z[i] >= 0 ? nbl[(z[i] - n0n) & (W - 1)] : 0.0;
-                    bo[i] = o[i] >= 0 ? nbl[(o[i] - n0n) & (W - 1)] : 0.0;
+                    tz[i] = nbl[iz[i]];
+                    to[i] = nbl[io[i]];
                 }
             }
             double m0, m1;
-            layer_marginals<W>(w, f, z, o, bz, bo, lam_l, m0, m1);
-            const double lam_new = average_in_group<K>(go, meta, m0, m1, lam_l);
+            {
+                double c0[W], c1[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    c0[i] = __dadd_rn(f0[i], tz[i]);
+                    c1[i] = __dadd_rn(f1[i], to[i]);
+                }
+                m0 = tree_lmin<W>(c0);
+                m1 = tree_lmin<W>(c1);
+            }
+            const double lam_new = average_in_group<K>(go, meta, gmask, m0, m1, lam_l);
             if (!go) continue;
             lam_l = lam_new;
             a.lam[l] = lam_l;
             if (a.trace) trace_mark(a, task, lane, 3, global_ns());
-            // rebuild this layer's distances to TRUE (kernels.py:340-358)
+            // rebuild this layer's distances to TRUE (kernels.py:340-358):
+            //   zero arc: B[z] (inner), +0.0 (TRUE), +INF (FALSE)  = rz + tz
+            //   one arc : lam + B[o], lam, +INF                    = (lam + to) + ro
+            // (x + -0.0 == x; +0.0 + -0.0 == +0.0; INF + finite == INF)
             double first = 0.0;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 if (i < w) {
-                    const double c0 = z[i] == dm::kTrue ? 0.0 : (z[i] == dm::kFalse ? DM_INF : bz[i]);
-                    const double c1 = o[i] == dm::kTrue ? lam_l : (o[i] == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo[i]));
+                    const double c0 = __dadd_rn(rz[i], tz[i]);
+                    const double c1 = __dadd_rn(__dadd_rn(lam_l, to[i]), ro[i]);
                     const double bv = (c0 <= c1) ? c0 : c1;
                     st_relaxed(a.B + nlo + i, bv);
                     if (i == 0) first = bv;

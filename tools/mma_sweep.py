@@ -28,9 +28,12 @@ def main():
     results = []
     ref = None
     configs = []
-    for sleep in (0, 20, 50, 100, 200, 400):
-        for threads, bps in ((256, 1), (128, 1), (128, 2)):
-            configs.append((threads, bps, sleep, 0, 1 << 16))
+    for threads, bps in ((256, 1), (128, 1), (64, 2)):
+        for probe in (0, 1):
+            for look in (0, 2, 4, 8):
+                configs.append((threads, bps, 0, probe, look | (1 << 16)))
+    configs.append((256, 1, 100, 0, 1 << 16))
+    configs.append((256, 1, 0, 0, 0))
     for threads, bps, sleep, probe, look in configs:
         try:
             st.dev.set_mma_config(threads, bps, sleep, probe, look)

@@ -25,11 +25,12 @@ def analyse(st, forward, trace, name):
     layers = np.zeros(ntask * 32, np.int32)
     _native.check(_native.load().dm_flat_task_levels(st.dev.handle, int(forward), levels.ctypes.data,
                                                     layers.ctypes.data))
-    tr = trace.cpu().numpy().reshape(ntask * 32, 5).astype(np.int64)
+    tr = trace.cpu().numpy().reshape(ntask * 32, 6).astype(np.int64)
     act = layers >= 0
     t0 = tr[act, 0].min()
-    start, own, seen, upd, done = (tr[:, k] - t0 for k in range(5))
-    own = np.where(tr[:, 1] == 0, seen, own)  # lanes without dependencies
+    start, own, seen, upd, done, issue = (tr[:, k] - t0 for k in range(6))
+    issue = np.where(tr[:, 5] == 0, start, issue)
+    own = np.where(tr[:, 1] == 0, start, own)  # lanes without dependencies are ready at start
     lane_level = np.repeat(levels, 32)
     # producer lane of each lane: layer l-1 (forward) / l+1 (backward) in the same diagram
     f = st.flat
@@ -63,6 +64,37 @@ def analyse(st, forward, trace, name):
            "average_ns": q(upd[act] - seen[act]), "publish_ns": q(done[act] - upd[act]),
            "seen_minus_start_ns": q(wait_after_start),
            "late_start_frac": float(np.mean(start[has_pred] > done[pslot[has_pred]]))}
+    # critical chain: walk back from the last published lane
+    var_of = np.where(act, f.layer_var[np.clip(l, 0, L - 1)], -1)
+    nwarps = int(st.dev.info["mma_grid"] * st.dev.info["mma_block"] // 32)
+    task_done = done.reshape(-1, 32).max(axis=1)
+    seg = {"work": 0, "gate": 0, "comm": 0, "comm_to_issue": 0, "comm_poll_rtt": 0, "late_poll": 0, "warp_busy": 0}
+    nseg = {k: 0 for k in seg}
+    cur = int(np.flatnonzero(act)[np.argmax(done[act])])
+    steps = 0
+    while steps < 100000:
+        steps += 1
+        t = cur // 32
+        lanes = np.arange(t * 32, t * 32 + 32)
+        grp = lanes[(var_of[lanes] == var_of[cur]) & act[lanes]]
+        crit = int(grp[np.argmax(own[grp])])
+        seg["work"] += done[cur] - seen[cur]; nseg["work"] += 1
+        seg["gate"] += seen[cur] - own[crit]; nseg["gate"] += 1
+        if has_pred[crit] and start[crit] < done[pslot[crit]]:
+            seg["comm"] += own[crit] - done[pslot[crit]]; nseg["comm"] += 1
+            seg["comm_to_issue"] += issue[crit] - done[pslot[crit]]; nseg["comm_to_issue"] += 1
+            seg["comm_poll_rtt"] += own[crit] - issue[crit]; nseg["comm_poll_rtt"] += 1
+            cur = int(pslot[crit])
+        else:
+            seg["late_poll"] += own[crit] - start[crit]; nseg["late_poll"] += 1
+            prev = (cur // 32) - nwarps
+            if prev < 0:
+                break
+            seg["warp_busy"] += start[crit] - task_done[prev]; nseg["warp_busy"] += 1
+            cur = int(prev * 32 + np.argmax(done[prev * 32:prev * 32 + 32]))
+    out["critical_chain"] = {k: {"total_ns": int(v), "n": nseg[k], "mean_ns": float(v / max(nseg[k], 1))}
+                             for k, v in seg.items()}
+    out["critical_chain_start_ns"] = int(start[cur])
     late = has_pred.copy()
     late[has_pred] = start[has_pred] > done[pslot[has_pred]]
     if late.any():
@@ -79,7 +111,7 @@ def main():
         mma_pass(st, BACKWARD)
     for forward, name in ((True, "forward"), (False, "backward")):
         ntask = st.dev.info["fw_tasks" if forward else "bw_tasks"]
-        trace = torch.zeros(ntask * 32 * 5, dtype=torch.int64, device=st.device)
+        trace = torch.zeros(ntask * 32 * 6, dtype=torch.int64, device=st.device)
         _native.check(_native.load().dm_flat_set_trace(st.dev.handle, trace.data_ptr()))
         mma_pass(st, FORWARD if forward else BACKWARD)
         torch.cuda.synchronize()

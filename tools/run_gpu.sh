@@ -24,6 +24,13 @@ for step in "$@"; do
           -o gpurun_out/prof_sweep $B >> gpurun_out/ncu_full.log 2>&1 && \
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:pw_leaf -s 20 -c 1 \
           -o gpurun_out/prof_pwleaf $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full rc=$?" >> gpurun_out/ncu_full.log ;;
+    ncu_mma)
+      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
+      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_forward -s 1 -c 1 \
+          -o gpurun_out/prof_mma_fw $B > gpurun_out/ncu_mma.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_backward -s 1 -c 1 \
+          -o gpurun_out/prof_mma_bw $B >> gpurun_out/ncu_mma.log 2>&1; echo "ncu_mma rc=$?" >> gpurun_out/ncu_mma.log ;;
     ab) timeout 1200 python tools/ab_mma.py tools/ab/*.so tools/ab/*.so > gpurun_out/ab.jsonl 2> gpurun_out/ab.err ;;
     abdesc) timeout 1200 python tools/ab_mma.py DM_MMA_DESC=0 DM_MMA_DESC=1 DM_MMA_DESC=0 DM_MMA_DESC=1 > gpurun_out/abdesc.jsonl 2> gpurun_out/abdesc.err ;;
     phases) timeout 900 python tools/step_phases.py 12 > gpurun_out/phases.jsonl 2> gpurun_out/phases.err ;;
