@@ -227,6 +227,26 @@ def aggregate_work_time(work: float, ms: float, world: int, device=None):
     return float(t[0]), float(t[1])
 
 
+# one-way visibility of a relaxed gpu-scope store to a polling SM on B200,
+# measured by tools/pingpong.cu (534 ns round trip / 2)
+VISIBILITY_NS = 267.0
+
+
+def _traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture summary (profiles/traffic.json, tools/ncu_summary.py), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            tr = json.load(f)
+    except (OSError, ValueError):
+        return None
+    for name, b in tr.items():
+        if name.startswith(kernel + "_kernel") or name.startswith(kernel + "<") or name == kernel:
+            return b
+    return None
+
+
 def algorithmic_bytes(flat):
     """Per-launch algorithmic HBM bytes."""
     N, L, nb = flat.num_nodes, flat.num_layers, flat.num_bdds
@@ -311,8 +331,18 @@ def run_b200(args, rank, world, local_rank):
         if dom:
             a = kernels[dom]["achieved_gbs"]
             roof = {"bound": "hbm", "kernel": dom, "achieved": round(a, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(a / hbm, 4), "traffic": None,
+                    "frac": round(a / hbm, 4), "traffic": _traffic(dom),
+                    "algorithmic_bytes": kernels[dom]["bytes_per_launch"],
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+            if dom.startswith("mma"):
+                # the exact passes are bound by their dependency chain, not by bytes
+                depth = info["fw_depth"] if dom == "mma_forward" else info["bw_depth"]
+                ns = kernels[dom]["avg_ms"] * 1e6 / depth
+                roof["critical_path"] = {
+                    "levels": depth, "ns_per_level": round(ns, 1),
+                    "visibility_floor_ns": VISIBILITY_NS,
+                    "frac": round(VISIBILITY_NS / ns, 4),
+                    "note": "per level >= one-way store->poll visibility between SMs (tools/pingpong.cu)"}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,

@@ -16,14 +16,19 @@ for step in "$@"; do
       timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
           --log-file gpurun_out/launches.csv $B > gpurun_out/ncu.log 2>&1; echo "ncu_list rc=$?" >> gpurun_out/ncu.log ;;
     ncu_full)
-      B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
+      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
       timeout 900 $B > gpurun_out/plain.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_forward -s 1 -c 1 \
-          -o gpurun_out/prof_mma_fw $B > gpurun_out/ncu_full.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:sweep_backward -s 3 -c 1 \
-          -o gpurun_out/prof_sweep $B >> gpurun_out/ncu_full.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:pw_leaf -s 20 -c 1 \
-          -o gpurun_out/prof_pwleaf $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full rc=$?" >> gpurun_out/ncu_full.log ;;
+      for k in mma_forward mma_backward sweep_backward chunk_step_kernel k_argmin; do
+        timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+            -o gpurun_out/full_$k $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full $k rc=$?" >> gpurun_out/ncu_full.log
+      done ;;
+    ncu_mma2)
+      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
+      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
+      for k in mma_forward mma_backward k_argmin; do
+        timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+            -o gpurun_out/full_$k $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full $k rc=$?" >> gpurun_out/ncu_full.log
+      done ;;
     ncu_mma)
       B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
       timeout 900 $B > gpurun_out/plain.log 2>&1 && \
