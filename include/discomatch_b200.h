@@ -108,6 +108,8 @@ typedef struct {
     int64_t mma_grid, mma_block;
     int64_t max_width, max_degree;
     int64_t device_bytes;
+    int64_t lanes_per_task;     /* trace / task_levels records per task: 32 (one per BDD copy lane),
+                                   8 (node-parallel kernels: one per copy slot) */
 } dm_flat_info;
 
 int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out);
@@ -122,16 +124,18 @@ int dm_flat_status(dm_flat *flat, void *stream);
  * (a warp polls its inputs only once a task within `lookahead` levels of its
  * own has finished; 0 disables the gating) in bits 0-15 of `lookahead`;
  * bit 16 enables L2 warming of the polled lines, bit 17 forces the generic
- * tree publish in the forward pass instead of the per-layer descriptors.
+ * tree publish in the forward pass instead of the per-layer descriptors,
+ * bit 18 forces the per-copy kernels instead of the node-parallel ones
+ * (used by default when layers have <= 8 nodes and variables <= 8 copies).
  * Defaults come from DM_MMA_THREADS / DM_MMA_BLOCKS_PER_SM / DM_MMA_SLEEP_NS /
- * DM_MMA_PROBE / DM_MMA_LOOKAHEAD / DM_MMA_WARM / DM_MMA_DESC. */
+ * DM_MMA_PROBE / DM_MMA_LOOKAHEAD / DM_MMA_WARM / DM_MMA_DESC / DM_MMA_NP. */
 int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sleep_ns, int probe,
                            int lookahead);
-/* Profiling hooks: a device buffer of tasks*32*6 u64 receives, per lane,
+/* Profiling hooks: a device buffer of tasks*lanes_per_task*6 u64 receives, per lane (copy slot),
  * %globaltimer stamps (task start, own inputs seen, group go, dual updated, outputs published,
  * issue of the successful input poll) of the
  * following exact passes (NULL disables); dm_flat_task_levels copies the
- * DAG level of every task (and optionally the 32 lane layers per task) of
+ * DAG level of every task (and optionally the lanes_per_task lane layers per task) of
  * the forward/backward schedule. */
 int dm_flat_set_trace(dm_flat *flat, unsigned long long *trace);
 int dm_flat_task_levels(const dm_flat *flat, int forward, int32_t *levels, int32_t *lane_layers);

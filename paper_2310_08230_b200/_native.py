@@ -42,7 +42,7 @@ class FlatDesc(ctypes.Structure):
 class FlatInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "fw_depth", "bw_depth", "fw_tasks", "bw_tasks", "mma_grid", "mma_block", "max_width",
-        "max_degree", "device_bytes")]
+        "max_degree", "device_bytes", "lanes_per_task")]
 
 
 # name -> (argtypes, restype); kept in sync with include/discomatch_b200.h

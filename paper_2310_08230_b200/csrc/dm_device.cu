@@ -373,6 +373,10 @@ struct MmaArgs {
     int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
     int warm;                   // prefetch the polled lines into L2 at task start
     const uint64_t *relax_layer;  // per-layer source nibbles (forward, W == 8 only)
+    // node-parallel kernels: task -> visitation position, its copies (CSR) and
+    // per-layer first/last flags (bit 0 first layer of its BDD, bit 1 last)
+    const int32_t *task_pos, *proc_ptr, *proc_layers;
+    const uint8_t *layer_flags;
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -775,6 +779,286 @@ __global__ void __launch_bounds__(256) mma_backward_kernel(MmaArgs a) {
     }
 }
 
+// ===========================================================================
+// Node-parallel exact passes: one warp task per visitation position (one
+// variable), 4 lanes per BDD copy, 2 nodes per lane (layers up to 8 nodes,
+// up to 8 copies).  Lane 4c+q handles nodes 2q, 2q+1 of copy c's layer.
+// Same DAG schedule, same arithmetic and reduction trees as the per-copy
+// kernels above — the min trees are split across the copy's 4 lanes with
+// xor shuffles that keep tree_lmin<8>'s shape — so the duals are
+// bit-identical; a task's post-wait work is ~4x fewer instructions and runs
+// once (one group per warp).
+// ===========================================================================
+constexpr int kNpCopies = 8;
+
+__device__ __forceinline__ void np_trace(const MmaArgs &a, int64_t task, int c, int q, int slot, uint64_t t) {
+    if (a.trace && q == 0) a.trace[(task * kNpCopies + c) * 6 + slot] = t;
+}
+
+// leftmost min across the 4 lanes of a copy (lower lane = lower node index)
+__device__ __forceinline__ double np_lmin4(double v, int q) {
+#pragma unroll
+    for (int s = 1; s < 4; s <<= 1) {
+        const double o = __shfl_xor_sync(kFull, v, s);
+        v = (q & s) ? lmin(o, v) : lmin(v, o);
+    }
+    return v;
+}
+
+// value of node i (0..7) of copy c from the lane pair that holds it
+__device__ __forceinline__ double np_node(double v0, double v1, int c, int i) {
+    const int src = 4 * c + ((i >> 1) & 3);
+    const double a = __shfl_sync(kFull, v0, src), b = __shfl_sync(kFull, v1, src);
+    return (i & 1) ? b : a;
+}
+
+// Sequential sum of the copies' deltas in copy order + the new dual, as
+// average_in_group (same +0.0 / exact-reciprocal identities).
+__device__ __forceinline__ double np_average(bool act, int k, int q, double m0, double m1, double lam_l) {
+    const bool fin = act && m0 != DM_INF && m1 != DM_INF;
+    const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
+    const unsigned finmask = __ballot_sync(kFull, fin && q == 0);
+    double dk[kNpCopies];
+#pragma unroll
+    for (int c = 0; c < kNpCopies; ++c) dk[c] = __shfl_sync(kFull, dlt, 4 * c);
+    double fsum = 0.0;
+#pragma unroll
+    for (int c = 0; c < kNpCopies; ++c)
+        if (c < k) fsum = __dadd_rn(fsum, dk[c]);
+    const int fcnt = __popc(finmask);
+    if (fin && fcnt > 0) {
+        double avg;
+        if ((fcnt & (fcnt - 1)) == 0)
+            avg = __dmul_rn(fsum, fcnt == 1 ? 1.0 : fcnt == 2 ? 0.5 : fcnt == 4 ? 0.25 : 0.125);
+        else
+            avg = __ddiv_rn(fsum, (double)fcnt);
+        lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
+    }
+    return lam_l;
+}
+
+struct NpLane {
+    int c, q, k;
+    bool act, first, last;
+    int32_t l, nlo, w;
+};
+
+__device__ __forceinline__ NpLane np_lane(const MmaArgs &a, int64_t task, int lane) {
+    NpLane r;
+    r.c = lane >> 2;
+    r.q = lane & 3;
+    const int32_t p = a.task_pos[task];
+    const int32_t lo = a.proc_ptr[p];
+    r.k = a.proc_ptr[p + 1] - lo;
+    r.act = r.c < r.k;
+    r.l = r.act ? a.proc_layers[lo + r.c] : -1;
+    const int fl = r.act ? a.layer_flags[r.l] : 0;
+    r.first = fl & 1;
+    r.last = fl & 2;
+    r.nlo = r.act ? a.lnl[r.l] : 0;
+    r.w = r.act ? a.lnl[r.l + 1] - r.nlo : 0;
+    return r;
+}
+
+template <bool D>
+__global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
+        const NpLane r = np_lane(a, task, lane);
+        const int i0 = 2 * r.q, i1 = i0 + 1;
+        int32_t n0 = 0, wn = 0;
+        double lam_l = 0.0;
+        int32_t z0 = dm::kFalse, z1 = dm::kFalse, o0 = dm::kFalse, o1 = dm::kFalse;
+        uint64_t desc = 0;
+        if (r.act) {
+            if (!r.last) {
+                n0 = a.lnl[r.l + 1];
+                wn = a.lnl[r.l + 2] - n0;
+                if (D) desc = a.relax_layer[r.l];
+            }
+            lam_l = a.lam[r.l];
+            if (i0 < r.w) z0 = a.zero_t[r.nlo + i0], o0 = a.one_t[r.nlo + i0];
+            if (i1 < r.w) z1 = a.zero_t[r.nlo + i1], o1 = a.one_t[r.nlo + i1];
+        }
+        // marginal arc terms (see layer_marginals): +INF FALSE/padding, -0.0 TRUE
+        const double t00 = arc_term(z0, z0 >= 0 ? a.B[z0] : 0.0), t01 = arc_term(z1, z1 >= 0 ? a.B[z1] : 0.0);
+        const double t10 = arc_term(o0, o0 >= 0 ? a.B[o0] : 0.0), t11 = arc_term(o1, o1 >= 0 ? a.B[o1] : 0.0);
+        double f0 = DM_INF, f1 = DM_INF;
+        bool have = !r.act || i0 >= r.w;
+        unsigned spins = 0;
+        const uint64_t t_wait = global_ns();
+        if (r.act) np_trace(a, task, r.c, r.q, 0, t_wait);
+        const double *src0 = a.F + r.nlo + (i0 < r.w ? i0 : 0), *src1 = a.F + r.nlo + (i1 < r.w ? i1 : i0 < r.w ? i0 : 0);
+        while (true) {
+            if (!have) {
+                const uint64_t t_issue = a.trace ? global_ns() : 0;
+                const double v0 = ld_relaxed(src0), v1 = ld_relaxed(src1);
+                if (!is_sentinel(v0) && !is_sentinel(v1)) {
+                    have = true;
+                    f0 = v0;
+                    f1 = i1 < r.w ? v1 : DM_INF;
+                    if (a.trace) {
+                        np_trace(a, task, r.c, r.q, 1, global_ns());
+                        np_trace(a, task, r.c, r.q, 5, t_issue);
+                    }
+                }
+            }
+            if (__all_sync(kFull, have)) break;
+            if (watchdog(a, t_wait, spins)) return;
+            if (a.sleep_ns) __nanosleep(a.sleep_ns);
+        }
+        if (r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
+        // min-marginals over the layer (tree_lmin<8> split over the 4 lanes)
+        const double m0 = np_lmin4(lmin(__dadd_rn(f0, t00), __dadd_rn(f1, t01)), r.q);
+        const double m1 = np_lmin4(lmin(__dadd_rn(__dadd_rn(f0, lam_l), t10), __dadd_rn(__dadd_rn(f1, lam_l), t11)), r.q);
+        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
+        if (r.act && r.q == 0) a.lam[r.l] = lam_l;
+        if (r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
+        const double c0 = __dadd_rn(f0, lam_l), c1 = __dadd_rn(f1, lam_l);
+        if (D) {
+            // targets 2q, 2q+1 of the next layer from the per-layer source nibbles
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int u = i0 + j;
+                const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
+                const double fa = np_node(f0, f1, r.c, zi & 7), fo = np_node(f0, f1, r.c, oi & 7);
+                const double A = zi < 8 ? fa : DM_INF;
+                const double C = oi < 8 ? __dadd_rn(fo, lam_l) : DM_INF;
+                if (r.act && !r.last && u < wn) st_relaxed(a.F + n0 + u, (C < A || (C == A && oi < zi)) ? C : A);
+            }
+        } else {
+            // generic scatter: every target is the leftmost minimum over (node
+            // ascending, zero arc, one arc), gathered from all 8 nodes
+            double fv[8], cv[8];
+            int32_t zv[8], ov[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                fv[i] = np_node(f0, f1, r.c, i);
+                cv[i] = np_node(c0, c1, r.c, i);
+                const int src = 4 * r.c + (i >> 1);
+                const int32_t za = __shfl_sync(kFull, z0, src), zb = __shfl_sync(kFull, z1, src);
+                const int32_t oa = __shfl_sync(kFull, o0, src), ob = __shfl_sync(kFull, o1, src);
+                zv[i] = (i & 1) ? zb : za;
+                ov[i] = (i & 1) ? ob : oa;
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int u = i0 + j;
+                const int32_t tgt = n0 + u;
+                double cand[16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    cand[2 * i] = zv[i] == tgt ? fv[i] : DM_INF;
+                    cand[2 * i + 1] = ov[i] == tgt ? cv[i] : DM_INF;
+                }
+                const double v = tree_lmin<16>(cand);
+                if (r.act && !r.last && u < wn) st_relaxed(a.F + tgt, v);
+            }
+        }
+        {
+            // bound of a diagram whose last layer this is: leftmost min over
+            // (node, zero arc, one arc) of the arcs into TRUE (tree_lmin<16>
+            // split over the 4 lanes; every lane shuffles, the warp stays converged)
+            const double a0 = z0 == dm::kTrue ? f0 : DM_INF, b0 = o0 == dm::kTrue ? c0 : DM_INF;
+            const double a1 = z1 == dm::kTrue ? f1 : DM_INF, b1 = o1 == dm::kTrue ? c1 : DM_INF;
+            const double bound = np_lmin4(lmin(lmin(a0, b0), lmin(a1, b1)), r.q);
+            if (r.act && r.last && r.q == 0) a.bounds[a.layer_bdd[r.l]] = bound;
+        }
+        if (r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
+    }
+}
+
+__global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
+        const NpLane r = np_lane(a, task, lane);
+        const int i0 = 2 * r.q, i1 = i0 + 1;
+        int32_t n0n = 0, wnext = 0;
+        double lam_l = 0.0;
+        if (r.act) {
+            if (!r.last) {
+                n0n = a.lnl[r.l + 1];
+                wnext = a.lnl[r.l + 2] - n0n;
+            }
+            lam_l = a.lam[r.l];
+        }
+        // per node: next-layer slot of each arc (8 = terminal/padding: -0.0),
+        // marginal bases and rebuild offsets as in mma_backward_kernel
+        int iz[2] = {8, 8}, io[2] = {8, 8};
+        double f0b[2] = {DM_INF, DM_INF}, f1b[2] = {DM_INF, DM_INF}, rz[2] = {DM_INF, DM_INF},
+               ro[2] = {DM_INF, DM_INF};
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = i0 + j;
+            if (r.act && i < r.w) {
+                const int32_t z = a.zero_t[r.nlo + i], o = a.one_t[r.nlo + i];
+                const double fv = a.F[r.nlo + i];
+                iz[j] = z >= 0 ? ((z - n0n) & 7) : 8;
+                io[j] = o >= 0 ? ((o - n0n) & 7) : 8;
+                f0b[j] = z == dm::kFalse ? DM_INF : fv;
+                f1b[j] = o == dm::kFalse ? DM_INF : __dadd_rn(fv, lam_l);
+                rz[j] = z == dm::kFalse ? DM_INF : (z == dm::kTrue ? 0.0 : -0.0);
+                ro[j] = o == dm::kFalse ? DM_INF : -0.0;
+            }
+        }
+        // this lane polls next-layer nodes 2q, 2q+1
+        double nb0 = -0.0, nb1 = -0.0;
+        bool have = !r.act || r.last || i0 >= wnext;
+        unsigned spins = 0;
+        const uint64_t t_wait = global_ns();
+        if (r.act) np_trace(a, task, r.c, r.q, 0, t_wait);
+        const double *src0 = a.B + n0n + (i0 < wnext ? i0 : 0);
+        const double *src1 = a.B + n0n + (i1 < wnext ? i1 : i0 < wnext ? i0 : 0);
+        while (true) {
+            if (!have) {
+                const uint64_t t_issue = a.trace ? global_ns() : 0;
+                const double v0 = ld_relaxed(src0), v1 = ld_relaxed(src1);
+                if (!is_sentinel(v0) && !is_sentinel(v1)) {
+                    have = true;
+                    nb0 = v0;
+                    nb1 = i1 < wnext ? v1 : -0.0;
+                    if (a.trace) {
+                        np_trace(a, task, r.c, r.q, 1, global_ns());
+                        np_trace(a, task, r.c, r.q, 5, t_issue);
+                    }
+                }
+            }
+            if (__all_sync(kFull, have)) break;
+            if (watchdog(a, t_wait, spins)) return;
+            if (a.sleep_ns) __nanosleep(a.sleep_ns);
+        }
+        if (r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
+        // route the next layer's distances to this lane's arcs
+        double tz[2], to[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const double vz = np_node(nb0, nb1, r.c, iz[j] & 7), vo = np_node(nb0, nb1, r.c, io[j] & 7);
+            tz[j] = iz[j] < 8 ? vz : -0.0;
+            to[j] = io[j] < 8 ? vo : -0.0;
+        }
+        const double m0 = np_lmin4(lmin(__dadd_rn(f0b[0], tz[0]), __dadd_rn(f0b[1], tz[1])), r.q);
+        const double m1 = np_lmin4(lmin(__dadd_rn(f1b[0], to[0]), __dadd_rn(f1b[1], to[1])), r.q);
+        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
+        if (r.act && r.q == 0) a.lam[r.l] = lam_l;
+        if (r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
+        // rebuild this layer's distances to TRUE (kernels.py:340-358)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = i0 + j;
+            if (r.act && i < r.w) {
+                const double cz = __dadd_rn(rz[j], tz[j]);
+                const double co = __dadd_rn(__dadd_rn(lam_l, to[j]), ro[j]);
+                const double bv = (cz <= co) ? cz : co;
+                st_relaxed(a.B + r.nlo + i, bv);
+                if (i == 0 && r.first) a.bounds[a.layer_bdd[r.l]] = bv;  // kernels.py:359-361
+            }
+        }
+        if (r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
+    }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -805,6 +1089,12 @@ struct dm_flat {
     uint64_t *relax_layer = nullptr;  // forward publish descriptors (W == 8 instances)
     bool relax_ok = false;
     bool mma_desc = true;
+    // node-parallel exact passes (layers <= 8 nodes, <= 8 copies per variable)
+    bool np_ok = false, mma_np = false;
+    int32_t *fw_pos = nullptr, *bw_pos = nullptr;
+    uint8_t *layer_flags = nullptr;
+    int64_t np_fw_tasks = 0, np_bw_tasks = 0;
+    std::vector<int32_t> fw_pos_level, bw_pos_level, fw_pos_h, bw_pos_h;  // host copies (profiling)
     int mma_w = 8, mma_k = 8;
     int mma_threads = 256, mma_blocks_per_sm = 0;
     unsigned mma_sleep_ns = 0;
@@ -891,6 +1181,13 @@ inline int grid_stride_blocks(int64_t n) { return (int)std::min<int64_t>(148 * 1
 // when every non-final layer of the instance has one source per arc kind.
 template <int W, int K>
 const void *mma_fn(const dm_flat *f, bool forward) {
+    if constexpr (W == 8 && K == 8) {
+        if (f->mma_np) {
+            if (!forward) return (const void *)mma_np_backward_kernel;
+            return f->relax_ok && f->mma_desc ? (const void *)mma_np_forward_kernel<true>
+                                              : (const void *)mma_np_forward_kernel<false>;
+        }
+    }
     if (!forward) return (const void *)mma_backward_kernel<W, K>;
     if constexpr (W == 8) {
         if (f->relax_ok && f->mma_desc) return (const void *)mma_forward_kernel<8, K, true>;
@@ -935,6 +1232,7 @@ static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sl
     f->mma_lookahead = lookahead < 0 ? 0 : (lookahead & 0xffff);
     f->mma_warm = (lookahead >> 16) & 1;   // bit 16 of the lookahead word: L2 warming
     f->mma_desc = !((lookahead >> 17) & 1);  // bit 17: force the tree publish
+    f->mma_np = f->np_ok && !((lookahead >> 18) & 1);  // bit 18: force the per-copy kernels
     if (threads < 32 || threads > 256 || threads % 32) {
         dm::set_error("exact-pass block size must be a multiple of 32 in [32, 256]");
         return DM_ERR_INVALID;
@@ -1142,10 +1440,28 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     }
     f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
     f->mma_k = max_degree <= 8 ? 8 : 32;
+    if (f->mma_w == 8 && f->mma_k == 8) {
+        std::vector<uint8_t> flags(L, 0);
+        for (int64_t j = 0; j < nb; ++j) {
+            flags[bl[j]] |= 1;
+            flags[bl[j + 1] - 1] |= 2;
+        }
+        if ((rc = upload(f.get(), &f->layer_flags, flags.data(), L, s))) return rc;
+        if ((rc = up(&f->fw_pos, fw.pos_order))) return rc;
+        if ((rc = up(&f->bw_pos, bw.pos_order))) return rc;
+        DM_CUDA(cudaStreamSynchronize(s));  // `flags` dies with this scope
+        f->np_fw_tasks = (int64_t)fw.pos_order.size();
+        f->np_bw_tasks = (int64_t)bw.pos_order.size();
+        f->fw_pos_level = std::move(fw.pos_order_level);
+        f->bw_pos_level = std::move(bw.pos_order_level);
+        f->fw_pos_h = std::move(fw.pos_order);
+        f->bw_pos_h = std::move(bw.pos_order);
+        f->np_ok = true;
+    }
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 2),
                        (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
                        env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16) |
-                           ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17));
+                           ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17) | ((env_int("DM_MMA_NP", 1) ? 0 : 1) << 18));
     if (rc) return rc;
     DevPlan *dummy;
     if ((rc = get_plan(nb, &dummy))) return rc;
@@ -1165,8 +1481,9 @@ int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
     }
     info->fw_depth = f->fw_depth;
     info->bw_depth = f->bw_depth;
-    info->fw_tasks = f->fw_tasks;
-    info->bw_tasks = f->bw_tasks;
+    info->fw_tasks = f->mma_np ? f->np_fw_tasks : f->fw_tasks;
+    info->bw_tasks = f->mma_np ? f->np_bw_tasks : f->bw_tasks;
+    info->lanes_per_task = f->mma_np ? 8 : 32;
     info->mma_grid = f->mma_grid_fw;
     info->mma_block = f->mma_threads;
     info->max_width = f->max_width;
@@ -1202,6 +1519,22 @@ int dm_flat_task_levels(const dm_flat *f, int forward, int32_t *levels, int32_t 
     if (!f) {
         dm::set_error("invalid arguments");
         return DM_ERR_INVALID;
+    }
+    if (f->mma_np) {  // one task per position, 8 copy slots per task
+        const auto &v = forward ? f->fw_pos_level : f->bw_pos_level;
+        const auto &pos = forward ? f->fw_pos_h : f->bw_pos_h;
+        if (levels) std::memcpy(levels, v.data(), v.size() * sizeof(int32_t));
+        if (lane_layers) {
+            std::vector<int32_t> pp(f->P + 1), pl(f->L);
+            DM_CUDA(cudaMemcpy(pp.data(), f->proc_ptr, pp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            DM_CUDA(cudaMemcpy(pl.data(), f->proc_layers, pl.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            for (size_t t = 0; t < pos.size(); ++t)
+                for (int c = 0; c < 8; ++c) {
+                    const int32_t lo = pp[pos[t]], k = pp[pos[t] + 1] - lo;
+                    lane_layers[t * 8 + c] = c < k ? pl[lo + c] : -1;
+                }
+        }
+        return DM_OK;
     }
     const auto &v = forward ? f->fw_level : f->bw_level;
     const auto &w = forward ? f->fw_layer_h : f->bw_layer_h;
@@ -1287,6 +1620,14 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.lookahead = f->mma_lookahead;
     args.warm = f->mma_warm;
     args.relax_layer = f->relax_layer;
+    args.task_pos = forward ? f->fw_pos : f->bw_pos;
+    args.proc_ptr = f->proc_ptr;
+    args.proc_layers = f->proc_layers;
+    args.layer_flags = f->layer_flags;
+    if (f->mma_np) {
+        args.ntasks = forward ? f->np_fw_tasks : f->np_bw_tasks;
+        args.lookahead = 0;  // the progress gate indexes per-copy task levels
+    }
     DM_CUDA(cudaMemsetAsync(f->progress, 0xff, sizeof(int), s));  // -1: nothing finished
 #define DM_LAUNCH(W, K) launch_mma<W, K>(f, forward, args, s)
     return DM_MMA_DISPATCH(f, DM_LAUNCH);

@@ -350,6 +350,12 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
             if (pos_level[p] >= 0) bylevel[at[pos_level[p]]++] = p;
         }
     }
+    s.pos_order.resize(bylevel.size());
+    s.pos_order_level.resize(bylevel.size());
+    for (size_t i = 0; i < bylevel.size(); ++i) {
+        s.pos_order[i] = (int32_t)bylevel[i];
+        s.pos_order_level[i] = pos_level[bylevel[i]];
+    }
     s.task_layer.clear();
     s.task_meta.clear();
     s.depth = depth;

@@ -62,6 +62,9 @@ PairwisePlan plan_pairwise(int64_t n);
 struct MmaSchedule {
     std::vector<int32_t> task_layer, task_meta, task_level;
     int64_t depth = 0, tasks = 0;
+    // one task per visitation position (the node-parallel kernels): positions
+    // with copies in level order, and their levels
+    std::vector<int32_t> pos_order, pos_order_level;
 };
 int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_bdd_or_null,
                        const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,

@@ -40,10 +40,15 @@ def oracle_twin(inst):
     return model.from_flat_table(inst.costs, inst.variable_order, f.constraint_counts, arrays)
 
 
+MMA_KERNELS = {"node_parallel": 0, "per_copy": 1 << 18}  # dm_flat_set_mma_config lookahead-word bit 18
+
+
+@pytest.mark.parametrize("kernels", list(MMA_KERNELS))
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
-def test_exact_passes_match_reference(case):
+def test_exact_passes_match_reference(case, kernels):
     inst = product_instance(case)
     st = init_duals(inst)
+    st.dev.set_mma_config(256, 2, 0, False, (1 << 16) | MMA_KERNELS[kernels])
     assert st.bound == case["init"]["bound"]
     assert h(st.lam) == case["init"]["lam"]
     mma_pass(st, FORWARD)

@@ -21,17 +21,18 @@ from paper_2310_08230_b200.dual import BACKWARD, FORWARD, init_duals, mma_pass  
 
 def analyse(st, forward, trace, name):
     ntask = st.dev.info["fw_tasks" if forward else "bw_tasks"]
+    lpt = int(st.dev.info.get("lanes_per_task", 32) or 32)
     levels = np.zeros(ntask, np.int32)
-    layers = np.zeros(ntask * 32, np.int32)
+    layers = np.zeros(ntask * lpt, np.int32)
     _native.check(_native.load().dm_flat_task_levels(st.dev.handle, int(forward), levels.ctypes.data,
                                                     layers.ctypes.data))
-    tr = trace.cpu().numpy().reshape(ntask * 32, 6).astype(np.int64)
+    tr = trace.cpu().numpy().reshape(ntask * lpt, 6).astype(np.int64)
     act = layers >= 0
     t0 = tr[act, 0].min()
     start, own, seen, upd, done, issue = (tr[:, k] - t0 for k in range(6))
     issue = np.where(tr[:, 5] == 0, start, issue)
     own = np.where(tr[:, 1] == 0, start, own)  # lanes without dependencies are ready at start
-    lane_level = np.repeat(levels, 32)
+    lane_level = np.repeat(levels, lpt)
     # producer lane of each lane: layer l-1 (forward) / l+1 (backward) in the same diagram
     f = st.flat
     L = f.num_layers
@@ -67,15 +68,15 @@ def analyse(st, forward, trace, name):
     # critical chain: walk back from the last published lane
     var_of = np.where(act, f.layer_var[np.clip(l, 0, L - 1)], -1)
     nwarps = int(st.dev.info["mma_grid"] * st.dev.info["mma_block"] // 32)
-    task_done = done.reshape(-1, 32).max(axis=1)
+    task_done = np.where(act, done, 0).reshape(-1, lpt).max(axis=1)
     seg = {"work": 0, "gate": 0, "comm": 0, "comm_to_issue": 0, "comm_poll_rtt": 0, "late_poll": 0, "warp_busy": 0}
     nseg = {k: 0 for k in seg}
     cur = int(np.flatnonzero(act)[np.argmax(done[act])])
     steps = 0
     while steps < 100000:
         steps += 1
-        t = cur // 32
-        lanes = np.arange(t * 32, t * 32 + 32)
+        t = cur // lpt
+        lanes = np.arange(t * lpt, t * lpt + lpt)
         grp = lanes[(var_of[lanes] == var_of[cur]) & act[lanes]]
         crit = int(grp[np.argmax(own[grp])])
         seg["work"] += done[cur] - seen[cur]; nseg["work"] += 1
@@ -87,11 +88,11 @@ def analyse(st, forward, trace, name):
             cur = int(pslot[crit])
         else:
             seg["late_poll"] += own[crit] - start[crit]; nseg["late_poll"] += 1
-            prev = (cur // 32) - nwarps
+            prev = (cur // lpt) - nwarps
             if prev < 0:
                 break
             seg["warp_busy"] += start[crit] - task_done[prev]; nseg["warp_busy"] += 1
-            cur = int(prev * 32 + np.argmax(done[prev * 32:prev * 32 + 32]))
+            cur = int(prev * lpt + np.argmax(np.where(act[prev * lpt:prev * lpt + lpt], done[prev * lpt:prev * lpt + lpt], -1)))
     out["critical_chain"] = {k: {"total_ns": int(v), "n": nseg[k], "mean_ns": float(v / max(nseg[k], 1))}
                              for k, v in seg.items()}
     out["critical_chain_start_ns"] = int(start[cur])
@@ -111,7 +112,8 @@ def main():
         mma_pass(st, BACKWARD)
     for forward, name in ((True, "forward"), (False, "backward")):
         ntask = st.dev.info["fw_tasks" if forward else "bw_tasks"]
-        trace = torch.zeros(ntask * 32 * 6, dtype=torch.int64, device=st.device)
+        lpt = int(st.dev.info.get("lanes_per_task", 32) or 32)
+        trace = torch.zeros(ntask * lpt * 6, dtype=torch.int64, device=st.device)
         _native.check(_native.load().dm_flat_set_trace(st.dev.handle, trace.data_ptr()))
         mma_pass(st, FORWARD if forward else BACKWARD)
         torch.cuda.synchronize()
