@@ -377,6 +377,9 @@ struct MmaArgs {
     // per-layer first/last flags (bit 0 first layer of its BDD, bit 1 last)
     const int32_t *task_pos, *proc_ptr, *proc_layers;
     const uint8_t *layer_flags;
+    // per position p, 8 copy records {layer, first node, w | wn<<8 | flags<<16 | k<<24, 0}
+    const int4 *np_rec;
+    int *task_counter;  // dynamic task queue of the node-parallel kernels
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -450,6 +453,11 @@ __device__ __forceinline__ double tree_lmin(double (&v)[N]) {
 // adding +0.0 leaves it bit-unchanged.  Division by a power-of-two count is a
 // multiplication by its exact reciprocal (both correctly rounded from the same
 // real quotient); other counts take __ddiv_rn.
+// 1/n for n a power of two, built from the exponent bits (no table lookup)
+__device__ __forceinline__ double exact_inverse_pow2(int n) {
+    return __longlong_as_double((long long)(1023 - (__ffs(n) - 1)) << 52);
+}
+
 template <int K>
 __device__ __forceinline__ double average_in_group(bool go, int32_t meta, unsigned gmask, double m0, double m1,
                                                    double lam_l) {
@@ -468,7 +476,7 @@ __device__ __forceinline__ double average_in_group(bool go, int32_t meta, unsign
     if (fin && fcnt > 0) {
         double avg;
         if ((fcnt & (fcnt - 1)) == 0)
-            avg = __dmul_rn(fsum, fcnt == 1 ? 1.0 : fcnt == 2 ? 0.5 : fcnt == 4 ? 0.25 : fcnt == 8 ? 0.125 : 1.0 / fcnt);
+            avg = __dmul_rn(fsum, exact_inverse_pow2(fcnt));
         else
             avg = __ddiv_rn(fsum, (double)fcnt);
         lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
@@ -829,7 +837,7 @@ __device__ __forceinline__ double np_average(bool act, int k, int q, double m0, 
     if (fin && fcnt > 0) {
         double avg;
         if ((fcnt & (fcnt - 1)) == 0)
-            avg = __dmul_rn(fsum, fcnt == 1 ? 1.0 : fcnt == 2 ? 0.5 : fcnt == 4 ? 0.25 : 0.125);
+            avg = __dmul_rn(fsum, exact_inverse_pow2(fcnt));
         else
             avg = __ddiv_rn(fsum, (double)fcnt);
         lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
@@ -843,29 +851,55 @@ struct NpLane {
     int32_t l, nlo, w;
 };
 
-__device__ __forceinline__ NpLane np_lane(const MmaArgs &a, int64_t task, int lane) {
-    NpLane r;
+struct NpLaneX : NpLane {
+    int32_t wn;  // width of the next layer (0 for a last layer)
+};
+
+// Two dependent loads per task: its position, then the copy's packed record.
+// watchdog with a lazily taken start time (no %globaltimer read per task)
+__device__ __forceinline__ bool np_watchdog(const MmaArgs &a, uint64_t &t_start, unsigned &spins) {
+    if ((++spins & 63u) != 0) return false;
+    if (*(volatile int *)a.status) return true;
+    const uint64_t now = global_ns();
+    if (t_start == 0) t_start = now;
+    if (now - t_start > kWaitLimitNs) {
+        atomicExch(a.status, 1);
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ NpLaneX np_lane(const MmaArgs &a, int64_t task, int lane) {
+    NpLaneX r;
     r.c = lane >> 2;
     r.q = lane & 3;
     const int32_t p = a.task_pos[task];
-    const int32_t lo = a.proc_ptr[p];
-    r.k = a.proc_ptr[p + 1] - lo;
+    const int4 rec = a.np_rec[(int64_t)p * kNpCopies + r.c];
+    const unsigned m = (unsigned)rec.z;
+    r.k = (int)(m >> 24);
     r.act = r.c < r.k;
-    r.l = r.act ? a.proc_layers[lo + r.c] : -1;
-    const int fl = r.act ? a.layer_flags[r.l] : 0;
-    r.first = fl & 1;
-    r.last = fl & 2;
-    r.nlo = r.act ? a.lnl[r.l] : 0;
-    r.w = r.act ? a.lnl[r.l + 1] - r.nlo : 0;
+    r.l = rec.x;
+    r.nlo = rec.y;
+    r.w = (int)(m & 0xff);
+    r.wn = (int)((m >> 8) & 0xff);
+    r.first = (m >> 16) & 1;
+    r.last = (m >> 17) & 1;
     return r;
+}
+
+// Next task of this warp from the pass's queue (tasks are level-ordered, so a
+// warp only ever waits on tasks already taken by running warps).
+__device__ __forceinline__ int64_t np_next_task(const MmaArgs &a, int lane) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.task_counter, 1);
+    return __shfl_sync(kFull, t, 0);
 }
 
 template <bool D>
 __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
-        const NpLane r = np_lane(a, task, lane);
+    for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
+        const NpLaneX r = np_lane(a, task, lane);
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0 = 0, wn = 0;
         double lam_l = 0.0;
@@ -873,8 +907,8 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
         uint64_t desc = 0;
         if (r.act) {
             if (!r.last) {
-                n0 = a.lnl[r.l + 1];
-                wn = a.lnl[r.l + 2] - n0;
+                n0 = r.nlo + r.w;
+                wn = r.wn;
                 if (D) desc = a.relax_layer[r.l];
             }
             lam_l = a.lam[r.l];
@@ -887,8 +921,8 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
         double f0 = DM_INF, f1 = DM_INF;
         bool have = !r.act || i0 >= r.w;
         unsigned spins = 0;
-        const uint64_t t_wait = global_ns();
-        if (r.act) np_trace(a, task, r.c, r.q, 0, t_wait);
+        uint64_t t_wait = 0;
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 0, global_ns());
         const double *src0 = a.F + r.nlo + (i0 < r.w ? i0 : 0), *src1 = a.F + r.nlo + (i1 < r.w ? i1 : i0 < r.w ? i0 : 0);
         while (true) {
             if (!have) {
@@ -905,16 +939,16 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
                 }
             }
             if (__all_sync(kFull, have)) break;
-            if (watchdog(a, t_wait, spins)) return;
+            if (__any_sync(kFull, np_watchdog(a, t_wait, spins))) return;  // the whole warp leaves together
             if (a.sleep_ns) __nanosleep(a.sleep_ns);
         }
-        if (r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
         // min-marginals over the layer (tree_lmin<8> split over the 4 lanes)
         const double m0 = np_lmin4(lmin(__dadd_rn(f0, t00), __dadd_rn(f1, t01)), r.q);
         const double m1 = np_lmin4(lmin(__dadd_rn(__dadd_rn(f0, lam_l), t10), __dadd_rn(__dadd_rn(f1, lam_l), t11)), r.q);
         lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
-        if (r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         const double c0 = __dadd_rn(f0, lam_l), c1 = __dadd_rn(f1, lam_l);
         if (D) {
             // targets 2q, 2q+1 of the next layer from the per-layer source nibbles
@@ -965,22 +999,21 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
             const double bound = np_lmin4(lmin(lmin(a0, b0), lmin(a1, b1)), r.q);
             if (r.act && r.last && r.q == 0) a.bounds[a.layer_bdd[r.l]] = bound;
         }
-        if (r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
     }
 }
 
 __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
     const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < a.ntasks; task += nwarps) {
-        const NpLane r = np_lane(a, task, lane);
+    for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
+        const NpLaneX r = np_lane(a, task, lane);
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0n = 0, wnext = 0;
         double lam_l = 0.0;
         if (r.act) {
             if (!r.last) {
-                n0n = a.lnl[r.l + 1];
-                wnext = a.lnl[r.l + 2] - n0n;
+                n0n = r.nlo + r.w;
+                wnext = r.wn;
             }
             lam_l = a.lam[r.l];
         }
@@ -1007,8 +1040,8 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         double nb0 = -0.0, nb1 = -0.0;
         bool have = !r.act || r.last || i0 >= wnext;
         unsigned spins = 0;
-        const uint64_t t_wait = global_ns();
-        if (r.act) np_trace(a, task, r.c, r.q, 0, t_wait);
+        uint64_t t_wait = 0;
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 0, global_ns());
         const double *src0 = a.B + n0n + (i0 < wnext ? i0 : 0);
         const double *src1 = a.B + n0n + (i1 < wnext ? i1 : i0 < wnext ? i0 : 0);
         while (true) {
@@ -1026,10 +1059,10 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 }
             }
             if (__all_sync(kFull, have)) break;
-            if (watchdog(a, t_wait, spins)) return;
+            if (__any_sync(kFull, np_watchdog(a, t_wait, spins))) return;  // the whole warp leaves together
             if (a.sleep_ns) __nanosleep(a.sleep_ns);
         }
-        if (r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
         // route the next layer's distances to this lane's arcs
         double tz[2], to[2];
 #pragma unroll
@@ -1042,7 +1075,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         const double m1 = np_lmin4(lmin(__dadd_rn(f1b[0], to[0]), __dadd_rn(f1b[1], to[1])), r.q);
         lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
-        if (r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         // rebuild this layer's distances to TRUE (kernels.py:340-358)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -1055,7 +1088,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 if (i == 0 && r.first) a.bounds[a.layer_bdd[r.l]] = bv;  // kernels.py:359-361
             }
         }
-        if (r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
+        if (a.trace && r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
     }
 }
 
@@ -1093,6 +1126,7 @@ struct dm_flat {
     bool np_ok = false, mma_np = false;
     int32_t *fw_pos = nullptr, *bw_pos = nullptr;
     uint8_t *layer_flags = nullptr;
+    int4 *np_rec = nullptr;
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
     std::vector<int32_t> fw_pos_level, bw_pos_level, fw_pos_h, bw_pos_h;  // host copies (profiling)
     int mma_w = 8, mma_k = 8;
@@ -1401,7 +1435,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = up(&f->var_count, std::move(var_count)))) return rc;
     if ((rc = up(&f->fw_task_level, fw.task_level))) return rc;
     if ((rc = up(&f->bw_task_level, bw.task_level))) return rc;
-    if ((rc = up(&f->progress, std::vector<int32_t>(1, -1)))) return rc;
+    if ((rc = up(&f->progress, std::vector<int32_t>{-1, 0}))) return rc;  // progress hint, task queue
     f->fw_level = fw.task_level;
     f->bw_level = bw.task_level;
     f->fw_layer_h = fw.task_layer;
@@ -1447,9 +1481,26 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
             flags[bl[j + 1] - 1] |= 2;
         }
         if ((rc = upload(f.get(), &f->layer_flags, flags.data(), L, s))) return rc;
+        std::vector<int4> rec((size_t)P * 8);
+        for (int64_t p = 0; p < P; ++p) {
+            const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
+            for (int c = 0; c < 8; ++c) {
+                int4 r{-1, 0, (int)((unsigned)k << 24), 0};
+                if (c < k) {
+                    const int64_t l = desc->proc_layers[lo + c];
+                    const int64_t w = lnl[l + 1] - lnl[l];
+                    const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
+                    r.x = (int)l;
+                    r.y = (int)lnl[l];
+                    r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) | ((unsigned)k << 24));
+                }
+                rec[(size_t)p * 8 + c] = r;
+            }
+        }
+        if ((rc = upload(f.get(), &f->np_rec, rec.data(), (int64_t)rec.size(), s))) return rc;
         if ((rc = up(&f->fw_pos, fw.pos_order))) return rc;
         if ((rc = up(&f->bw_pos, bw.pos_order))) return rc;
-        DM_CUDA(cudaStreamSynchronize(s));  // `flags` dies with this scope
+        DM_CUDA(cudaStreamSynchronize(s));  // `flags`, `rec` die with this scope
         f->np_fw_tasks = (int64_t)fw.pos_order.size();
         f->np_bw_tasks = (int64_t)bw.pos_order.size();
         f->fw_pos_level = std::move(fw.pos_order_level);
@@ -1458,7 +1509,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         f->bw_pos_h = std::move(bw.pos_order);
         f->np_ok = true;
     }
-    rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 2),
+    rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 3),
                        (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
                        env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16) |
                            ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17) | ((env_int("DM_MMA_NP", 1) ? 0 : 1) << 18));
@@ -1624,11 +1675,14 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.proc_ptr = f->proc_ptr;
     args.proc_layers = f->proc_layers;
     args.layer_flags = f->layer_flags;
+    args.np_rec = f->np_rec;
+    args.task_counter = f->progress + 1;
     if (f->mma_np) {
         args.ntasks = forward ? f->np_fw_tasks : f->np_bw_tasks;
         args.lookahead = 0;  // the progress gate indexes per-copy task levels
     }
     DM_CUDA(cudaMemsetAsync(f->progress, 0xff, sizeof(int), s));  // -1: nothing finished
+    DM_CUDA(cudaMemsetAsync(f->progress + 1, 0, sizeof(int), s));  // empty task queue
 #define DM_LAUNCH(W, K) launch_mma<W, K>(f, forward, args, s)
     return DM_MMA_DISPATCH(f, DM_LAUNCH);
 #undef DM_LAUNCH

@@ -28,12 +28,8 @@ def main():
     results = []
     ref = None
     configs = []
-    for threads, bps in ((256, 1), (128, 1), (64, 2)):
-        for probe in (0, 1):
-            for look in (0, 2, 4, 8):
-                configs.append((threads, bps, 0, probe, look | (1 << 16)))
-    configs.append((256, 1, 100, 0, 1 << 16))
-    configs.append((256, 1, 0, 0, 0))
+    for threads, bps in ((256, 2), (256, 3), (256, 4), (128, 4), (128, 6), (128, 8), (64, 8), (64, 12), (64, 16)):
+        configs.append((threads, bps, 0, 0, 1 << 16))
     for threads, bps, sleep, probe, look in configs:
         try:
             st.dev.set_mma_config(threads, bps, sleep, probe, look)
