@@ -822,17 +822,21 @@ __device__ __forceinline__ double np_node(double v0, double v1, int c, int i) {
 
 // Sequential sum of the copies' deltas in copy order + the new dual, as
 // average_in_group (same +0.0 / exact-reciprocal identities).
-__device__ __forceinline__ double np_average(bool act, int k, int q, double m0, double m1, double lam_l) {
+// The copies' deltas meet in the warp's shared-memory row `sd` (8 doubles).
+__device__ __forceinline__ double np_average(bool act, int k, int c, int q, double m0, double m1, double lam_l,
+                                             double *sd) {
     const bool fin = act && m0 != DM_INF && m1 != DM_INF;
     const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
     const unsigned finmask = __ballot_sync(kFull, fin && q == 0);
+    if (q == 0) sd[c] = dlt;
+    __syncwarp();
     double dk[kNpCopies];
 #pragma unroll
-    for (int c = 0; c < kNpCopies; ++c) dk[c] = __shfl_sync(kFull, dlt, 4 * c);
+    for (int j = 0; j < kNpCopies; ++j) dk[j] = sd[j];
     double fsum = 0.0;
 #pragma unroll
-    for (int c = 0; c < kNpCopies; ++c)
-        if (c < k) fsum = __dadd_rn(fsum, dk[c]);
+    for (int j = 0; j < kNpCopies; ++j)
+        if (j < k) fsum = __dadd_rn(fsum, dk[j]);
     const int fcnt = __popc(finmask);
     if (fin && fcnt > 0) {
         double avg;
@@ -895,11 +899,22 @@ __device__ __forceinline__ int64_t np_next_task(const MmaArgs &a, int lane) {
     return __shfl_sync(kFull, t, 0);
 }
 
+// Per warp: node values of each copy (9 slots, slot 8 the arc-to-nothing
+// value) and the copies' deltas, in shared memory.
+constexpr int kNpWarps = 8;  // 256-thread blocks
+struct NpShared {
+    double node[kNpWarps][kNpCopies][9];
+    double delta[kNpWarps][kNpCopies];
+};
+
 template <bool D>
 __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
-    const int lane = threadIdx.x & 31;
+    __shared__ NpShared sh;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
+        __syncwarp();  // the previous task's shared-memory reads are done
         const NpLaneX r = np_lane(a, task, lane);
+        double *nodes = sh.node[wib][r.c];
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0 = 0, wn = 0;
         double lam_l = 0.0;
@@ -920,6 +935,9 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
         const double t10 = arc_term(o0, o0 >= 0 ? a.B[o0] : 0.0), t11 = arc_term(o1, o1 >= 0 ? a.B[o1] : 0.0);
         double f0 = DM_INF, f1 = DM_INF;
         bool have = !r.act || i0 >= r.w;
+        nodes[i0] = DM_INF;
+        nodes[i1] = DM_INF;
+        if (r.q == 0) nodes[8] = DM_INF;
         unsigned spins = 0;
         uint64_t t_wait = 0;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 0, global_ns());
@@ -932,6 +950,8 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
                     have = true;
                     f0 = v0;
                     f1 = i1 < r.w ? v1 : DM_INF;
+                    nodes[i0] = f0;
+                    nodes[i1] = f1;
                     if (a.trace) {
                         np_trace(a, task, r.c, r.q, 1, global_ns());
                         np_trace(a, task, r.c, r.q, 5, t_issue);
@@ -946,7 +966,7 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
         // min-marginals over the layer (tree_lmin<8> split over the 4 lanes)
         const double m0 = np_lmin4(lmin(__dadd_rn(f0, t00), __dadd_rn(f1, t01)), r.q);
         const double m1 = np_lmin4(lmin(__dadd_rn(__dadd_rn(f0, lam_l), t10), __dadd_rn(__dadd_rn(f1, lam_l), t11)), r.q);
-        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
+        lam_l = np_average(r.act, r.k, r.c, r.q, m0, m1, lam_l, sh.delta[wib]);  // also orders `nodes`
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         const double c0 = __dadd_rn(f0, lam_l), c1 = __dadd_rn(f1, lam_l);
@@ -956,9 +976,8 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
             for (int j = 0; j < 2; ++j) {
                 const int u = i0 + j;
                 const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
-                const double fa = np_node(f0, f1, r.c, zi & 7), fo = np_node(f0, f1, r.c, oi & 7);
-                const double A = zi < 8 ? fa : DM_INF;
-                const double C = oi < 8 ? __dadd_rn(fo, lam_l) : DM_INF;
+                const double A = nodes[zi < 8 ? zi : 8];                  // slot 8: +INF
+                const double C = __dadd_rn(nodes[oi < 8 ? oi : 8], lam_l);  // +INF + lam = +INF
                 if (r.act && !r.last && u < wn) st_relaxed(a.F + n0 + u, (C < A || (C == A && oi < zi)) ? C : A);
             }
         } else {
@@ -1004,9 +1023,12 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
 }
 
 __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
-    const int lane = threadIdx.x & 31;
+    __shared__ NpShared sh;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
+        __syncwarp();  // the previous task's shared-memory reads are done
         const NpLaneX r = np_lane(a, task, lane);
+        double *nodes = sh.node[wib][r.c];  // next layer's distances, slot 8 = -0.0
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0n = 0, wnext = 0;
         double lam_l = 0.0;
@@ -1039,6 +1061,9 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         // this lane polls next-layer nodes 2q, 2q+1
         double nb0 = -0.0, nb1 = -0.0;
         bool have = !r.act || r.last || i0 >= wnext;
+        nodes[i0] = -0.0;
+        nodes[i1] = -0.0;
+        if (r.q == 0) nodes[8] = -0.0;
         unsigned spins = 0;
         uint64_t t_wait = 0;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 0, global_ns());
@@ -1052,6 +1077,8 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                     have = true;
                     nb0 = v0;
                     nb1 = i1 < wnext ? v1 : -0.0;
+                    nodes[i0] = nb0;
+                    nodes[i1] = nb1;
                     if (a.trace) {
                         np_trace(a, task, r.c, r.q, 1, global_ns());
                         np_trace(a, task, r.c, r.q, 5, t_issue);
@@ -1063,17 +1090,17 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
             if (a.sleep_ns) __nanosleep(a.sleep_ns);
         }
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
-        // route the next layer's distances to this lane's arcs
+        // route the next layer's distances to this lane's arcs (slot 8: -0.0)
+        __syncwarp();
         double tz[2], to[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const double vz = np_node(nb0, nb1, r.c, iz[j] & 7), vo = np_node(nb0, nb1, r.c, io[j] & 7);
-            tz[j] = iz[j] < 8 ? vz : -0.0;
-            to[j] = io[j] < 8 ? vo : -0.0;
+            tz[j] = nodes[iz[j]];
+            to[j] = nodes[io[j]];
         }
         const double m0 = np_lmin4(lmin(__dadd_rn(f0b[0], tz[0]), __dadd_rn(f0b[1], tz[1])), r.q);
         const double m1 = np_lmin4(lmin(__dadd_rn(f1b[0], to[0]), __dadd_rn(f1b[1], to[1])), r.q);
-        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l);
+        lam_l = np_average(r.act, r.k, r.c, r.q, m0, m1, lam_l, sh.delta[wib]);
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         // rebuild this layer's distances to TRUE (kernels.py:340-358)
