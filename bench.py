@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttg", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
-    ap.add_argument("--e2e-iters", type=int, default=10)
+    ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--ttg-max-iters", type=int, default=150)
     return ap.parse_args()
 

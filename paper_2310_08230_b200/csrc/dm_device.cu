@@ -1164,7 +1164,11 @@ struct dm_flat {
     int mma_probe = 0;
     unsigned long long *trace = nullptr;
     std::vector<int32_t> fw_level, bw_level;  // host copy: DAG level of each task
-    std::vector<int32_t> fw_layer_h, bw_layer_h;  // host copy of the lane layers (profiling)
+    std::vector<int32_t> fw_layer_h, bw_layer_h;  // host copy of the lane layers (profiling, lazy upload)
+    std::vector<int32_t> fw_meta_h, bw_meta_h;    // per-copy kernel lane metadata (lazy upload)
+    bool classic_uploaded = false;
+    std::vector<int32_t> pp_h, pl_h;  // host visitation CSR (int32) for the lazy task packing
+    std::vector<uint8_t> flags_h;     // host first/last-layer flags
     int mma_grid_fw = 0, mma_grid_bw = 0;
     int64_t bytes = 0;
     dm::SweepDev sweep;  // interleaved layout for the full-table sweeps
@@ -1291,6 +1295,31 @@ int mma_grid_for(const dm_flat *f, bool forward, int threads, int want_per_sm, i
     (f->mma_k <= 8 ? (f->mma_w == 8 ? CALL(8, 8) : f->mma_w == 16 ? CALL(16, 8) : CALL(32, 8)) \
                    : (f->mma_w == 8 ? CALL(8, 32) : f->mma_w == 16 ? CALL(16, 32) : CALL(32, 32)))
 
+// The per-copy kernels' warp tasks are packed and uploaded the first time
+// those kernels are selected (the node-parallel ones need only positions).
+static int ensure_per_copy_schedules(dm_flat *f, cudaStream_t s) {
+    if (f->classic_uploaded) return DM_OK;
+    dm::MmaSchedule fw, bw;
+    dm::pack_mma_tasks(f->fw_pos_h, f->fw_pos_level, f->pp_h.data(), f->pl_h.data(), f->flags_h.data(), fw);
+    dm::pack_mma_tasks(f->bw_pos_h, f->bw_pos_level, f->pp_h.data(), f->pl_h.data(), f->flags_h.data(), bw);
+    f->fw_tasks = fw.tasks;
+    f->bw_tasks = bw.tasks;
+    int rc;
+    if ((rc = upload(f, &f->fw_layer, fw.task_layer.data(), (int64_t)fw.task_layer.size(), s))) return rc;
+    if ((rc = upload(f, &f->fw_meta, fw.task_meta.data(), (int64_t)fw.task_meta.size(), s))) return rc;
+    if ((rc = upload(f, &f->bw_layer, bw.task_layer.data(), (int64_t)bw.task_layer.size(), s))) return rc;
+    if ((rc = upload(f, &f->bw_meta, bw.task_meta.data(), (int64_t)bw.task_meta.size(), s))) return rc;
+    if ((rc = upload(f, &f->fw_task_level, fw.task_level.data(), (int64_t)fw.task_level.size(), s))) return rc;
+    if ((rc = upload(f, &f->bw_task_level, bw.task_level.data(), (int64_t)bw.task_level.size(), s))) return rc;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_fail(cudaGetLastError(), "per-copy schedule upload");
+    f->fw_level = std::move(fw.task_level);
+    f->bw_level = std::move(bw.task_level);
+    f->fw_layer_h = std::move(fw.task_layer);
+    f->bw_layer_h = std::move(bw.task_layer);
+    f->classic_uploaded = true;
+    return DM_OK;
+}
+
 static int configure_mma(dm_flat *f, int threads, int blocks_per_sm, unsigned sleep_ns, int probe, int lookahead) {
     f->mma_lookahead = lookahead < 0 ? 0 : (lookahead & 0xffff);
     f->mma_warm = (lookahead >> 16) & 1;   // bit 16 of the lookahead word: L2 warming
@@ -1357,27 +1386,51 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     }
     std::vector<int32_t> layer_bdd(L), var_count, pos_var(P, -1);
     int64_t max_width = 0, max_degree = 0;
-    for (int64_t j = 0; j < nb; ++j) {
-        if (bl[j + 1] <= bl[j] || lnl[bl[j] + 1] - lnl[bl[j]] != 1) {
-            dm::set_error("every diagram needs >= 1 layer and a single root node");
-            return DM_ERR_INVALID;
-        }
-        for (int64_t l = bl[j]; l < bl[j + 1]; ++l) {
-            layer_bdd[l] = (int32_t)j;
-            const int64_t w = lnl[l + 1] - lnl[l];
-            if (w <= 0) {
-                dm::set_error("empty layer");
-                return DM_ERR_INVALID;
-            }
-            max_width = std::max(max_width, w);
-            const bool last = l + 1 == bl[j + 1];
-            for (int64_t v = lnl[l]; v < lnl[l + 1]; ++v)
-                for (int64_t t : {desc->zero_t[v], desc->one_t[v]}) {
-                    if (last ? (t >= 0 || t < -2) : (t == -2 || t < -2 || (t >= 0 && (t < lnl[l + 1] || t >= lnl[l + 2])))) {
-                        dm::set_error("arc targets must reach the next layer (or a terminal from the last layer)");
-                        return DM_ERR_UNSUPPORTED;
+    {
+        // diagram ranges validated in parallel; the first failing range reports
+        constexpr int kThreads = 8;
+        int64_t widths[kThreads] = {0};
+        int codes[kThreads] = {DM_OK};
+        const char *msgs[kThreads] = {nullptr};
+        std::vector<std::thread> th;
+        for (int t = 0; t < kThreads; ++t)
+            th.emplace_back([&, t] {
+                const int64_t jlo = nb * t / kThreads, jhi = nb * (t + 1) / kThreads;
+                for (int64_t j = jlo; j < jhi; ++j) {
+                    if (bl[j + 1] <= bl[j] || lnl[bl[j] + 1] - lnl[bl[j]] != 1) {
+                        codes[t] = DM_ERR_INVALID;
+                        msgs[t] = "every diagram needs >= 1 layer and a single root node";
+                        return;
+                    }
+                    for (int64_t l = bl[j]; l < bl[j + 1]; ++l) {
+                        layer_bdd[l] = (int32_t)j;
+                        const int64_t w = lnl[l + 1] - lnl[l];
+                        if (w <= 0) {
+                            codes[t] = DM_ERR_INVALID;
+                            msgs[t] = "empty layer";
+                            return;
+                        }
+                        widths[t] = std::max(widths[t], w);
+                        const bool last = l + 1 == bl[j + 1];
+                        for (int64_t v = lnl[l]; v < lnl[l + 1]; ++v)
+                            for (int64_t tt : {desc->zero_t[v], desc->one_t[v]}) {
+                                if (last ? (tt >= 0 || tt < -2)
+                                         : (tt == -2 || tt < -2 || (tt >= 0 && (tt < lnl[l + 1] || tt >= lnl[l + 2])))) {
+                                    codes[t] = DM_ERR_UNSUPPORTED;
+                                    msgs[t] = "arc targets must reach the next layer (or a terminal from the last layer)";
+                                    return;
+                                }
+                            }
                     }
                 }
+            });
+        for (auto &x : th) x.join();
+        for (int t = 0; t < kThreads; ++t) {
+            if (codes[t] != DM_OK) {
+                dm::set_error(msgs[t]);
+                return codes[t];
+            }
+            max_width = std::max(max_width, widths[t]);
         }
     }
     if (max_width > 32) {
@@ -1398,29 +1451,85 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         }
     }
     const double t_valid = host_seconds();
-    // the two pass schedules and the sweep layout are independent host plans
+    // Independent host plans and conversions run concurrently: the two pass
+    // schedules, the sweep layout, the forward publish descriptors, the
+    // node-parallel copy records and the int32 topology.
+    const bool want_np = max_width <= 8 && max_degree <= 8;
     dm::MmaSchedule fw, bw;
     dm::SweepLayout sl;
     std::vector<uint64_t> relax;
     bool relax_ok = false;
     int rc_fw = DM_OK, rc_bw = DM_OK, rc_sl = DM_OK;
     std::string err_fw, err_bw, err_sl;
+    std::vector<int32_t> zero32(N), one32(N), lnl32, var32, pp32, pl32, bl32;
+    std::vector<uint8_t> flags;
+    std::vector<int4> rec;
     {
-        std::thread t_fw([&] {
+        auto i32 = [](const int64_t *src, int64_t n) {
+            std::vector<int32_t> v(n);
+            for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)src[i];
+            return v;
+        };
+        std::vector<std::thread> th;
+        th.emplace_back([&] {
             rc_fw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
                                            true, fw);
             if (rc_fw) err_fw = dm_last_error();
         });
-        std::thread t_bw([&] {
+        th.emplace_back([&] {
             rc_bw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
                                            false, bw);
             if (rc_bw) err_bw = dm_last_error();
         });
-        rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
-        if (rc_sl) err_sl = dm_last_error();
-        relax_ok = max_width <= 8 && dm::build_relax_by_layer(bl, nb, lnl, desc->zero_t, desc->one_t, relax);
-        t_fw.join();
-        t_bw.join();
+        th.emplace_back([&] {
+            rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
+            if (rc_sl) err_sl = dm_last_error();
+        });
+        th.emplace_back([&] {
+            relax_ok = max_width <= 8 && dm::build_relax_by_layer(bl, nb, lnl, desc->zero_t, desc->one_t, relax);
+        });
+        const int nconv = 4;
+        for (int t = 0; t < nconv; ++t)
+            th.emplace_back([&, t] {
+                const int64_t lo = N * t / nconv, hi = N * (t + 1) / nconv;
+                for (int64_t i = lo; i < hi; ++i) {
+                    zero32[i] = (int32_t)desc->zero_t[i];
+                    one32[i] = (int32_t)desc->one_t[i];
+                }
+            });
+        th.emplace_back([&] {
+            bl32 = i32(bl, nb + 1);
+            lnl32 = i32(lnl, L + 1);
+            var32 = i32(desc->layer_var, L);
+            pp32 = i32(desc->proc_ptr, P + 1);
+            pl32 = i32(desc->proc_layers, L);
+        });
+        th.emplace_back([&] {
+                flags.assign(L, 0);
+                for (int64_t j = 0; j < nb; ++j) {
+                    flags[bl[j]] |= 1;
+                    flags[bl[j + 1] - 1] |= 2;
+                }
+                if (!want_np) return;
+                rec.resize((size_t)P * 8);
+                for (int64_t p = 0; p < P; ++p) {
+                    const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
+                    for (int c = 0; c < 8; ++c) {
+                        int4 r{-1, 0, (int)((unsigned)k << 24), 0};
+                        if (c < k) {
+                            const int64_t l = desc->proc_layers[lo + c];
+                            const int64_t w = lnl[l + 1] - lnl[l];
+                            const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
+                            r.x = (int)l;
+                            r.y = (int)lnl[l];
+                            r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) |
+                                        ((unsigned)k << 24));
+                        }
+                        rec[(size_t)p * 8 + c] = r;
+                    }
+                }
+            });
+        for (auto &t : th) t.join();
     }
     if (rc_fw) { dm::set_error(err_fw); return rc_fw; }
     if (rc_bw) { dm::set_error(err_bw); return rc_bw; }
@@ -1442,38 +1551,22 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     f->bw_depth = bw.depth;
     f->fw_tasks = fw.tasks;
     f->bw_tasks = bw.tasks;
-    auto i32 = [](const int64_t *src, int64_t n) {
-        std::vector<int32_t> v(n);
-        for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)src[i];
-        return v;
+    auto up = [&](int32_t **dst, const std::vector<int32_t> &v) {
+        return upload(f.get(), dst, v.data(), (int64_t)v.size(), s);
     };
-    std::vector<std::vector<int32_t>> keep;  // alive until the uploads finished
-    auto up = [&](int32_t **dst, std::vector<int32_t> v) {
-        keep.push_back(std::move(v));
-        return upload(f.get(), dst, keep.back().data(), (int64_t)keep.back().size(), s);
-    };
-    if ((rc = up(&f->bdd_layer_lo, i32(bl, nb + 1)))) return rc;
-    if ((rc = up(&f->lnl, i32(lnl, L + 1)))) return rc;
-    if ((rc = up(&f->layer_var, i32(desc->layer_var, L)))) return rc;
-    if ((rc = up(&f->zero_t, i32(desc->zero_t, N)))) return rc;
-    if ((rc = up(&f->one_t, i32(desc->one_t, N)))) return rc;
-    if ((rc = up(&f->proc_ptr, i32(desc->proc_ptr, P + 1)))) return rc;
-    if ((rc = up(&f->proc_layers, i32(desc->proc_layers, L)))) return rc;
-    if ((rc = up(&f->layer_bdd, std::move(layer_bdd)))) return rc;
-    if ((rc = up(&f->pos_var, std::move(pos_var)))) return rc;
-    if ((rc = up(&f->var_count, std::move(var_count)))) return rc;
-    if ((rc = up(&f->fw_task_level, fw.task_level))) return rc;
-    if ((rc = up(&f->bw_task_level, bw.task_level))) return rc;
-    if ((rc = up(&f->progress, std::vector<int32_t>{-1, 0}))) return rc;  // progress hint, task queue
-    f->fw_level = fw.task_level;
-    f->bw_level = bw.task_level;
-    f->fw_layer_h = fw.task_layer;
-    f->bw_layer_h = bw.task_layer;
-    if ((rc = up(&f->fw_layer, std::move(fw.task_layer)))) return rc;
-    if ((rc = up(&f->fw_meta, std::move(fw.task_meta)))) return rc;
-    if ((rc = up(&f->bw_layer, std::move(bw.task_layer)))) return rc;
-    if ((rc = up(&f->bw_meta, std::move(bw.task_meta)))) return rc;
-    if ((rc = up(&f->status, std::vector<int32_t>(1, 0)))) return rc;
+    if ((rc = up(&f->bdd_layer_lo, bl32))) return rc;
+    if ((rc = up(&f->lnl, lnl32))) return rc;
+    if ((rc = up(&f->layer_var, var32))) return rc;
+    if ((rc = up(&f->zero_t, zero32))) return rc;
+    if ((rc = up(&f->one_t, one32))) return rc;
+    if ((rc = up(&f->proc_ptr, pp32))) return rc;
+    if ((rc = up(&f->proc_layers, pl32))) return rc;
+    if ((rc = up(&f->layer_bdd, layer_bdd))) return rc;
+    if ((rc = up(&f->pos_var, pos_var))) return rc;
+    if ((rc = up(&f->var_count, var_count))) return rc;
+    const std::vector<int32_t> progress_init{-1, 0}, status_init{0};
+    if ((rc = up(&f->progress, progress_init))) return rc;  // progress hint, task queue
+    if ((rc = up(&f->status, status_init))) return rc;
     if (relax_ok) {
         if ((rc = upload(f.get(), &f->relax_layer, relax.data(), L, s))) return rc;
         f->relax_ok = true;
@@ -1481,14 +1574,13 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     {
         int32_t *gb, *gn, *pw, *zl, *ol;
         int64_t *gp, *ps;
-        if ((rc = up(&gb, std::move(sl.grp_bdd)))) return rc;
-        if ((rc = up(&gn, std::move(sl.grp_npos)))) return rc;
-        if ((rc = up(&pw, std::move(sl.pos_width)))) return rc;
-        if ((rc = up(&zl, std::move(sl.zl)))) return rc;
-        if ((rc = up(&ol, std::move(sl.ol)))) return rc;
+        if ((rc = up(&gb, sl.grp_bdd))) return rc;
+        if ((rc = up(&gn, sl.grp_npos))) return rc;
+        if ((rc = up(&pw, sl.pos_width))) return rc;
+        if ((rc = upload(f.get(), &zl, sl.zl.data(), (int64_t)sl.zl.size(), s))) return rc;
+        if ((rc = upload(f.get(), &ol, sl.ol.data(), (int64_t)sl.ol.size(), s))) return rc;
         if ((rc = upload(f.get(), &gp, sl.grp_pos_lo.data(), (int64_t)sl.grp_pos_lo.size(), s))) return rc;
         if ((rc = upload(f.get(), &ps, sl.pos_slot.data(), (int64_t)sl.pos_slot.size(), s))) return rc;
-        DM_CUDA(cudaStreamSynchronize(s));  // sl's int64 vectors die with this scope
         f->sweep.groups = sl.groups;
         f->sweep.max_width = (int32_t)sl.max_width;
         f->sweep.grp_bdd = gb;
@@ -1503,39 +1595,13 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     }
     f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
     f->mma_k = max_degree <= 8 ? 8 : 32;
-    if (f->mma_w == 8 && f->mma_k == 8) {
-        std::vector<uint8_t> flags(L, 0);
-        for (int64_t j = 0; j < nb; ++j) {
-            flags[bl[j]] |= 1;
-            flags[bl[j + 1] - 1] |= 2;
-        }
+    if (want_np) {
         if ((rc = upload(f.get(), &f->layer_flags, flags.data(), L, s))) return rc;
-        std::vector<int4> rec((size_t)P * 8);
-        for (int64_t p = 0; p < P; ++p) {
-            const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
-            for (int c = 0; c < 8; ++c) {
-                int4 r{-1, 0, (int)((unsigned)k << 24), 0};
-                if (c < k) {
-                    const int64_t l = desc->proc_layers[lo + c];
-                    const int64_t w = lnl[l + 1] - lnl[l];
-                    const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
-                    r.x = (int)l;
-                    r.y = (int)lnl[l];
-                    r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) | ((unsigned)k << 24));
-                }
-                rec[(size_t)p * 8 + c] = r;
-            }
-        }
         if ((rc = upload(f.get(), &f->np_rec, rec.data(), (int64_t)rec.size(), s))) return rc;
         if ((rc = up(&f->fw_pos, fw.pos_order))) return rc;
         if ((rc = up(&f->bw_pos, bw.pos_order))) return rc;
-        DM_CUDA(cudaStreamSynchronize(s));  // `flags`, `rec` die with this scope
         f->np_fw_tasks = (int64_t)fw.pos_order.size();
         f->np_bw_tasks = (int64_t)bw.pos_order.size();
-        f->fw_pos_level = std::move(fw.pos_order_level);
-        f->bw_pos_level = std::move(bw.pos_order_level);
-        f->fw_pos_h = std::move(fw.pos_order);
-        f->bw_pos_h = std::move(bw.pos_order);
         f->np_ok = true;
     }
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 3),
@@ -1546,7 +1612,17 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     DevPlan *dummy;
     if ((rc = get_plan(nb, &dummy))) return rc;
     if ((rc = get_plan(L, &dummy))) return rc;
-    DM_CUDA(cudaStreamSynchronize(s));
+    DM_CUDA(cudaStreamSynchronize(s));  // the host staging vectors die with this scope
+    // kept on the host: level order of the positions (profiling) and what the
+    // per-copy kernels' task packing needs if they are selected later
+    f->fw_pos_level = std::move(fw.pos_order_level);
+    f->bw_pos_level = std::move(bw.pos_order_level);
+    f->fw_pos_h = std::move(fw.pos_order);
+    f->bw_pos_h = std::move(bw.pos_order);
+    f->pp_h = std::move(pp32);
+    f->pl_h = std::move(pl32);
+    f->flags_h = std::move(flags);
+    if (!f->mma_np && (rc = ensure_per_copy_schedules(f.get(), s))) return rc;
     if (env_int("DM_VERBOSE", 0))
         std::fprintf(stderr, "[dm_flat_create] validate %.3fs, plans %.3fs, upload %.3fs\n", t_valid - t_begin,
                      t_plans - t_valid, host_seconds() - t_plans);
@@ -1583,7 +1659,9 @@ int dm_flat_set_mma_config(dm_flat *f, int threads, int blocks_per_sm, int sleep
         dm::set_error("null flat handle");
         return DM_ERR_INVALID;
     }
-    return configure_mma(f, threads, blocks_per_sm, (unsigned)std::max(0, sleep_ns), probe, lookahead);
+    int rc = configure_mma(f, threads, blocks_per_sm, (unsigned)std::max(0, sleep_ns), probe, lookahead);
+    if (rc == DM_OK && !f->mma_np) rc = ensure_per_copy_schedules(f, 0);
+    return rc;
 }
 
 int dm_flat_set_trace(dm_flat *f, unsigned long long *trace) {
@@ -1679,6 +1757,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     }
     int rc = check_stream_error("mma fill");
     if (rc) return rc;
+    if (!f->mma_np && (rc = ensure_per_copy_schedules(const_cast<dm_flat *>(f), s))) return rc;
     MmaArgs args;
     args.ntasks = forward ? f->fw_tasks : f->bw_tasks;
     args.task_layer = forward ? f->fw_layer : f->bw_layer;

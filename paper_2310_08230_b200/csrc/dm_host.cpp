@@ -356,39 +356,50 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
         s.pos_order[i] = (int32_t)bylevel[i];
         s.pos_order_level[i] = pos_level[bylevel[i]];
     }
+    s.depth = depth;
     s.task_layer.clear();
     s.task_meta.clear();
-    s.depth = depth;
+    s.task_level.clear();
+    s.tasks = 0;
+    return DM_OK;
+}
+
+// Per-copy warp tasks (the fallback kernels): same-level positions packed
+// into 32-lane tasks, copies of a position adjacent in copy order.
+void pack_mma_tasks(const std::vector<int32_t> &pos_order, const std::vector<int32_t> &pos_order_level,
+                    const int32_t *proc_ptr, const int32_t *proc_layers, const uint8_t *layer_flags,
+                    MmaSchedule &s) {
+    s.task_layer.clear();
+    s.task_meta.clear();
+    s.task_level.clear();
     int used = 32;  // lanes used in the open task (32 = none open)
     int32_t open_level = -1;
-    s.task_level.clear();
     auto open_task = [&]() {
         s.task_layer.insert(s.task_layer.end(), 32, -1);
         s.task_meta.insert(s.task_meta.end(), 32, 0);
         used = 0;
     };
-    for (int64_t i = 0; i < (int64_t)bylevel.size(); ++i) {
-        const int64_t p = bylevel[i];
+    for (size_t i = 0; i < pos_order.size(); ++i) {
+        const int64_t p = pos_order[i];
         const int64_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
         const int c = (int)(hi - lo);
-        if (pos_level[p] != open_level || used + c > 32) {
+        if (pos_order_level[i] != open_level || used + c > 32) {
             open_task();
-            open_level = pos_level[p];
+            open_level = pos_order_level[i];
             s.task_level.push_back(open_level);
         }
         const size_t base = s.task_layer.size() - 32;
         for (int k = 0; k < c; ++k) {
             const int64_t l = proc_layers[lo + k];
             int32_t meta = used | (c << 8);
-            if (layer_level[l] & kFirstFlag) meta |= 1 << 16;
-            if (layer_level[l] & kLastFlag) meta |= 1 << 17;
+            if (layer_flags[l] & 1) meta |= 1 << 16;
+            if (layer_flags[l] & 2) meta |= 1 << 17;
             s.task_layer[base + used + k] = (int32_t)l;
             s.task_meta[base + used + k] = meta;
         }
         used += c;
     }
     s.tasks = (int64_t)s.task_layer.size() / 32;
-    return DM_OK;
 }
 
 }  // namespace dm
@@ -639,6 +650,17 @@ int dm_debug_emulate_mma(const dm_flat_desc *d, int forward, double *lam, double
     int rc = dm::build_mma_schedule(d->bdd_layer_lo, nb, nullptr, d->layer_var, L, d->proc_ptr,
                                     d->proc_layers, P, forward != 0, s);
     if (rc != DM_OK) return rc;
+    {
+        std::vector<uint8_t> flags(L, 0);
+        for (int64_t j = 0; j < nb; ++j) {
+            flags[d->bdd_layer_lo[j]] |= 1;
+            flags[d->bdd_layer_lo[j + 1] - 1] |= 2;
+        }
+        std::vector<int32_t> pp(P + 1), pl(L);
+        for (int64_t p = 0; p <= P; ++p) pp[p] = (int32_t)d->proc_ptr[p];
+        for (int64_t l = 0; l < L; ++l) pl[l] = (int32_t)d->proc_layers[l];
+        dm::pack_mma_tasks(s.pos_order, s.pos_order_level, pp.data(), pl.data(), flags.data(), s);
+    }
     if (depth_out) *depth_out = s.depth;
     std::vector<int64_t> layer_bdd(L);
     for (int64_t j = 0; j < nb; ++j)

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/discomatch_b200.h"
@@ -69,6 +70,25 @@ struct MmaSchedule {
 int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_bdd_or_null,
                        const int64_t *layer_var, int64_t L, const int64_t *proc_ptr,
                        const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &out);
+void pack_mma_tasks(const std::vector<int32_t> &pos_order, const std::vector<int32_t> &pos_order_level,
+                    const int32_t *proc_ptr, const int32_t *proc_layers, const uint8_t *layer_flags,
+                    MmaSchedule &s);
+
+// Uninitialised int32 buffer (every element of the sweep targets is written
+// by the parallel fill, so a value-initialising std::vector would only add a
+// serial pass over hundreds of MB).
+struct I32Buffer {
+    std::unique_ptr<int32_t[]> p;
+    size_t n = 0;
+    void resize(size_t m) {
+        p.reset(new int32_t[m]);
+        n = m;
+    }
+    int32_t *data() { return p.get(); }
+    const int32_t *data() const { return p.get(); }
+    size_t size() const { return n; }
+    int32_t &operator[](size_t i) { return p[i]; }
+};
 
 // Interleaved sweep layout (dm_layout.cpp): 32 diagrams per warp group,
 // layers aligned at the last layer (position 0), node slots interleaved by
@@ -80,7 +100,7 @@ struct SweepLayout {
     std::vector<int64_t> grp_pos_lo;  // [groups+1] into pos_width / pos_slot
     std::vector<int32_t> pos_width;   // widest layer at each position of each group
     std::vector<int64_t> pos_slot;    // first node slot of each position
-    std::vector<int32_t> zl, ol;      // [slots*32] local targets, -1 FALSE, -2 TRUE
+    I32Buffer zl, ol;                 // [slots*32] local targets, -1 FALSE, -2 TRUE
 };
 int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *layer_node_lo,
                        const int64_t *zero_t, const int64_t *one_t, SweepLayout &out);

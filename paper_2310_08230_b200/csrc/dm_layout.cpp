@@ -15,6 +15,7 @@
 // to FALSE and never feed a real node.
 #include <algorithm>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "dm_internal.h"
@@ -23,53 +24,78 @@ namespace dm {
 
 int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *lnl, const int64_t *zero_t,
                        const int64_t *one_t, SweepLayout &s) {
-    std::vector<int64_t> order(nb);
-    std::iota(order.begin(), order.end(), 0);
     auto nlay = [&](int64_t j) { return bdd_layer_lo[j + 1] - bdd_layer_lo[j]; };
-    auto nnod = [&](int64_t j) { return lnl[bdd_layer_lo[j + 1]] - lnl[bdd_layer_lo[j]]; };
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        if (nlay(a) != nlay(b)) return nlay(a) > nlay(b);
-        return nnod(a) > nnod(b);
+    constexpr int kThreads = 8;
+    auto par = [&](int64_t n, auto &&fn) {  // fn(lo, hi) over kThreads contiguous ranges
+        std::vector<std::thread> th;
+        for (int t = 0; t < kThreads; ++t)
+            th.emplace_back([&, t] { fn(n * t / kThreads, n * (t + 1) / kThreads); });
+        for (auto &x : th) x.join();
+    };
+    // shape order: more layers first, then more nodes, then diagram id
+    std::vector<std::pair<uint64_t, int64_t>> key(nb);
+    par(nb, [&](int64_t lo, int64_t hi) {
+        for (int64_t j = lo; j < hi; ++j) {
+            const uint64_t L = (uint64_t)nlay(j), Nn = (uint64_t)(lnl[bdd_layer_lo[j + 1]] - lnl[bdd_layer_lo[j]]);
+            key[j] = {(~L << 32) | (~Nn & 0xffffffffull), j};
+        }
     });
+    std::sort(key.begin(), key.end());
     s.groups = (nb + 31) / 32;
     s.grp_bdd.assign(s.groups * 32, -1);
     s.grp_npos.assign(s.groups, 0);
     s.grp_pos_lo.assign(s.groups + 1, 0);
-    s.pos_width.clear();
-    s.pos_slot.clear();
-    s.max_width = 0;
-    int64_t slots = 0;
     for (int64_t g = 0; g < s.groups; ++g) {
         int64_t K = 0;
         for (int t = 0; t < 32 && g * 32 + t < nb; ++t) {
-            const int64_t j = order[g * 32 + t];
+            const int64_t j = key[g * 32 + t].second;
             s.grp_bdd[g * 32 + t] = (int32_t)j;
             K = std::max(K, nlay(j));
         }
         s.grp_npos[g] = (int32_t)K;
-        for (int64_t k = 0; k < K; ++k) {
-            int64_t w = 0;
+        s.grp_pos_lo[g + 1] = s.grp_pos_lo[g] + K;
+    }
+    const int64_t npos_total = s.grp_pos_lo[s.groups];
+    s.pos_width.assign(npos_total, 0);
+    par(s.groups, [&](int64_t glo, int64_t ghi) {
+        for (int64_t g = glo; g < ghi; ++g)
             for (int t = 0; t < 32; ++t) {
                 const int32_t j = s.grp_bdd[g * 32 + t];
-                if (j < 0 || k >= nlay(j)) continue;
-                const int64_t l = bdd_layer_lo[j + 1] - 1 - k;
-                w = std::max(w, lnl[l + 1] - lnl[l]);
+                if (j < 0) continue;
+                for (int64_t k = 0; k < nlay(j); ++k) {
+                    const int64_t l = bdd_layer_lo[j + 1] - 1 - k;
+                    int32_t &w = s.pos_width[s.grp_pos_lo[g] + k];
+                    w = std::max<int32_t>(w, (int32_t)(lnl[l + 1] - lnl[l]));
+                }
             }
-            s.pos_width.push_back((int32_t)w);
-            s.pos_slot.push_back(slots);
-            slots += w;
-            s.max_width = std::max<int64_t>(s.max_width, w);
-        }
-        s.grp_pos_lo[g + 1] = (int64_t)s.pos_width.size();
+    });
+    s.pos_slot.assign(npos_total, 0);
+    s.max_width = 0;
+    int64_t slots = 0;
+    for (int64_t q = 0; q < npos_total; ++q) {
+        s.pos_slot[q] = slots;
+        slots += s.pos_width[q];
+        s.max_width = std::max<int64_t>(s.max_width, s.pos_width[q]);
     }
     if (slots * 32 >= INT32_MAX) {
         set_error("sweep layout exceeds the int32 element range");
         return DM_ERR_UNSUPPORTED;
     }
     s.slots = slots;
-    s.zl.assign(slots * 32, kFalse);
-    s.ol.assign(slots * 32, kFalse);
-    for (int64_t g = 0; g < s.groups; ++g) {
+    s.zl.resize(slots * 32);
+    s.ol.resize(slots * 32);
+    // groups own disjoint slot ranges: fill them in parallel
+    std::vector<std::thread> th;
+    for (int th_i = 0; th_i < kThreads; ++th_i)
+        th.emplace_back([&, th_i] {
+    const int64_t glo = s.groups * th_i / kThreads, ghi = s.groups * (th_i + 1) / kThreads;
+    if (glo < ghi) {
+        const int64_t slo = s.pos_slot[s.grp_pos_lo[glo]] * 32;
+        const int64_t shi = (ghi == s.groups ? slots : s.pos_slot[s.grp_pos_lo[ghi]]) * 32;
+        std::fill(s.zl.data() + slo, s.zl.data() + shi, kFalse);
+        std::fill(s.ol.data() + slo, s.ol.data() + shi, kFalse);
+    }
+    for (int64_t g = glo; g < ghi; ++g) {
         const int64_t p0 = s.grp_pos_lo[g];
         for (int t = 0; t < 32; ++t) {
             const int32_t j = s.grp_bdd[g * 32 + t];
@@ -86,6 +112,8 @@ int build_sweep_layout(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
             }
         }
     }
+        });
+    for (auto &t : th) t.join();
     return DM_OK;
 }
 
