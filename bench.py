@@ -241,9 +241,12 @@ def _traffic(kernel):
             tr = json.load(f)
     except (OSError, ValueError):
         return None
-    for name, b in tr.items():
-        if name.startswith(kernel + "_kernel") or name.startswith(kernel + "<") or name == kernel:
-            return b
+    # the exact passes run their node-parallel instantiation when the instance allows it
+    cands = [kernel.replace("mma_", "mma_np_"), kernel] if kernel.startswith("mma_") else [kernel]
+    for cand in cands:
+        for name, b in tr.items():
+            if name.startswith(cand + "_kernel") or name.startswith(cand + "<") or name == cand:
+                return b
     return None
 
 

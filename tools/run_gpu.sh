@@ -18,7 +18,7 @@ for step in "$@"; do
     ncu_full)
       B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
       timeout 900 $B > gpurun_out/plain.log 2>&1 && \
-      for k in mma_forward mma_backward sweep_backward chunk_step_kernel k_argmin; do
+      for k in mma_np_forward mma_np_backward sweep_backward chunk_step_kernel k_argmin; do
         timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
             -o gpurun_out/full_$k $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full $k rc=$?" >> gpurun_out/ncu_full.log
       done ;;
