@@ -160,6 +160,12 @@ int dm_k_min_marginals(const dm_flat *f, const double *lam, const double *F, con
                        double *m0, double *m1, void *stream);
 /* kernels.py:401-431 */
 int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bits, void *stream);
+/* The argmin walk (dm_k_argmin) from the per-node decisions the last exact
+ * backward pass recorded when it ran the node-parallel kernels — valid only
+ * while lam and B are exactly what that pass left (the caller tracks this;
+ * DualState does via its distance-table generation).  B must be the table that
+ * pass wrote; DM_ERR_INVALID otherwise.  Bit-identical to dm_k_argmin there. */
+int dm_k_argmin_from_pass(const dm_flat *flat, const double *B, double *bits, void *stream);
 
 /* --- vectors over dual coordinates / variables ----------------------------- */
 /* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */

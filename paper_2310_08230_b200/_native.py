@@ -68,6 +68,7 @@ SIGNATURES = {
     "dm_k_mma_backward": ([_P, _P, _P, _P, _P, _P], _INT),
     "dm_k_min_marginals": ([_P, _P, _P, _P, _P, _P, _P], _INT),
     "dm_k_argmin": ([_P, _P, _P, _P, _P], _INT),
+    "dm_k_argmin_from_pass": ([_P, _P, _P, _P], _INT),
     "dm_init_duals": ([_P, _P, _P, _P], _INT),
     "dm_project_direction": ([_P, _P, _P, _P], _INT),
     "dm_lambda_sums": ([_P, _P, _P, _P], _INT),
@@ -128,7 +129,7 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_k_mma_backward", "dm_k_min_marginals", "dm_k_argmin", "dm_init_duals",
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
-                  "dm_lbfgs_direction"}
+                  "dm_lbfgs_direction", "dm_k_argmin_from_pass"}
 launch_count = 0
 
 

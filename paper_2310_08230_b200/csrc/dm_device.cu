@@ -168,6 +168,22 @@ __global__ void k_argmin_kernel(int32_t nb, const int32_t *__restrict__ bdd_laye
     }
 }
 
+// The same walk from the decisions the node-parallel backward pass recorded:
+// one dependent load per layer instead of two.
+__global__ void k_argmin_walk_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
+                                     const int32_t *__restrict__ lnl, const int32_t *__restrict__ dec,
+                                     double *__restrict__ bits) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nb) return;
+    int32_t v = lnl[bdd_layer_lo[j]];
+    for (int32_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
+        const int32_t code = dec[v];
+        bits[l] = (double)(code & 1);
+        const int32_t nxt = (code >> 1) - 2;
+        if (nxt >= 0) v = nxt;
+    }
+}
+
 // --------------------------------------------------------------------------
 // per-variable kernels (thread per visitation position)
 // --------------------------------------------------------------------------
@@ -380,6 +396,7 @@ struct MmaArgs {
     // per position p, 8 copy records {layer, first node, w | wn<<8 | flags<<16 | k<<24, 0}
     const int4 *np_rec;
     int *task_counter;  // dynamic task queue of the node-parallel kernels
+    int32_t *dec;       // node-parallel backward: per node ((chosen target + 2) << 1) | bit
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -1051,6 +1068,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         // per node: next-layer slot of each arc (8 = terminal/padding: -0.0),
         // marginal bases and rebuild offsets as in mma_backward_kernel
         int iz[2] = {8, 8}, io[2] = {8, 8};
+        int32_t zt[2] = {dm::kFalse, dm::kFalse}, ot[2] = {dm::kFalse, dm::kFalse};
         double f0b[2] = {DM_INF, DM_INF}, f1b[2] = {DM_INF, DM_INF}, rz[2] = {DM_INF, DM_INF},
                ro[2] = {DM_INF, DM_INF};
 #pragma unroll
@@ -1059,6 +1077,8 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
             if (r.act && i < r.w) {
                 const int32_t z = a.zero_t[r.nlo + i], o = a.one_t[r.nlo + i];
                 const double fv = a.F[r.nlo + i];
+                zt[j] = z;
+                ot[j] = o;
                 iz[j] = z >= 0 ? ((z - n0n) & 7) : 8;
                 io[j] = o >= 0 ? ((o - n0n) & 7) : 8;
                 f0b[j] = z == dm::kFalse ? DM_INF : fv;
@@ -1112,8 +1132,12 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
             if (r.act && i < r.w) {
                 const double cz = __dadd_rn(rz[j], tz[j]);
                 const double co = __dadd_rn(__dadd_rn(lam_l, to[j]), ro[j]);
-                const double bv = (cz <= co) ? cz : co;
+                const bool zero_wins = cz <= co;
+                const double bv = zero_wins ? cz : co;
                 st_relaxed(a.B + r.nlo + i, bv);
+                // the argmin walk's decision at this node (kernels.py:402-431 on
+                // the final duals and distances: same operands, same compare)
+                if (a.dec) a.dec[r.nlo + i] = (((zero_wins ? zt[j] : ot[j]) + 2) << 1) | (zero_wins ? 0 : 1);
                 if (i == 0 && r.first) a.bounds[a.layer_bdd[r.l]] = bv;  // kernels.py:359-361
             }
         }
@@ -1156,6 +1180,8 @@ struct dm_flat {
     int32_t *fw_pos = nullptr, *bw_pos = nullptr;
     uint8_t *layer_flags = nullptr;
     int4 *np_rec = nullptr;
+    int32_t *dec = nullptr;          // decisions of the last node-parallel backward pass
+    const double *dec_B = nullptr;   // ... and the distance table it wrote (nullptr: none)
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
     std::vector<int32_t> fw_pos_level, bw_pos_level, fw_pos_h, bw_pos_h;  // host copies (profiling)
     int mma_w = 8, mma_k = 8;
@@ -1784,6 +1810,19 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.proc_layers = f->proc_layers;
     args.layer_flags = f->layer_flags;
     args.np_rec = f->np_rec;
+    args.dec = nullptr;
+    if (f->mma_np && !forward) {
+        dm_flat *m = const_cast<dm_flat *>(f);
+        if (!m->dec) {
+            DM_CUDA(cudaMalloc((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t)));
+            m->allocs.push_back(m->dec);
+            m->bytes += (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t);
+        }
+        args.dec = m->dec;
+        m->dec_B = B;
+    } else if (!forward) {
+        const_cast<dm_flat *>(f)->dec_B = nullptr;
+    }
     args.task_counter = f->progress + 1;
     if (f->mma_np) {
         args.ntasks = forward ? f->np_fw_tasks : f->np_bw_tasks;
@@ -1821,6 +1860,18 @@ int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bi
     k_argmin_kernel<<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
         (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, lam, B, bits);
     return check_stream_error("k_argmin");
+}
+
+int dm_k_argmin_from_pass(const dm_flat *f, const double *B, double *bits, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (f->nb == 0) return DM_OK;
+    if (!f->dec || f->dec_B != B || !B) {
+        dm::set_error("dm_k_argmin_from_pass: no node-parallel backward pass wrote this distance table");
+        return DM_ERR_INVALID;
+    }
+    k_argmin_walk_kernel<<<blocks_for(f->nb, 128), 128, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->nb, f->bdd_layer_lo, f->lnl, f->dec, bits);
+    return check_stream_error("k_argmin_walk");
 }
 
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {

@@ -80,6 +80,7 @@ class DualState:
         self.pass_timer: KernelTimer | None = None
         self._bgen = 0  # generation of the distance-to-TRUE table B
         self._argmin_cache = None
+        self._dec_gen = -1  # B generation whose argmin decisions the last backward pass recorded
         free = instance.unconstrained_variables()
         self.free_values = {int(v): (0 if instance.costs[v] >= 0 else 1) for v in free}
         self.free_contribution = float(np.minimum(instance.costs[free], 0.0).sum()) if len(free) else 0.0
@@ -225,6 +226,8 @@ def mma_pass(state: DualState, direction: str) -> DualState:
         if ev:
             timer.end(ev)
         state._bgen += 1
+        if state.dev.records_decisions:
+            state._dec_gen = state._bgen
         state.b_valid = True
         state.f_valid = False
     else:
@@ -247,7 +250,10 @@ def subgradient_device(state: DualState) -> torch.Tensor:
     if cached is not None and cached[0] == state._bgen:
         return cached[1]
     bits = torch.empty(state.flat.num_layers, dtype=_F64, device=state.device)
-    state.dev.k_argmin(state.lam_d, state.B, bits)
+    if state._dec_gen == state._bgen:
+        state.dev.k_argmin_from_pass(state.B, bits)  # decisions of the pass that wrote B
+    else:
+        state.dev.k_argmin(state.lam_d, state.B, bits)
     state._argmin_cache = (state._bgen, bits)
     return bits
 

@@ -120,6 +120,15 @@ class DeviceFlat:
     def k_argmin(self, lam, B, bits):
         _native.call("dm_k_argmin", self._h, _ptr(lam), _ptr(B), _ptr(bits), self._s())
 
+    def k_argmin_from_pass(self, B, bits):
+        """Argmin walk from the decisions of the last node-parallel backward pass."""
+        _native.call("dm_k_argmin_from_pass", self._h, _ptr(B), _ptr(bits), self._s())
+
+    @property
+    def records_decisions(self) -> bool:
+        """Whether the exact backward pass records argmin decisions (node-parallel kernels)."""
+        return int(self.info.get("lanes_per_task", 32)) == 8
+
     # --- per-variable vectors ------------------------------------------------
     def init_duals(self, costs_by_var, lam):
         _native.call("dm_init_duals", self._h, _ptr(costs_by_var), _ptr(lam), self._s())

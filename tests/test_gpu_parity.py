@@ -69,6 +69,24 @@ def test_exact_passes_match_reference(case, kernels):
 
 
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_argmin_from_backward_pass_decisions(case):
+    inst = product_instance(case)
+    st = init_duals(inst)
+    for _ in range(2):
+        mma_pass(st, FORWARD)
+        mma_pass(st, BACKWARD)
+        walk = torch.empty(st.flat.num_layers, dtype=torch.float64, device=st.device)
+        st.dev.k_argmin(st.lam_d, st.B, walk)
+        if st.dev.records_decisions:
+            rec = torch.empty_like(walk)
+            st.dev.k_argmin_from_pass(st.B, rec)
+            assert rec.cpu().numpy().tobytes() == walk.cpu().numpy().tobytes()
+        assert subgradient(st).tobytes() == walk.cpu().numpy().tobytes()
+    with pytest.raises(ValueError):  # a table no backward pass wrote
+        st.dev.k_argmin_from_pass(st.F, torch.empty_like(st.lam_d))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
 def test_mma_only_solve_matches_reference(case):
     inst = product_instance(case)
     g = case["mma-only"]
