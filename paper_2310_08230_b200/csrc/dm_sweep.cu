@@ -375,10 +375,29 @@ struct FinishPlans {
 // element pair (2p, 2p+1) of row i of leaf o, as a double2 index
 __device__ __forceinline__ int pair_index(int i) { return (threadIdx.x >> 2) * 64 + (threadIdx.x & 3) + 4 * i; }
 
+// Programmatic dependent launch inside the two-loop: a step's blocks start
+// while the previous step's finishing block runs, pull their (constant)
+// history vectors into L2, and only then wait for the previous grid.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int kMode>
 __global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, double *__restrict__ partial) {
-    const StepCoef c = step_coef<kMode>(a);
+    pdl_launch_dependents();
     const int64_t off = (int64_t)blockIdx.x * kChunk;
+    {
+        // 32 KB per vector and block: two 128-byte lines per thread
+        const char *pu = reinterpret_cast<const char *>((kMode == kDot ? a.x : a.u) + off);
+        const char *pv = reinterpret_cast<const char *>((a.v ? a.v : a.x) + off);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int line = (threadIdx.x + k * kChunkThreads) * 128;
+            if (kMode != kDot) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + line));
+            if (a.v) asm volatile("prefetch.global.L2 [%0];" ::"l"(pv + line));
+        }
+    }
+    pdl_wait();  // the previous step's x and scalars are complete from here
+    const StepCoef c = step_coef<kMode>(a);
     double2 *x2 = reinterpret_cast<double2 *>(a.x + off);
     const double2 *u2 = reinterpret_cast<const double2 *>((kMode == kDot ? a.x : a.u) + off);
     const double2 *v2 = reinterpret_cast<const double2 *>((a.v ? a.v : a.x) + off);
@@ -431,6 +450,8 @@ __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep 
                                                                       double *__restrict__ partial,
                                                                       const __grid_constant__ FinishPlans plans) {
     __shared__ double buf[kChunk];
+    pdl_launch_dependents();
+    pdl_wait();
     const StepCoef c = step_coef<kMode>(a);
     if ((kMode == kFirst || kMode == kScale) && threadIdx.x == 0 && a.alpha_out) a.alpha_out[0] = c.coef;
     const bool dot = a.v != nullptr;
@@ -480,17 +501,36 @@ __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep 
 
 inline bool aligned16(const void *p) { return p == nullptr || ((uintptr_t)p & 15) == 0; }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, bool pdl,
+                             Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// `pdl`: the previous launch on the stream is one of these kernels, which
+// never write the step's u / v vectors, so they may be read before the wait.
 template <int kMode>
-cudaError_t chunk_step(const ChunkStep &a, int64_t n, double *partial, cudaStream_t st) {
+cudaError_t chunk_step(const ChunkStep &a, int64_t n, double *partial, cudaStream_t st, bool pdl = false) {
     const bool vec = aligned16(a.x) && aligned16(a.u) && aligned16(a.v);
     const int64_t full = vec ? n / kChunk : 0;
-    if (full > 0) chunk_step_kernel<kMode><<<(unsigned)full, kChunkThreads, 0, st>>>(a, partial);
+    cudaError_t e;
+    if (full > 0 &&
+        (e = launch_maybe_pdl(chunk_step_kernel<kMode>, (unsigned)full, kChunkThreads, st, pdl, a, partial)))
+        return e;
     FinishPlans plans;
     plans.chunk = make_sum_plan(kChunk);
     plans.tail = make_sum_plan((int)(n % kChunk));
     plans.totals = make_sum_plan((int)((n + kChunk - 1) / kChunk));
-    chunk_finish_kernel<kMode><<<1, kFinishThreads, 0, st>>>(a, n, full, partial, plans);
-    return cudaGetLastError();
+    return launch_maybe_pdl(chunk_finish_kernel<kMode>, 1, kFinishThreads, st, true, a, n, full, partial, plans);
 }
 
 }  // namespace
@@ -511,7 +551,7 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
     a.u = g;
     a.v = s[0];
     a.dot_out = dot1;
-    if ((e = chunk_step<kCopy>(a, n, partial, st))) return fail(e, "two_loop copy");
+    if ((e = chunk_step<kCopy>(a, n, partial, st, true))) return fail(e, "two_loop copy");
     for (int i = 0; i < m; ++i) {
         a = ChunkStep{};
         a.x = d;
@@ -522,13 +562,13 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
         if (i + 1 < m) {
             a.v = s[i + 1];
             a.dot_out = dot1 + i + 1;
-            e = chunk_step<kFirst>(a, n, partial, st);
+            e = chunk_step<kFirst>(a, n, partial, st, true);
         } else {  // last step of the first loop carries the scaling and starts the second loop
             a.sy0 = sy[0];
             a.yy = yy;
             a.v = y[m - 1];
             a.dot_out = dot2;
-            e = chunk_step<kScale>(a, n, partial, st);
+            e = chunk_step<kScale>(a, n, partial, st, true);
         }
         if (e) return fail(e, "two_loop first");
     }
@@ -544,7 +584,7 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
             a.v = y[i - 1];
             a.dot_out = dot2 + k + 1;
         }
-        if ((e = chunk_step<kSecond>(a, n, partial, st))) return fail(e, "two_loop second");
+        if ((e = chunk_step<kSecond>(a, n, partial, st, true))) return fail(e, "two_loop second");
     }
     return DM_OK;
 }
