@@ -12,8 +12,6 @@
 // order with strict <.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include <string>
 #include <vector>
 
@@ -252,11 +250,6 @@ int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bound
 namespace {
 
 constexpr int kChunk = 4096;
-
-bool env_flag(const char *name, bool dflt) {
-    const char *v = std::getenv(name);
-    return v ? std::atoi(v) != 0 : dflt;
-}
 constexpr int kChunkThreads = 128;
 constexpr int kFinishThreads = 1024;
 
@@ -552,39 +545,6 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
     // slots: [0, m) first-loop dots, [m, 2m) alphas, 2m = y0.y0, [2m+1, 3m+1) second-loop dots
     double *dot1 = slots, *alpha = slots + m, *yy = slots + 2 * m, *dot2 = slots + 2 * m + 1;
     if (int rc = dm::chunk_dot(y[0], y[0], n, partial, yy, stream)) return rc;
-    // d is read and written by every step while each history vector is read
-    // once: keep d in the persisting part of L2 for the recursion
-    const size_t dbytes = (size_t)n * sizeof(double);
-    bool window = false;
-    {
-        int dev = 0, maxp = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess && maxp > 0 &&
-            env_flag("DM_LBFGS_L2_WINDOW", true)) {
-            size_t lim = 0;
-            cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize);
-            if (lim < (size_t)maxp) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
-            cudaStreamAttrValue v = {};
-            v.accessPolicyWindow.base_ptr = d;
-            v.accessPolicyWindow.num_bytes = dbytes;
-            v.accessPolicyWindow.hitRatio = dbytes <= (size_t)maxp ? 1.0f : (float)maxp / (float)dbytes;
-            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            window = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
-        }
-        cudaGetLastError();  // an unsupported policy is not an error
-    }
-    struct WindowReset {
-        cudaStream_t st;
-        bool on;
-        ~WindowReset() {
-            if (!on) return;
-            cudaStreamAttrValue v = {};
-            v.accessPolicyWindow.num_bytes = 0;
-            cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
-            cudaGetLastError();
-        }
-    } reset{st, window};
     cudaError_t e;
     ChunkStep a{};
     a.x = d;

@@ -43,7 +43,6 @@ res = {
     "copy_us": timed(lambda: g.copy_(a)),
     "two_loop_fused_us": timed(lambda: qn.lbfgs_direction(g, h), 5),
     "two_loop_plain_us": timed(lambda: qn.lbfgs_direction(g, h, fused=False), 5),
-    "two_loop_fused_again_us": timed(lambda: qn.lbfgs_direction(g, h), 5),
 }
 res["dot_gbs"] = 16 * n / res["dot_us"] / 1e3
 res["sub_gbs"] = 24 * n / res["sub_us"] / 1e3
