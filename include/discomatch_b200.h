@@ -84,6 +84,18 @@ int dm_instance_export(const dm_instance *inst, double *costs, int64_t *variable
                        int64_t *layer_bdd, int64_t *zero_t, int64_t *one_t, int64_t *proc_ptr,
                        int64_t *proc_layers, int64_t *constraint_counts);
 void dm_instance_free(dm_instance *inst);
+/* Conditioning for the primal side (reference bdd.py:243-264 Bdd.condition,
+ * bdd.py:278-334 reduce_bdd, primal.py:114-175 fix_and_reduce): every diagram
+ * of the flat table (FlatBdds arrays, global node ids) that touches a fixed
+ * variable (fixed[v] = 0/1, -1 free) is clamped and re-reduced; diagrams left
+ * as a single chain accepting every fix-consistent assignment are dropped
+ * (count in *dropped_out); the rest become a new instance with the same
+ * costs and variable order, unsplit.  DM_ERR_INFEASIBLE when a diagram
+ * empties (the reference raises InfeasibleAfterFixing). */
+int dm_condition_flat(int64_t num_variables, const double *costs, const int64_t *variable_order,
+                      int64_t num_bdds, const int64_t *bdd_layer_lo, const int64_t *layer_var,
+                      const int64_t *layer_node_lo, const int64_t *zero_t, const int64_t *one_t,
+                      const int8_t *fixed, int64_t *dropped_out, dm_instance **out);
 
 /* ------------------------------------------------------------------------
  * Device-resident flat table (FlatBdds on the GPU) + exact-pass schedules.

@@ -13,6 +13,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "dm_internal.h"
@@ -548,6 +549,135 @@ int dm_instance_from_bdds(int64_t num_variables, const double *costs, const int6
     else
         std::iota(order.begin(), order.end(), 0);
     return split_and_flatten(bdds, std::move(cst), std::move(order), chunk_size, out);
+}
+
+// Conditioning for the primal side (bdd.py:243-264 Bdd.condition +
+// reduce_bdd bdd.py:278-334, primal.py:114-175 fix_and_reduce): clamp the
+// fixed variables of every touched diagram, re-reduce it (prune dead arcs
+// bottom-up, drop unreachable nodes, merge isomorphic nodes keeping
+// first-occurrence order), drop diagrams that became a single chain
+// accepting every fix-consistent assignment, and lower what remains as a new
+// instance (same costs and variable order, no splitting).
+namespace {
+
+// local arcs: >= 0 next-layer node, FALSE (-1), TRUE (-2); returns false when emptied
+bool reduce_local(std::vector<std::vector<int32_t>> &zs, std::vector<std::vector<int32_t>> &os) {
+    const size_t n = zs.size();
+    std::vector<std::vector<char>> alive(n);
+    for (size_t l = n; l-- > 0;) {
+        for (auto *arcs : {&zs[l], &os[l]})
+            if (l + 1 < n)
+                for (auto &t : *arcs)
+                    if (t >= 0 && !alive[l + 1][t]) t = dm::kFalse;
+        alive[l].resize(zs[l].size());
+        for (size_t i = 0; i < zs[l].size(); ++i) alive[l][i] = zs[l][i] != dm::kFalse || os[l][i] != dm::kFalse;
+    }
+    if (!alive[0][0]) return false;
+    std::vector<std::vector<char>> reach(n);
+    reach[0].assign(1, 1);
+    for (size_t l = 0; l + 1 < n; ++l) {
+        reach[l + 1].assign(zs[l + 1].size(), 0);
+        for (auto *arcs : {&zs[l], &os[l]})
+            for (size_t i = 0; i < arcs->size(); ++i)
+                if (reach[l][i] && (*arcs)[i] >= 0) reach[l + 1][(*arcs)[i]] = 1;
+    }
+    std::vector<int64_t> remap;  // old id in layer l+1 -> new id (or FALSE)
+    for (size_t l = n; l-- > 0;) {
+        const size_t w = zs[l].size();
+        std::vector<int32_t> nz, no;
+        std::vector<int64_t> rm(w, dm::kFalse);
+        // merge key exactly as reduce_bdd forms it: (z + 2) * (width of THIS
+        // layer + 3) + (o + 2), first occurrence wins
+        std::map<int64_t, int32_t> first;
+        for (size_t i = 0; i < w; ++i) {
+            if (!(alive[l][i] && reach[l][i])) continue;
+            int32_t z = zs[l][i], o = os[l][i];
+            if (z >= 0) z = (int32_t)remap[z];
+            if (o >= 0) o = (int32_t)remap[o];
+            const int64_t key = ((int64_t)z + 2) * ((int64_t)w + 3) + ((int64_t)o + 2);
+            auto it = first.find(key);
+            if (it == first.end()) {
+                const int32_t id = (int32_t)nz.size();
+                first.emplace(key, id);
+                nz.push_back(z);
+                no.push_back(o);
+                rm[i] = id;
+            } else {
+                rm[i] = it->second;
+            }
+        }
+        zs[l] = std::move(nz);
+        os[l] = std::move(no);
+        remap = std::move(rm);
+    }
+    return true;
+}
+
+}  // namespace
+
+int dm_condition_flat(int64_t num_variables, const double *costs, const int64_t *variable_order, int64_t num_bdds,
+                      const int64_t *bdd_layer_lo, const int64_t *layer_var, const int64_t *layer_node_lo,
+                      const int64_t *zero_t, const int64_t *one_t, const int8_t *fixed, int64_t *dropped_out,
+                      dm_instance **out) {
+    if (!out || !fixed || num_variables < 0 || num_bdds < 0 || (num_variables && !costs) ||
+        (num_bdds && (!bdd_layer_lo || !layer_var || !layer_node_lo || !zero_t || !one_t))) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    *out = nullptr;
+    std::vector<dm::HostBdd> kept;
+    int64_t dropped = 0;
+    for (int64_t j = 0; j < num_bdds; ++j) {
+        const int64_t l0 = bdd_layer_lo[j], l1 = bdd_layer_lo[j + 1], n = l1 - l0;
+        bool touched = false;
+        for (int64_t l = l0; l < l1; ++l) touched |= fixed[layer_var[l]] >= 0;
+        std::vector<std::vector<int32_t>> zs(n), os(n);
+        for (int64_t l = l0; l < l1; ++l) {
+            const int64_t a = layer_node_lo[l], b = layer_node_lo[l + 1], nxt = layer_node_lo[l + 1];
+            for (int64_t v = a; v < b; ++v) {
+                const int64_t z = zero_t[v], o = one_t[v];
+                zs[l - l0].push_back((int32_t)(z >= 0 ? z - nxt : z));
+                os[l - l0].push_back((int32_t)(o >= 0 ? o - nxt : o));
+            }
+            const int8_t fx = fixed[layer_var[l]];
+            if (fx == 1) std::fill(zs[l - l0].begin(), zs[l - l0].end(), dm::kFalse);
+            if (fx == 0) std::fill(os[l - l0].begin(), os[l - l0].end(), dm::kFalse);
+        }
+        if (touched) {
+            if (!reduce_local(zs, os)) {
+                dm::set_error("conditioning emptied constraint " + std::to_string(j));
+                return DM_ERR_INFEASIBLE;
+            }
+            // primal.py:114-130: a single chain accepting every fix-consistent assignment
+            bool constant = true;
+            for (int64_t k = 0; k < n && constant; ++k) {
+                if (zs[k].size() != 1) constant = false;
+                else if (fixed[layer_var[l0 + k]] >= 0) continue;
+                else if (zs[k][0] == dm::kFalse || zs[k][0] != os[k][0]) constant = false;
+            }
+            if (constant) {
+                ++dropped;
+                continue;
+            }
+        }
+        dm::HostBdd hb;
+        hb.vars.assign(layer_var + l0, layer_var + l1);
+        hb.layer_lo.assign(1, 0);
+        for (int64_t k = 0; k < n; ++k) {
+            hb.layer_lo.push_back(hb.layer_lo.back() + (int64_t)zs[k].size());
+            hb.zeros.insert(hb.zeros.end(), zs[k].begin(), zs[k].end());
+            hb.ones.insert(hb.ones.end(), os[k].begin(), os[k].end());
+        }
+        kept.push_back(std::move(hb));
+    }
+    if (dropped_out) *dropped_out = dropped;
+    std::vector<double> cst(costs, costs + num_variables);
+    std::vector<int64_t> order(num_variables);
+    if (variable_order)
+        order.assign(variable_order, variable_order + num_variables);
+    else
+        std::iota(order.begin(), order.end(), 0);
+    return split_and_flatten(kept, std::move(cst), std::move(order), 0, out);
 }
 
 int dm_instance_get_info(const dm_instance *inst, dm_instance_info *info) {

@@ -35,3 +35,11 @@ def case_inputs(case):
 
 FLAT_FIELDS = ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd", "zero_t", "one_t", "proc_ptr",
                "proc_layers")
+
+
+PRIMAL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "primal.json")
+
+
+def load_primal_cases():
+    with open(PRIMAL) as fh:
+        return json.load(fh)["cases"]
