@@ -1311,6 +1311,8 @@ int mma_grid_for(const dm_flat *f, bool forward, int threads, int want_per_sm, i
     }
     if (want_per_sm > 0) per = std::min(per, want_per_sm);
     *grid = sms * per;
+    if (const char *cap = std::getenv("DM_MMA_MAX_BLOCKS"))  // profiling: shrink the persistent grid
+        if (std::atoi(cap) > 0) *grid = std::min(*grid, std::atoi(cap));
     return DM_OK;
 }
 

@@ -286,3 +286,45 @@ def test_free_variables_clamped():  # test_dual.py:84-90
     assert sums.tolist() == [-2.0, 1.0, 3.0]
     sc = agreement_scores(st)
     assert not sc.agrees[0] and not sc.agrees[2]
+
+
+def _wide_dense_rows(seed, n_vars, n_rows, row_len, coef_max, hub_vars):
+    """Random feasible equality rows: coefficients 1..coef_max (layer widths grow
+    with the number of distinct partial sums); every row also contains the
+    `hub_vars`, so those variables have n_rows copies."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for _ in range(n_rows):
+        vs = rng.choice(np.arange(hub_vars, n_vars), size=row_len - hub_vars, replace=False)
+        vs = np.concatenate([np.arange(hub_vars), vs]).astype(np.int64)
+        cs = rng.integers(1, coef_max + 1, size=len(vs)).astype(np.int64)
+        pick = rng.random(len(vs)) < 0.5
+        rows.append((vs, cs, int(cs[pick].sum())))
+    return rng.standard_normal(n_vars), rows
+
+
+@pytest.mark.parametrize("seed,row_len,coef_max,n_rows,hubs", [
+    (0, 12, 4, 6, 0),    # layers wider than 8: per-copy W=16 / W=32 kernels
+    (1, 14, 6, 6, 0),
+    (2, 6, 1, 12, 2),    # variables with 12 copies: per-copy K=32 kernels
+    (3, 12, 5, 12, 2),   # both
+])
+def test_exact_passes_wide_and_dense_instances(seed, row_len, coef_max, n_rows, hubs):
+    costs, rows = _wide_dense_rows(seed, 40, n_rows, row_len, coef_max, hubs)
+    inst = IlpInstance.from_rows(costs, [make_row(*r) for r in rows])
+    f = inst.flat
+    assert f.max_width > 8 or f.max_degree > 8
+    oi, of = oracle_twin(inst)
+    ost = solver.init_duals(oi, of)
+    st = init_duals(inst)
+    assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
+    for _ in range(3):
+        mma_pass(st, FORWARD)
+        ost.mma(True)
+        assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
+        assert st.F.cpu().numpy().tobytes() == ost.F.tobytes()
+        mma_pass(st, BACKWARD)
+        ost.mma(False)
+        assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
+        assert st.B.cpu().numpy().tobytes() == ost.B.tobytes()
+        assert subgradient(st).tobytes() == ost.subgradient().tobytes()

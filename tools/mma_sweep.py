@@ -28,8 +28,9 @@ def main():
     results = []
     ref = None
     configs = []
-    for threads, bps in ((256, 2), (256, 3), (256, 4), (128, 4), (128, 6), (128, 8), (64, 8), (64, 12), (64, 16)):
-        configs.append((threads, bps, 0, 0, 1 << 16))
+    for threads, bps, sleep in ((256, 3, 0), (256, 3, 20), (256, 3, 50), (256, 3, 100), (256, 2, 0), (128, 3, 0),
+                                (128, 4, 0), (256, 1, 0), (128, 2, 0)):
+        configs.append((threads, bps, sleep, 0, 1 << 16))
     for threads, bps, sleep, probe, look in configs:
         try:
             st.dev.set_mma_config(threads, bps, sleep, probe, look)
