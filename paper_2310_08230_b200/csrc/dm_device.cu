@@ -1215,10 +1215,25 @@ int cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
+// Instance arrays come from the device's stream-ordered pool, which keeps
+// freed blocks (release threshold raised once): re-creating a flat for the
+// next solve reuses them instead of paying cudaMalloc again.
+void keep_pool_memory(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[device] = true;
+}
+
 template <typename T>
 int upload(dm_flat *f, T **dst, const T *src, int64_t n, cudaStream_t s) {
     size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
-    DM_CUDA(cudaMalloc((void **)dst, bytes));
+    DM_CUDA(cudaMallocAsync((void **)dst, bytes, s));
     f->allocs.push_back(*dst);
     f->bytes += bytes;
     if (n > 0 && src) DM_CUDA(cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -1490,49 +1505,71 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     int rc_fw = DM_OK, rc_bw = DM_OK, rc_sl = DM_OK;
     std::string err_fw, err_bw, err_sl;
     std::vector<int32_t> zero32(N), one32(N), lnl32, var32, pp32, pl32, bl32;
+    double plan_s[5] = {0, 0, 0, 0, 0};  // fw, bw schedules, sweep layout, relax, records
     std::vector<uint8_t> flags;
     std::vector<int4> rec;
+    // plan threads keep running while the topology is converted and uploaded
+    std::vector<std::thread> th;
+    struct Joiner {
+        std::vector<std::thread> &t;
+        ~Joiner() {
+            for (auto &x : t)
+                if (x.joinable()) x.join();
+        }
+    } joiner{th};
     {
         auto i32 = [](const int64_t *src, int64_t n) {
             std::vector<int32_t> v(n);
             for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)src[i];
             return v;
         };
-        std::vector<std::thread> th;
         th.emplace_back([&] {
+            const double t0 = host_seconds();
             rc_fw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
                                            true, fw);
             if (rc_fw) err_fw = dm_last_error();
+            plan_s[0] = host_seconds() - t0;
         });
         th.emplace_back([&] {
+            const double t0 = host_seconds();
             rc_bw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
                                            false, bw);
             if (rc_bw) err_bw = dm_last_error();
+            plan_s[1] = host_seconds() - t0;
         });
         th.emplace_back([&] {
+            const double t0 = host_seconds();
             rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
             if (rc_sl) err_sl = dm_last_error();
+            plan_s[2] = host_seconds() - t0;
         });
         th.emplace_back([&] {
+            const double t0 = host_seconds();
             relax_ok = max_width <= 8 && dm::build_relax_by_layer(bl, nb, lnl, desc->zero_t, desc->one_t, relax);
+            plan_s[3] = host_seconds() - t0;
         });
+        std::vector<std::thread> conv;
         const int nconv = 4;
         for (int t = 0; t < nconv; ++t)
-            th.emplace_back([&, t] {
+            conv.emplace_back([&, t] {
                 const int64_t lo = N * t / nconv, hi = N * (t + 1) / nconv;
                 for (int64_t i = lo; i < hi; ++i) {
                     zero32[i] = (int32_t)desc->zero_t[i];
                     one32[i] = (int32_t)desc->one_t[i];
                 }
             });
+        conv.emplace_back([&] { bl32 = i32(bl, nb + 1); });
+        conv.emplace_back([&] { lnl32 = i32(lnl, L + 1); });
+        conv.emplace_back([&] { var32 = i32(desc->layer_var, L); });
+        conv.emplace_back([&] { pp32 = i32(desc->proc_ptr, P + 1); });
+        conv.emplace_back([&] { pl32 = i32(desc->proc_layers, L); });
+        for (auto &t : conv) t.join();
         th.emplace_back([&] {
-            bl32 = i32(bl, nb + 1);
-            lnl32 = i32(lnl, L + 1);
-            var32 = i32(desc->layer_var, L);
-            pp32 = i32(desc->proc_ptr, P + 1);
-            pl32 = i32(desc->proc_layers, L);
-        });
-        th.emplace_back([&] {
+                const double t0 = host_seconds();
+                struct Stamp {
+                    double t0, &out;
+                    ~Stamp() { out = host_seconds() - t0; }
+                } stamp{t0, plan_s[4]};
                 flags.assign(L, 0);
                 for (int64_t j = 0; j < nb; ++j) {
                     flags[bl[j]] |= 1;
@@ -1540,32 +1577,34 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
                 }
                 if (!want_np) return;
                 rec.resize((size_t)P * 8);
-                for (int64_t p = 0; p < P; ++p) {
-                    const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
-                    for (int c = 0; c < 8; ++c) {
-                        int4 r{-1, 0, (int)((unsigned)k << 24), 0};
-                        if (c < k) {
-                            const int64_t l = desc->proc_layers[lo + c];
-                            const int64_t w = lnl[l + 1] - lnl[l];
-                            const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
-                            r.x = (int)l;
-                            r.y = (int)lnl[l];
-                            r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) |
-                                        ((unsigned)k << 24));
+                constexpr int kRecThreads = 6;
+                std::vector<std::thread> rt;
+                for (int t = 0; t < kRecThreads; ++t)
+                    rt.emplace_back([&, t] {
+                        const int64_t plo = P * t / kRecThreads, phi = P * (t + 1) / kRecThreads;
+                        for (int64_t p = plo; p < phi; ++p) {
+                            const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
+                            for (int c = 0; c < 8; ++c) {
+                                int4 r{-1, 0, (int)((unsigned)k << 24), 0};
+                                if (c < k) {
+                                    const int64_t l = desc->proc_layers[lo + c];
+                                    const int64_t w = lnl[l + 1] - lnl[l];
+                                    const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
+                                    r.x = (int)l;
+                                    r.y = (int)lnl[l];
+                                    r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) |
+                                                ((unsigned)k << 24));
+                                }
+                                rec[(size_t)p * 8 + c] = r;
+                            }
                         }
-                        rec[(size_t)p * 8 + c] = r;
-                    }
-                }
+                    });
+                for (auto &x : rt) x.join();
             });
-        for (auto &t : th) t.join();
     }
-    if (rc_fw) { dm::set_error(err_fw); return rc_fw; }
-    if (rc_bw) { dm::set_error(err_bw); return rc_bw; }
-    if (rc_sl) { dm::set_error(err_sl); return rc_sl; }
     int rc = DM_OK;
-    const double t_plans = host_seconds();
-
     DM_CUDA(cudaSetDevice(device));
+    keep_pool_memory(device);
     cudaStream_t s = (cudaStream_t)stream;
     auto f = std::make_unique<dm_flat>();
     f->device = device;
@@ -1575,10 +1614,6 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     f->P = P;
     f->max_width = max_width;
     f->max_degree = max_degree;
-    f->fw_depth = fw.depth;
-    f->bw_depth = bw.depth;
-    f->fw_tasks = fw.tasks;
-    f->bw_tasks = bw.tasks;
     auto up = [&](int32_t **dst, const std::vector<int32_t> &v) {
         return upload(f.get(), dst, v.data(), (int64_t)v.size(), s);
     };
@@ -1595,6 +1630,15 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     const std::vector<int32_t> progress_init{-1, 0}, status_init{0};
     if ((rc = up(&f->progress, progress_init))) return rc;  // progress hint, task queue
     if ((rc = up(&f->status, status_init))) return rc;
+    for (auto &t : th) t.join();  // host plans (overlapped with the topology upload)
+    if (rc_fw) { dm::set_error(err_fw); return rc_fw; }
+    if (rc_bw) { dm::set_error(err_bw); return rc_bw; }
+    if (rc_sl) { dm::set_error(err_sl); return rc_sl; }
+    const double t_plans = host_seconds();
+    f->fw_depth = fw.depth;
+    f->bw_depth = bw.depth;
+    f->fw_tasks = fw.tasks;
+    f->bw_tasks = bw.tasks;
     if (relax_ok) {
         if ((rc = upload(f.get(), &f->relax_layer, relax.data(), L, s))) return rc;
         f->relax_ok = true;
@@ -1652,8 +1696,11 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     f->flags_h = std::move(flags);
     if (!f->mma_np && (rc = ensure_per_copy_schedules(f.get(), s))) return rc;
     if (env_int("DM_VERBOSE", 0))
-        std::fprintf(stderr, "[dm_flat_create] validate %.3fs, plans %.3fs, upload %.3fs\n", t_valid - t_begin,
-                     t_plans - t_valid, host_seconds() - t_plans);
+        std::fprintf(stderr,
+                     "[dm_flat_create] validate %.3fs, topology upload + plans %.3fs, plan upload %.3fs "
+                     "(plans: fw %.3f bw %.3f sweep %.3f relax %.3f records %.3f)\n",
+                     t_valid - t_begin, t_plans - t_valid, host_seconds() - t_plans, plan_s[0], plan_s[1], plan_s[2],
+                     plan_s[3], plan_s[4]);
     *out = f.release();
     return DM_OK;
 }
@@ -1745,7 +1792,9 @@ int dm_flat_status(dm_flat *f, void *stream) {
 
 void dm_flat_destroy(dm_flat *f) {
     if (!f) return;
-    for (void *p : f->allocs) cudaFree(p);
+    // legacy default stream: ordered after all work on blocking streams
+    for (void *p : f->allocs) cudaFreeAsync(p, 0);
+    cudaGetLastError();
     delete f;
 }
 
@@ -1816,7 +1865,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     if (f->mma_np && !forward) {
         dm_flat *m = const_cast<dm_flat *>(f);
         if (!m->dec) {
-            DM_CUDA(cudaMalloc((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t)));
+            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t), s));
             m->allocs.push_back(m->dec);
             m->bytes += (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t);
         }

@@ -14,6 +14,7 @@
 #include <numeric>
 #include <string>
 #include <map>
+#include <thread>
 #include <vector>
 
 #include "dm_internal.h"
@@ -303,18 +304,38 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
                        const int64_t *proc_layers, int64_t npos, bool forward, MmaSchedule &s) {
     (void)layer_var;
     (void)layer_bdd;
-    // level of each position along the dependency DAG: a copy at layer l
+    // Level of each position along the dependency DAG: a copy at layer l
     // depends on the copy at layer l-1 (forward) / l+1 (backward) of its
-    // diagram, which the visitation order processes earlier.
-    std::vector<int32_t> layer_level(L, 0);
+    // diagram, which the visitation order processes just before — so it is
+    // the diagram's most recently processed layer, and a per-diagram "level
+    // of the last processed layer" (small, cache-resident) replaces random
+    // reads of a per-layer table.  The per-copy diagram ids and end flags are
+    // gathered in parallel first.
+    std::vector<int32_t> lbdd(L), cb(L);
+    std::vector<uint8_t> ce(L);
+    {
+        constexpr int kThreads = 8;
+        auto par = [&](int64_t n, auto &&fn) {
+            std::vector<std::thread> th;
+            for (int t = 0; t < kThreads; ++t) th.emplace_back([&, t] { fn(n * t / kThreads, n * (t + 1) / kThreads); });
+            for (auto &x : th) x.join();
+        };
+        par(nb, [&](int64_t lo, int64_t hi) {
+            for (int64_t j = lo; j < hi; ++j)
+                for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) lbdd[l] = (int32_t)j;
+        });
+        par(L, [&](int64_t lo, int64_t hi) {
+            for (int64_t t = lo; t < hi; ++t) {
+                const int64_t l = proc_layers[t];
+                const int32_t j = lbdd[l];
+                cb[t] = j;
+                ce[t] = forward ? (l == bdd_layer_lo[j]) : (l + 1 == bdd_layer_lo[j + 1]);
+            }
+        });
+    }
+    std::vector<int32_t> last_level(nb, 0);
     std::vector<int32_t> pos_level(npos, -1);
     int32_t depth = 0;
-    // first/last-layer flags packed above the level bits, filled in memory order
-    constexpr int32_t kFirstFlag = 1 << 29, kLastFlag = 1 << 30, kLevelMask = (1 << 29) - 1;
-    for (int64_t j = 0; j < nb; ++j) {
-        layer_level[bdd_layer_lo[j]] |= kFirstFlag;
-        layer_level[bdd_layer_lo[j + 1] - 1] |= kLastFlag;
-    }
     for (int64_t k = 0; k < npos; ++k) {
         const int64_t p = forward ? k : npos - 1 - k;
         const int64_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
@@ -325,16 +346,9 @@ int build_mma_schedule(const int64_t *bdd_layer_lo, int64_t nb, const int64_t *l
             return DM_ERR_UNSUPPORTED;
         }
         int32_t lev = 0;
-        for (int64_t t = lo; t < hi; ++t) {
-            const int64_t l = proc_layers[t];
-            // one cache line: the flags of l and the level of its neighbour
-            if (forward && !(layer_level[l] & kFirstFlag)) lev = std::max(lev, (layer_level[l - 1] & kLevelMask) + 1);
-            if (!forward && !(layer_level[l] & kLastFlag)) lev = std::max(lev, (layer_level[l + 1] & kLevelMask) + 1);
-        }
-        for (int64_t t = lo; t < hi; ++t) {
-            int32_t &slot = layer_level[proc_layers[t]];
-            slot = (slot & ~kLevelMask) | lev;
-        }
+        for (int64_t t = lo; t < hi; ++t)
+            if (!ce[t]) lev = std::max(lev, last_level[cb[t]] + 1);
+        for (int64_t t = lo; t < hi; ++t) last_level[cb[t]] = lev;
         pos_level[p] = lev;
         depth = std::max(depth, lev + 1);
     }

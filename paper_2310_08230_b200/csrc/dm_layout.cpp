@@ -154,28 +154,43 @@ bool build_relax_by_layer(const int64_t *bdd_layer_lo, int64_t nb, const int64_t
                           const int64_t *one_t, std::vector<uint64_t> &desc_out) {
     const int64_t L = nb ? bdd_layer_lo[nb] : 0;
     desc_out.assign(L, ~0ull);
-    for (int64_t j = 0; j < nb; ++j)
-        for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
-            if (l + 1 == bdd_layer_lo[j + 1]) continue;  // last layers keep the tree path
-            const int64_t v0 = lnl[l], w = lnl[l + 1] - v0;
-            const int64_t n0 = lnl[l + 1];
-            const int64_t wn = lnl[l + 2] - n0;
-            if (w > 8 || wn > 8) return false;
-            uint64_t desc = ~0ull;
-            for (int64_t i = 0; i < w; ++i) {
-                const int64_t t[2] = {zero_t[v0 + i], one_t[v0 + i]};
-                for (int k = 0; k < 2; ++k) {
-                    if (t[k] < 0) continue;  // terminal
-                    const int64_t u = t[k] - n0;
-                    if (u < 0 || u >= wn) return false;
-                    const int sh = 8 * (int)u + 4 * k;
-                    if (((desc >> sh) & 15) != 15) return false;
-                    desc &= ~(15ull << sh);
-                    desc |= (uint64_t)i << sh;
+    constexpr int kThreads = 6;
+    bool ok[kThreads];
+    std::vector<std::thread> th;
+    for (int t = 0; t < kThreads; ++t)
+        th.emplace_back([&, t] {
+            ok[t] = true;
+            for (int64_t j = nb * t / kThreads; j < nb * (t + 1) / kThreads && ok[t]; ++j)
+                for (int64_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1] && ok[t]; ++l) {
+                    if (l + 1 == bdd_layer_lo[j + 1]) continue;  // last layers keep the tree path
+                    const int64_t v0 = lnl[l], w = lnl[l + 1] - v0;
+                    const int64_t n0 = lnl[l + 1];
+                    const int64_t wn = lnl[l + 2] - n0;
+                    if (w > 8 || wn > 8) {
+                        ok[t] = false;
+                        break;
+                    }
+                    uint64_t desc = ~0ull;
+                    for (int64_t i = 0; i < w && ok[t]; ++i) {
+                        const int64_t tg[2] = {zero_t[v0 + i], one_t[v0 + i]};
+                        for (int k = 0; k < 2; ++k) {
+                            if (tg[k] < 0) continue;  // terminal
+                            const int64_t u = tg[k] - n0;
+                            const int sh = 8 * (int)u + 4 * k;
+                            if (u < 0 || u >= wn || ((desc >> sh) & 15) != 15) {
+                                ok[t] = false;
+                                break;
+                            }
+                            desc &= ~(15ull << sh);
+                            desc |= (uint64_t)i << sh;
+                        }
+                    }
+                    desc_out[l] = desc;
                 }
-            }
-            desc_out[l] = desc;
-        }
+        });
+    for (auto &x : th) x.join();
+    for (int t = 0; t < kThreads; ++t)
+        if (!ok[t]) return false;
     return true;
 }
 

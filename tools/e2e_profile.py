@@ -29,3 +29,4 @@ for rep in range(3):
     t3 = time.perf_counter()
     print(f"rep {rep}: FlatBdds {t1 - t0:.3f}s init_duals {t2 - t1:.3f}s solve(10) {t3 - t2:.3f}s total {t3 - t0:.3f}s",
           flush=True)
+    del flat, st, res
