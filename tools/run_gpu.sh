@@ -41,6 +41,7 @@ for step in "$@"; do
     abnp) timeout 1200 python tools/ab_mma.py DM_MMA_NP=0 DM_MMA_NP=1 DM_MMA_NP=0 DM_MMA_NP=1 > gpurun_out/abnp.jsonl 2> gpurun_out/abnp.err ;;
     e2eprof) timeout 900 python tools/e2e_profile.py > gpurun_out/e2eprof.txt 2>&1 ;;
     worklat) timeout 600 python tools/work_latency.py icosa > gpurun_out/worklat.txt 2>&1 ;;
+    timeline) timeout 900 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err ;;
     phases) timeout 900 python tools/step_phases.py 12 > gpurun_out/phases.jsonl 2> gpurun_out/phases.err ;;
     vec) timeout 300 python tools/vec_bench.py > gpurun_out/vec.json 2> gpurun_out/vec.err && \
       timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -c 400 --csv \
