@@ -168,19 +168,19 @@ __global__ void k_argmin_kernel(int32_t nb, const int32_t *__restrict__ bdd_laye
     }
 }
 
-// The same walk from the decisions the node-parallel backward pass recorded:
-// one dependent load per layer instead of two.
+// The same walk from the decisions the node-parallel backward pass recorded
+// (one byte per node: (next-layer slot << 1) | bit, an L2-resident table):
+// one dependent byte load per layer instead of two table lookups.
 __global__ void k_argmin_walk_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
-                                     const int32_t *__restrict__ lnl, const int32_t *__restrict__ dec,
+                                     const int32_t *__restrict__ lnl, const uint8_t *__restrict__ dec,
                                      double *__restrict__ bits) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= nb) return;
-    int32_t v = lnl[bdd_layer_lo[j]];
+    int32_t slot = 0;  // the root
     for (int32_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
-        const int32_t code = dec[v];
+        const int32_t code = dec[lnl[l] + slot];
         bits[l] = (double)(code & 1);
-        const int32_t nxt = (code >> 1) - 2;
-        if (nxt >= 0) v = nxt;
+        slot = code >> 1;
     }
 }
 
@@ -396,7 +396,7 @@ struct MmaArgs {
     // per position p, 8 copy records {layer, first node, w | wn<<8 | flags<<16 | k<<24, 0}
     const int4 *np_rec;
     int *task_counter;  // dynamic task queue of the node-parallel kernels
-    int32_t *dec;       // node-parallel backward: per node ((chosen target + 2) << 1) | bit
+    uint8_t *dec;       // node-parallel backward: per node (chosen next-layer slot << 1) | bit
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -1137,7 +1137,10 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 st_relaxed(a.B + r.nlo + i, bv);
                 // the argmin walk's decision at this node (kernels.py:402-431 on
                 // the final duals and distances: same operands, same compare)
-                if (a.dec) a.dec[r.nlo + i] = (((zero_wins ? zt[j] : ot[j]) + 2) << 1) | (zero_wins ? 0 : 1);
+                if (a.dec) {
+                    const int32_t t = zero_wins ? zt[j] : ot[j];
+                    a.dec[r.nlo + i] = (uint8_t)(((t >= 0 ? t - n0n : 0) << 1) | (zero_wins ? 0 : 1));
+                }
                 if (i == 0 && r.first) a.bounds[a.layer_bdd[r.l]] = bv;  // kernels.py:359-361
             }
         }
@@ -1180,7 +1183,7 @@ struct dm_flat {
     int32_t *fw_pos = nullptr, *bw_pos = nullptr;
     uint8_t *layer_flags = nullptr;
     int4 *np_rec = nullptr;
-    int32_t *dec = nullptr;          // decisions of the last node-parallel backward pass
+    uint8_t *dec = nullptr;          // decisions of the last node-parallel backward pass
     const double *dec_B = nullptr;   // ... and the distance table it wrote (nullptr: none)
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
     std::vector<int32_t> fw_pos_level, bw_pos_level, fw_pos_h, bw_pos_h;  // host copies (profiling)
@@ -1865,9 +1868,9 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     if (f->mma_np && !forward) {
         dm_flat *m = const_cast<dm_flat *>(f);
         if (!m->dec) {
-            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t), s));
+            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1), s));
             m->allocs.push_back(m->dec);
-            m->bytes += (size_t)std::max<int64_t>(f->N, 1) * sizeof(int32_t);
+            m->bytes += (size_t)std::max<int64_t>(f->N, 1);
         }
         args.dec = m->dec;
         m->dec_B = B;
