@@ -197,9 +197,9 @@ int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, in
  * L-BFGS path — numpy pairwise over each 4096-element chunk of a*b, then
  * over the chunk totals (n <= 4096^2); the reference's OpenBLAS ddot order
  * is host-dependent, so any fixed order is parity-equivalent.  Results land in device
- * memory.  Reduction trees are planned once per (device, length) and cached
- * for the process; reductions of the same length must not run concurrently
- * on two streams of one device. */
+ * memory.  Reduction trees and their scratch are planned once per (device,
+ * length, stream) and cached for the process, so solves on different streams
+ * may run concurrently; calls on one stream are ordered by that stream. */
 int dm_sum(const double *x, int64_t n, double *out, void *stream);
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream);
 

@@ -33,6 +33,7 @@
 #include <chrono>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "dm_internal.h"
@@ -1243,11 +1244,12 @@ int upload(dm_flat *f, T **dst, const T *src, int64_t n, cudaStream_t s) {
     return DM_OK;
 }
 
-// Pairwise plans are cached per (device, length) for the process lifetime.
-// The value scratch of a plan is shared: reductions of one length must not
-// run concurrently on two streams of the same device.
+// Pairwise plans are cached per (device, length, stream) for the process
+// lifetime: a plan's value scratch belongs to one stream, so instances solved
+// concurrently on different streams never share it.
 std::mutex g_plan_mu;
-std::map<std::pair<int, int64_t>, DevPlan> g_plans;
+using ScratchKey = std::tuple<int, int64_t, uintptr_t>;
+std::map<ScratchKey, DevPlan> g_plans;
 
 template <typename T>
 int plan_upload(T **dst, const std::vector<T> &src, size_t extra = 0) {
@@ -1257,11 +1259,11 @@ int plan_upload(T **dst, const std::vector<T> &src, size_t extra = 0) {
     return DM_OK;
 }
 
-int get_plan(int64_t n, DevPlan **out) {
+int get_plan(int64_t n, cudaStream_t stream, DevPlan **out) {
     int dev;
     DM_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_plan_mu);
-    auto key = std::make_pair(dev, n);
+    auto key = ScratchKey(dev, n, (uintptr_t)stream);
     auto it = g_plans.find(key);
     if (it != g_plans.end()) {
         *out = &it->second;
@@ -1685,8 +1687,8 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
                            ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17) | ((env_int("DM_MMA_NP", 1) ? 0 : 1) << 18));
     if (rc) return rc;
     DevPlan *dummy;
-    if ((rc = get_plan(nb, &dummy))) return rc;
-    if ((rc = get_plan(L, &dummy))) return rc;
+    if ((rc = get_plan(nb, s, &dummy))) return rc;
+    if ((rc = get_plan(L, s, &dummy))) return rc;
     DM_CUDA(cudaStreamSynchronize(s));  // the host staging vectors die with this scope
     // kept on the host: level order of the positions (profiling) and what the
     // per-copy kernels' task packing needs if they are selected later
@@ -1967,7 +1969,7 @@ static int pairwise(const double *a, const double *b, int64_t n, double *out, cu
         return DM_ERR_INVALID;
     }
     DevPlan *p;
-    int rc = get_plan(n, &p);
+    int rc = get_plan(n, s, &p);
     if (rc) return rc;
     if (b)
         pw_leaf_kernel<true><<<blocks_for((int64_t)p->nleaves * 8, 256), 256, 0, s>>>(p->nleaves, p->leaf_off, p->leaf_len, a, b, p->vals);
@@ -1981,21 +1983,21 @@ int dm_sum(const double *x, int64_t n, double *out, void *stream) {
     return pairwise(x, nullptr, n, out, (cudaStream_t)stream);
 }
 
-// Per-(device, length) scratch of the chunked dot: chunk totals and the
-// two-loop scalars (same single-stream contract as the pairwise plans).
+// Per-(device, length, stream) scratch of the chunked dot: chunk totals and
+// the two-loop scalars (same per-stream ownership as the pairwise plans).
 struct DotScratch {
     double *partial = nullptr;  // chunk totals
     double *slots = nullptr;    // two-loop scalars (dm_lbfgs_direction)
 };
-static std::map<std::pair<int, int64_t>, DotScratch> g_dot;
+static std::map<ScratchKey, DotScratch> g_dot;
 constexpr int kMaxPairs = 64;
 
-static int dot_scratch(int64_t n, bool slots, DotScratch **out) {
+static int dot_scratch(int64_t n, void *stream, bool slots, DotScratch **out) {
     const int64_t nch = (n + dm::kDotChunk - 1) / dm::kDotChunk;
     int dev;
     DM_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_plan_mu);
-    auto key = std::make_pair(dev, n);
+    auto key = ScratchKey(dev, n, (uintptr_t)stream);
     auto it = g_dot.find(key);
     if (it == g_dot.end()) {
         DotScratch d;
@@ -2026,7 +2028,7 @@ int dm_dot(const double *a, const double *b, int64_t n, double *out, void *strea
         return DM_ERR_UNSUPPORTED;
     }
     DotScratch *sc;
-    if (int rc = dot_scratch(n, false, &sc)) return rc;
+    if (int rc = dot_scratch(n, stream, false, &sc)) return rc;
     return dm::chunk_dot(a, b, n, sc->partial, out, stream);
 }
 
@@ -2046,7 +2048,7 @@ int dm_lbfgs_direction(const double *g, const double *const *s, const double *co
             return DM_ERR_INVALID;
         }
     DotScratch *sc;
-    if (int rc = dot_scratch(n, true, &sc)) return rc;
+    if (int rc = dot_scratch(n, stream, true, &sc)) return rc;
     return dm::lbfgs_two_loop(g, s, y, rho, sy, m, n, d, sc->slots, sc->partial, stream);
 }
 

@@ -328,3 +328,14 @@ def test_exact_passes_wide_and_dense_instances(seed, row_len, coef_max, n_rows, 
         assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
         assert st.B.cpu().numpy().tobytes() == ost.B.tobytes()
         assert subgradient(st).tobytes() == ost.subgradient().tobytes()
+
+
+def test_solve_batch_matches_sequential_solves():
+    insts = [product_instance(c) for c in CASES if c["name"] in ("ps_tetra", "ps_icosa", "random3_c3", "random7_c0")]
+    cfg = SolveConfig(mode="hybrid", max_iterations=8)
+    seq = [qn.solve(i, cfg) for i in insts]
+    for k in (2, 3):
+        bat = qn.solve_batch(insts, cfg, concurrency=k)
+        for a, b in zip(seq, bat):
+            assert a.bounds == b.bounds
+            assert a.state.lam.tobytes() == b.state.lam.tobytes()

@@ -42,6 +42,8 @@ for step in "$@"; do
     e2eprof) timeout 900 python tools/e2e_profile.py > gpurun_out/e2eprof.txt 2>&1 ;;
     worklat) timeout 600 python tools/work_latency.py icosa > gpurun_out/worklat.txt 2>&1 ;;
     timeline) timeout 900 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err ;;
+    concur) timeout 900 python tools/concurrency.py > gpurun_out/concur.jsonl 2> gpurun_out/concur.err ;;
+    batch) timeout 1500 python tools/batch_solve.py 4 > gpurun_out/batch.jsonl 2> gpurun_out/batch.err ;;
     phases) timeout 900 python tools/step_phases.py 12 > gpurun_out/phases.jsonl 2> gpurun_out/phases.err ;;
     vec) timeout 300 python tools/vec_bench.py > gpurun_out/vec.json 2> gpurun_out/vec.err && \
       timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -c 400 --csv \
