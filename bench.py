@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--e2e-iters", type=int, default=50)
     ap.add_argument("--ttg-max-iters", type=int, default=150)
+    ap.add_argument("--batch", type=int, default=0, help="also time K independent instances via qn.solve_batch")
+    ap.add_argument("--batch-iters", type=int, default=30)
     return ap.parse_args()
 
 
@@ -376,6 +378,8 @@ def run_b200(args, rank, world, local_rank):
                                  "clock": "host perf_counter from solve() start, duals resident"}
     if rank == 0 and not args.no_e2e:
         result["e2e"] = e2e_run(args, inst, dev)
+    if rank == 0 and args.batch > 1:
+        result["batch"] = batch_run(args, inst, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, spi, thr = cpu_reference_run(inst, 1, args.cpu_iters)
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
@@ -385,6 +389,35 @@ def run_b200(args, rank, world, local_rank):
         if result.get("time_to_gap", {}).get("iterations"):
             result["time_to_gap"]["cpu_projected_s"] = spi * result["time_to_gap"]["iterations"]
     return result
+
+
+def batch_run(args, inst, dev):
+    """C5-style throughput on one GPU: --batch independent instances (seeds
+    seed..seed+K-1, the first being the bench instance) solved one after
+    another vs through qn.solve_batch (two concurrent streams); same
+    iteration count, duals required identical."""
+    import torch
+
+    from paper_2310_08230_b200.config import SolveConfig
+    from paper_2310_08230_b200.qn import solve, solve_batch
+
+    insts = [inst] + [build_instance(args.config, args.seed + k) for k in range(1, args.batch)]
+    cfg = SolveConfig(mode="hybrid", max_iterations=args.batch_iters, dual_tolerance=0.0)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    seq = [solve(i, cfg, device=dev) for i in insts]
+    torch.cuda.synchronize()
+    t_seq = time.perf_counter() - t
+    t = time.perf_counter()
+    bat = solve_batch(insts, cfg, device=dev, concurrency=2)
+    torch.cuda.synchronize()
+    t_bat = time.perf_counter() - t
+    same = all(a.state.lam.tobytes() == b.state.lam.tobytes() for a, b in zip(seq, bat))
+    arcs = sum(r.state.arc_updates for r in bat)
+    return {"instances": len(insts), "iterations": args.batch_iters, "concurrency": 2,
+            "sequential_s": t_seq, "batch_s": t_bat, "value": arcs / t_bat, "unit": UNIT,
+            "sequential_value": arcs / t_seq, "identical_to_sequential": same,
+            "step": "qn.solve from the lowered host instances incl. device upload, per instance"}
 
 
 def e2e_run(args, inst, dev):
