@@ -1797,7 +1797,10 @@ int dm_flat_status(dm_flat *f, void *stream) {
 
 void dm_flat_destroy(dm_flat *f) {
     if (!f) return;
-    // legacy default stream: ordered after all work on blocking streams
+    // the flat may still be in use by work on any (possibly non-blocking)
+    // stream: wait for the device, then hand the blocks back to the pool
+    cudaSetDevice(f->device);
+    cudaDeviceSynchronize();
     for (void *p : f->allocs) cudaFreeAsync(p, 0);
     cudaGetLastError();
     delete f;
