@@ -212,6 +212,13 @@ int dm_dot(const double *a, const double *b, int64_t n, double *out, void *strea
 int dm_lbfgs_direction(const double *g, const double *const *s, const double *const *y, const double *rho,
                        const double *sy, int m, int64_t n, double *d, void *stream);
 
+/* Curvature pair of one quasi-Newton iteration (reference qn.py:245-252 +
+ * update_history's s @ y, qn.py:85-92) in one pass: s = lam - lam_prev,
+ * y = g_prev - g, lam_prev = lam, *sy = s . y in dm_dot's order — values
+ * identical to dm_sub, dm_sub, dm_dot and a copy.  Shares dm_dot's scratch. */
+int dm_curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
+                      double *y, int64_t n, double *sy, void *stream);
+
 /* Elementwise updates with numpy's rounding (no contraction):
  *   dm_axpy_dev : x[i] = x[i] - (alpha_host * dot_dev[0]) * y[i]            (qn.py:108-109)
  *   dm_scale_dev: x[i] = (num_host / den_dev[0]) * x[i]                     (qn.py:111-112)

@@ -80,6 +80,7 @@ SIGNATURES = {
     "dm_scale_dev": ([_P, _D, _P, _I, _P], _INT),
     "dm_lbfgs_up": ([_P, _P, _P, _D, _P, _I, _P], _INT),
     "dm_lbfgs_direction": ([_P, _P, _P, _P, _P, _INT, _I, _P, _P], _INT),
+    "dm_curvature_pair": ([_P, _P, _P, _P, _P, _P, _I, _P, _P], _INT),
     "dm_axpy_host": ([_P, _D, _P, _I, _P], _INT),
     "dm_sub": ([_P, _P, _P, _I, _P], _INT),
     "dm_host_pairwise_sum": ([_P, _I, _P], _INT),
@@ -125,12 +126,12 @@ def check(rc: int, what: str = "") -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
-LAUNCHES = {"dm_k_mma_forward": 3, "dm_k_mma_backward": 2, "dm_sum": 2}
+LAUNCHES = {"dm_k_mma_forward": 3, "dm_k_mma_backward": 2, "dm_sum": 2, "dm_curvature_pair": 2}
 KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_mma_forward",
                   "dm_k_mma_backward", "dm_k_min_marginals", "dm_k_argmin", "dm_init_duals",
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
-                  "dm_lbfgs_direction", "dm_k_argmin_from_pass"}
+                  "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair"}
 launch_count = 0
 
 

@@ -2055,6 +2055,21 @@ int dm_lbfgs_direction(const double *g, const double *const *s, const double *co
     return dm::lbfgs_two_loop(g, s, y, rho, sy, m, n, d, sc->slots, sc->partial, stream);
 }
 
+int dm_curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
+                      double *y, int64_t n, double *sy, void *stream) {
+    if (!lam || !lam_prev || !g || !g_prev || !s || !y || !sy || n < 1) {
+        dm::set_error("dm_curvature_pair: needs six vectors of length n >= 1 and an output");
+        return DM_ERR_INVALID;
+    }
+    if ((n + dm::kDotChunk - 1) / dm::kDotChunk > dm::kDotChunk) {
+        dm::set_error("dm_curvature_pair: length above 4096*4096 not supported");
+        return DM_ERR_UNSUPPORTED;
+    }
+    DotScratch *sc;
+    if (int rc = dot_scratch(n, stream, false, &sc)) return rc;
+    return dm::curvature_pair(lam, lam_prev, g, g_prev, s, y, n, sc->partial, sy, stream);
+}
+
 int dm_axpy_dev(double *x, const double *y, double alpha_host, const double *dot_dev, double *alpha_out, int64_t n,
                 void *stream) {
     axpy_dev_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, y, alpha_host, dot_dev, alpha_out, n);

@@ -133,6 +133,9 @@ int chunk_dot(const double *a, const double *b, int64_t n, double *partial, doub
 constexpr int64_t kDotChunk = 4096;
 // L-BFGS two-loop direction (qn.py:95-115) in 2m+2 fused launches; s/y are
 // host arrays of m device pointers (newest first), slots >= 3m+1 doubles.
+// s = lam - lam_prev, y = g_prev - g, lam_prev = lam and sy = s . y (chunked-dot order), one pass
+int curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
+                   double *y, int64_t n, double *partial, double *sy, void *stream);
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
 

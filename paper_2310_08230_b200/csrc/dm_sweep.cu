@@ -289,11 +289,13 @@ __device__ __forceinline__ double step_update(const StepCoef &c, double xo, doub
 // the leaves (<= 32 runs of <= 128 elements, left to right) are nodes
 // 0..nleaves-1; the additions are nodes nleaves.. in post-order (the root
 // last), each with its two children and its height above the leaves.
+// Up to 33 leaves for n <= 4096 (e.g. 217 lengths in [3849, 4095]).
+constexpr int kMaxLeaves = 33;
 struct SumPlan {
     int32_t nleaves, nint, height;
-    uint16_t off[32];
-    uint8_t len[32];
-    uint8_t left[31], right[31], h[31];
+    uint16_t off[kMaxLeaves];
+    uint8_t len[kMaxLeaves];
+    uint8_t left[kMaxLeaves - 1], right[kMaxLeaves - 1], h[kMaxLeaves - 1];
 };
 
 int plan_rec(SumPlan &p, int off, int len, int &height, std::vector<int> &post) {
@@ -333,12 +335,14 @@ SumPlan make_sum_plan(int n) {
 }
 
 // 0.0 + numpy pairwise_sum(sm[0:n]) of shared-memory values, by a block of
-// >= 256 threads: one octet per leaf (numpy's 8 accumulators), then warp 0
-// adds the tree level by level.  Result on thread 0.
+// any multiple of 32 threads: one octet per leaf (numpy's 8 accumulators),
+// then warp 0 adds the tree level by level.  Result on thread 0.
 __device__ double smem_pairwise(const double *sm, const SumPlan &p) {
-    __shared__ double node[64];
-    const int oct = threadIdx.x >> 3, q = threadIdx.x & 7;
-    if (oct < 32) {  // whole warps: 256 threads
+    __shared__ double node[2 * kMaxLeaves];
+    const int q = threadIdx.x & 7;
+    // octets in passes of blockDim/8 (uniform trip count: whole warps shuffle)
+    for (int base = 0; base < p.nleaves; base += (int)(blockDim.x >> 3)) {
+        const int oct = base + (int)(threadIdx.x >> 3);
         const bool live = oct < p.nleaves;
         const int off = live ? p.off[oct] : 0, len = live ? p.len[oct] : 0;
         const int stop = len - (len % 8);
@@ -358,7 +362,7 @@ __device__ double smem_pairwise(const double *sm, const SumPlan &p) {
     __syncthreads();
     double total = 0.0;
     if (threadIdx.x < 32 && p.nleaves > 0) {
-        const int k = threadIdx.x;
+        const int k = threadIdx.x;  // internal nodes: at most 32, one per lane
         for (int h = 1; h <= p.height; ++h) {
             if (k < p.nint && p.h[k] == h) node[p.nleaves + k] = __dadd_rn(node[p.left[k]], node[p.right[k]]);
             __syncwarp();
@@ -533,9 +537,108 @@ cudaError_t chunk_step(const ChunkStep &a, int64_t n, double *partial, cudaStrea
     return launch_maybe_pdl(chunk_finish_kernel<kMode>, 1, kFinishThreads, st, true, a, n, full, partial, plans);
 }
 
+// Curvature pair of one iteration (qn.py:85-92, 245-252) in one pass:
+// s = lam - lam_prev, y = g_prev - g, lam_prev = lam, and the chunk totals of
+// s . y in the chunked-dot order (every chunk, tail included, here; the
+// finishing block only reduces the totals).  Values equal dm_sub x2 + dm_dot.
+__global__ void __launch_bounds__(kChunkThreads) curvature_pair_kernel(const double *__restrict__ lam,
+                                                                       double *__restrict__ lam_prev,
+                                                                       const double *__restrict__ g,
+                                                                       const double *__restrict__ g_prev,
+                                                                       double *__restrict__ s_out,
+                                                                       double *__restrict__ y_out, int64_t n,
+                                                                       bool vec, double *__restrict__ partial,
+                                                                       const __grid_constant__ FinishPlans plans) {
+    __shared__ double buf[kChunk];
+    const int64_t off = (int64_t)blockIdx.x * kChunk;
+    const int len = (int)((n - off) < kChunk ? (n - off) : kChunk);
+    double t = 0.0;
+    if (vec && len == kChunk) {
+        const double2 *l2 = reinterpret_cast<const double2 *>(lam + off);
+        double2 *p2 = reinterpret_cast<double2 *>(lam_prev + off);
+        const double2 *g2 = reinterpret_cast<const double2 *>(g + off);
+        const double2 *q2 = reinterpret_cast<const double2 *>(g_prev + off);
+        double2 *s2 = reinterpret_cast<double2 *>(s_out + off);
+        double2 *y2 = reinterpret_cast<double2 *>(y_out + off);
+        double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+        for (int i0 = 0; i0 < 16; i0 += 4) {
+            double2 lv[4], pv[4], gv[4], qv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = pair_index(i0 + k);
+                lv[k] = l2[j];
+                pv[k] = p2[j];
+                gv[k] = g2[j];
+                qv[k] = q2[j];
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = pair_index(i0 + k);
+                const double2 sv = make_double2(__dsub_rn(lv[k].x, pv[k].x), __dsub_rn(lv[k].y, pv[k].y));
+                const double2 yv = make_double2(__dsub_rn(qv[k].x, gv[k].x), __dsub_rn(qv[k].y, gv[k].y));
+                s2[j] = sv;
+                y2[j] = yv;
+                p2[j] = lv[k];
+                const double p0 = __dmul_rn(sv.x, yv.x), p1 = __dmul_rn(sv.y, yv.y);
+                r0 = (i0 + k == 0) ? p0 : __dadd_rn(r0, p0);
+                r1 = (i0 + k == 0) ? p1 : __dadd_rn(r1, p1);
+            }
+        }
+        const unsigned m = 0xffffffffu;
+        double r = __dadd_rn(r0, r1);
+        r = __dadd_rn(r, __shfl_xor_sync(m, r, 1));
+        r = __dadd_rn(r, __shfl_xor_sync(m, r, 2));
+        if ((threadIdx.x & 3) == 0) buf[threadIdx.x >> 2] = r;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double x = buf[threadIdx.x];
+#pragma unroll
+            for (int w = 1; w < 32; w <<= 1) x = __dadd_rn(x, __shfl_xor_sync(m, x, w));
+            t = __dadd_rn(0.0, x);
+        }
+    } else {
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            const double sv = __dsub_rn(lam[off + i], lam_prev[off + i]);
+            const double yv = __dsub_rn(g_prev[off + i], g[off + i]);
+            s_out[off + i] = sv;
+            y_out[off + i] = yv;
+            lam_prev[off + i] = lam[off + i];
+            buf[i] = __dmul_rn(sv, yv);
+        }
+        __syncthreads();
+        t = smem_pairwise(buf, len == kChunk ? plans.chunk : plans.tail);
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
 }  // namespace
 
 namespace dm {
+
+int curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
+                   double *y, int64_t n, double *partial, double *sy, void *stream) {
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    if (n <= 0 || nch > kChunk) return DM_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool vec = aligned16(lam) && aligned16(lam_prev) && aligned16(g) && aligned16(g_prev) && aligned16(s) &&
+                     aligned16(y);
+    FinishPlans plans;
+    plans.chunk = make_sum_plan(kChunk);
+    plans.tail = make_sum_plan((int)(n % kChunk));
+    plans.totals = make_sum_plan((int)nch);
+    curvature_pair_kernel<<<(unsigned)nch, kChunkThreads, 0, st>>>(lam, lam_prev, g, g_prev, s, y, n, vec, partial,
+                                                                   plans);
+    cudaError_t e = cudaGetLastError();
+    if (e) return fail(e, "curvature_pair");
+    // totals only: every chunk is done (`full` = nch), so the finishing block just reduces them
+    ChunkStep a{};
+    a.x = s;
+    a.v = y;
+    a.dot_out = sy;
+    e = launch_maybe_pdl(chunk_finish_kernel<kDot>, 1, kFinishThreads, st, true, a, n, nch, partial, plans);
+    return e == cudaSuccess ? DM_OK : fail(e, "curvature_pair finish");
+}
 
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream) {

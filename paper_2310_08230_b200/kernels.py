@@ -187,6 +187,12 @@ def dev_lbfgs_direction(g, pairs, d):
                  launches=(2 * m + 2) * _chunk_launches(g.numel()))
 
 
+def dev_curvature_pair(lam, lam_prev, g, g_prev, s, y, sy_out):
+    """s = lam - lam_prev, y = g_prev - g, lam_prev = lam, sy_out[0] = s . y (one pass)."""
+    _native.call("dm_curvature_pair", _ptr(lam), _ptr(lam_prev), _ptr(g), _ptr(g_prev), _ptr(s), _ptr(y),
+                 lam.numel(), _ptr(sy_out), _stream(lam.device))
+
+
 def dev_axpy_host(x, gamma, y):
     _native.call("dm_axpy_host", _ptr(x), float(gamma), _ptr(y), x.numel(), _stream(x.device))
 

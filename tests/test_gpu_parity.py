@@ -151,8 +151,10 @@ def test_sweep_kernels_on_random_duals(name):
         assert st.lam.tobytes() == ost.lam.tobytes() and st.bound == ost.bound
 
 
-@pytest.mark.parametrize("n", [0, 1, 5, 7, 8, 9, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 4097, 65537, 636_800,
-                               2_000_003])
+# 3849..4095 (and totals counts in that range) are the lengths whose numpy
+# pairwise tree has 33 leaves
+@pytest.mark.parametrize("n", [0, 1, 5, 7, 8, 9, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 3849, 4095, 4096, 4097,
+                               2 * 4096 + 4000, 65537, 636_800, 2_000_003, 3849 * 4096 - 7])
 def test_pairwise_sum_and_dot_match_numpy(n):
     rng = np.random.default_rng(n)
     a = rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)
@@ -210,7 +212,7 @@ def test_lbfgs_direction_matches_dense_oracle_and_pairwise_oracle():  # test_qn.
         assert d.tobytes() == solver.lbfgs(g, pairs, solver._dot_chunked).tobytes()
 
 
-@pytest.mark.parametrize("n,m", [(1, 1), (4096, 1), (3 * 4096 + 123, 4), (100003, 10)])
+@pytest.mark.parametrize("n,m", [(1, 1), (4096, 1), (3 * 4096 + 123, 4), (100003, 10), (4095, 3), (5 * 4096 + 3900, 5)])
 def test_fused_two_loop_matches_unfused_and_oracle(n, m):
     rng = np.random.default_rng(n + m)
     history = qn.LbfgsHistory(10)
@@ -339,3 +341,21 @@ def test_solve_batch_matches_sequential_solves():
         for a, b in zip(seq, bat):
             assert a.bounds == b.bounds
             assert a.state.lam.tobytes() == b.state.lam.tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 7, 4095, 4096, 4097, 3 * 4096 + 5, 100003])
+def test_curvature_pair_matches_separate_ops(n):
+    from paper_2310_08230_b200.kernels import dev_curvature_pair
+
+    rng = np.random.default_rng(n)
+    lam, lp, g, gp = (torch.from_numpy(rng.standard_normal(n)).cuda() for _ in range(4))
+    s, y = torch.empty_like(lam), torch.empty_like(lam)
+    sy = torch.empty(1, dtype=torch.float64, device=lam.device)
+    lp_before = lp.clone()
+    dev_curvature_pair(lam, lp, g, gp, s, y, sy)
+    s_ref = lam.cpu().numpy() - lp_before.cpu().numpy()
+    y_ref = gp.cpu().numpy() - g.cpu().numpy()
+    assert s.cpu().numpy().tobytes() == s_ref.tobytes()
+    assert y.cpu().numpy().tobytes() == y_ref.tobytes()
+    assert lp.cpu().numpy().tobytes() == lam.cpu().numpy().tobytes()
+    assert float(sy[0]) == solver._dot_chunked(s_ref, y_ref)
