@@ -327,8 +327,14 @@ def run_b200(args, rank, world, local_rank):
         hbm = peaks.get("hbm_gbs", 6650.0)
         kernels = {}
         for name, k in kt.items():
-            key = "mma" if name.startswith("mma") else name
-            bpl = abytes[key]
+            if name == "step_search":
+                # one event pair around the device trial sequence: per-trial
+                # figures over the trials that ran (sweep + bound sum + decision)
+                trials = max(timer.counts.get("step_search_trials", 0), 1)
+                k = dict(k, searches=k["launches"], launches=trials, avg_ms=k["total_ms"] / trials)
+                bpl = abytes["backward_trial"]
+            else:
+                bpl = abytes["mma" if name.startswith("mma") else name]
             kernels[name] = dict(k, bytes_per_launch=bpl, achieved_gbs=bpl / (k["avg_ms"] * 1e-3) / 1e9,
                                  share_of_step=k["total_ms"] / ms)
         dom = max(kernels, key=lambda n: kernels[n]["total_ms"]) if kernels else None

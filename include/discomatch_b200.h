@@ -159,6 +159,15 @@ int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds
 /* dual.py:99-106 on lam + gamma*d (qn.py:147,153), without materialising it */
 int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, double gamma,
                         double *B, double *bounds, void *stream);
+/* qn.py:132-159 find_step_size, the whole trial sequence on the device: the
+ * trial sweeps on lam + gamma*d, their bound sums (+ free_contribution) and
+ * the reference's shrink/grow/stop decisions, enqueued without host round
+ * trips.  `state` (8 device doubles) ends as {gamma, e_init, e_best,
+ * gamma_best, e_cur, stop, trials, -}; the caller compares e_best with the
+ * current objective.  `bounds` is per-diagram scratch. */
+int dm_step_search(const dm_flat *f, const double *lam, const double *d, double gamma_prev,
+                   double free_contribution, double shrink, double grow, double min_ascent,
+                   int max_trials, double *bounds, double *state, void *stream);
 /* kernels.py:123-159 */
 int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream);
 /* kernels.py:162-270: exact (bitwise) Gauss-Seidel forward averaging pass */

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -309,7 +310,9 @@ __device__ __forceinline__ double pw_elem(const double *__restrict__ a, const do
 template <bool kDot>
 __global__ void pw_leaf_kernel(int32_t nleaves, const int64_t *__restrict__ leaf_off,
                                const int32_t *__restrict__ leaf_len, const double *__restrict__ a,
-                               const double *__restrict__ b, double *__restrict__ vals) {
+                               const double *__restrict__ b, double *__restrict__ vals,
+                               const double *__restrict__ skip = nullptr) {
+    if (skip && *skip != 0.0) return;  // device step search already stopped
     const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const int32_t k = t >> 3;
     const int q = threadIdx.x & 7;
@@ -349,16 +352,61 @@ __global__ void pw_leaf_kernel(int32_t nleaves, const int64_t *__restrict__ leaf
     vals[k] = res;
 }
 
+// Device step search (qn.py:132-159 find_step_size): state ctl =
+// {gamma, e_init, e_best, gamma_best, e_cur, stop, trials, -}; after trial
+// `trial`'s bound sum, the same comparisons and gamma updates as the host
+// loop, in double.
+struct StepParams {
+    double free_c, shrink, grow, min_ascent;
+    int32_t max_trials;
+};
+
+__device__ void step_decide(double *ctl, double sum, const StepParams &p, int trial) {
+    const double e = __dadd_rn(sum, p.free_c);  // dual_objective: bounds sum + free variables
+    ctl[6] = ctl[6] + 1.0;
+    if (trial == 0) {
+        ctl[1] = ctl[2] = ctl[4] = e;
+        ctl[3] = ctl[0];
+    } else {
+        ctl[4] = e;
+        if (e >= ctl[2]) {
+            ctl[3] = ctl[0];
+            ctl[2] = e;
+        }
+        if (__dsub_rn(e, ctl[1]) >= p.min_ascent) {
+            ctl[5] = 1.0;
+            return;
+        }
+    }
+    if (trial < p.max_trials)
+        ctl[0] = __dmul_rn(ctl[0], ctl[4] <= ctl[1] ? p.shrink : p.grow);
+    else
+        ctl[5] = 1.0;
+}
+
 __global__ void pw_combine_kernel(int32_t nleaves, int32_t maxh, const int32_t *__restrict__ height_lo,
                                   const int32_t *__restrict__ left, const int32_t *__restrict__ right,
-                                  int32_t root, double *__restrict__ vals, double *__restrict__ out) {
+                                  int32_t root, double *__restrict__ vals, double *__restrict__ out,
+                                  double *__restrict__ ctl = nullptr, StepParams prm = {}, int trial = 0) {
+    if (ctl && ctl[5] != 0.0) return;
     for (int32_t h = 1; h <= maxh; ++h) {
         const int32_t lo = height_lo[h - 1], hi = height_lo[h];
         for (int32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
             vals[nleaves + k] = __dadd_rn(vals[left[k]], vals[right[k]]);
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = __dadd_rn(0.0, vals[root]);
+    if (threadIdx.x == 0) {
+        const double res = __dadd_rn(0.0, vals[root]);
+        if (ctl)
+            step_decide(ctl, res, prm, trial);
+        else
+            out[0] = res;
+    }
+}
+
+__global__ void step_init_kernel(double *ctl, double gamma) {
+    ctl[0] = gamma;
+    for (int i = 1; i < 8; ++i) ctl[i] = 0.0;
 }
 
 // --------------------------------------------------------------------------
@@ -1187,7 +1235,7 @@ struct dm_flat {
     uint8_t *dec = nullptr;          // decisions of the last node-parallel backward pass
     const double *dec_B = nullptr;   // ... and the distance table it wrote (nullptr: none)
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
-    std::vector<int32_t> fw_pos_level, bw_pos_level, fw_pos_h, bw_pos_h;  // host copies (profiling)
+    int32_t *fw_lev = nullptr, *bw_lev = nullptr;  // levels of fw_pos / bw_pos (device)
     int mma_w = 8, mma_k = 8;
     int mma_threads = 256, mma_blocks_per_sm = 0;
     unsigned mma_sleep_ns = 0;
@@ -1197,8 +1245,6 @@ struct dm_flat {
     std::vector<int32_t> fw_layer_h, bw_layer_h;  // host copy of the lane layers (profiling, lazy upload)
     std::vector<int32_t> fw_meta_h, bw_meta_h;    // per-copy kernel lane metadata (lazy upload)
     bool classic_uploaded = false;
-    std::vector<int32_t> pp_h, pl_h;  // host visitation CSR (int32) for the lazy task packing
-    std::vector<uint8_t> flags_h;     // host first/last-layer flags
     int mma_grid_fw = 0, mma_grid_bw = 0;
     int64_t bytes = 0;
     dm::SweepDev sweep;  // interleaved layout for the full-table sweeps
@@ -1243,6 +1289,106 @@ int upload(dm_flat *f, T **dst, const T *src, int64_t n, cudaStream_t s) {
     if (n > 0 && src) DM_CUDA(cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
     return DM_OK;
 }
+
+// Host -> device staging through a small ring of pinned slots.  Copies from
+// pageable memory go through the driver's own bounce buffer one chunk at a
+// time (measured ~0.2 s for the C2 topology); here host threads fill a pinned
+// slot (converting int64 -> int32 on the way where the device layout is
+// narrower) while the copy engine drains the previous ones.  Rings are pooled
+// for the process lifetime; concurrent creates each take their own.
+constexpr size_t kStageSlotBytes = size_t(16) << 20;
+constexpr int kStageSlots = 4;
+struct StageRing {
+    int device = -1;
+    char *buf = nullptr;
+    cudaEvent_t ev[kStageSlots] = {};
+};
+std::mutex g_ring_mu;
+std::vector<StageRing *> g_rings;
+
+class Stager {
+  public:
+    Stager(int device, cudaStream_t s) : s_(s) {
+        {
+            std::lock_guard<std::mutex> lk(g_ring_mu);
+            for (size_t i = 0; i < g_rings.size(); ++i)
+                if (g_rings[i]->device == device) {
+                    ring_ = g_rings[i];
+                    g_rings.erase(g_rings.begin() + i);
+                    break;
+                }
+        }
+        if (!ring_) {
+            auto *r = new StageRing;
+            r->device = device;
+            if (cudaHostAlloc((void **)&r->buf, kStageSlotBytes * kStageSlots, cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                delete r;
+                return;
+            }
+            for (auto &e : r->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            ring_ = r;
+        }
+    }
+    ~Stager() {
+        if (!ring_) return;
+        for (auto &e : ring_->ev) cudaEventSynchronize(e);  // the slots are free again
+        std::lock_guard<std::mutex> lk(g_ring_mu);
+        g_rings.push_back(ring_);
+    }
+    // device array of n elements of T; element i is produced by
+    // fill(T *dst, int64_t first, int64_t count) writing elements
+    // [first, first + count) to dst (run on up to 4 threads per slot)
+    template <typename T, typename Fill>
+    int put(dm_flat *f, T **dst, int64_t n, Fill &&fill) {
+        int rc = upload(f, dst, (const T *)nullptr, n, s_);
+        if (rc) return rc;
+        if (!ring_) {  // no pinned memory: fill a pageable buffer and copy from it
+            std::vector<T> tmp(std::max<int64_t>(n, 0));
+            if (n > 0) {
+                fill(tmp.data(), 0, n);
+                DM_CUDA(cudaMemcpyAsync(*dst, tmp.data(), n * sizeof(T), cudaMemcpyHostToDevice, s_));
+                DM_CUDA(cudaStreamSynchronize(s_));
+            }
+            return DM_OK;
+        }
+        const int64_t per = (int64_t)(kStageSlotBytes / sizeof(T));
+        for (int64_t lo = 0; lo < n; lo += per) {
+            const int64_t cnt = std::min(per, n - lo);
+            const int slot = next_++ % kStageSlots;
+            DM_CUDA(cudaEventSynchronize(ring_->ev[slot]));
+            T *buf = (T *)(ring_->buf + slot * kStageSlotBytes);
+            const int nt = cnt * (int64_t)sizeof(T) >= (int64_t(1) << 20) ? 4 : 1;
+            if (nt == 1) {
+                fill(buf, lo, cnt);
+            } else {
+                std::thread th[4];
+                for (int t = 0; t < nt; ++t) {
+                    const int64_t a = cnt * t / nt, b = cnt * (t + 1) / nt;
+                    th[t] = std::thread([&, a, b] { fill(buf + a, lo + a, b - a); });
+                }
+                for (int t = 0; t < nt; ++t) th[t].join();
+            }
+            DM_CUDA(cudaMemcpyAsync(*dst + lo, buf, cnt * sizeof(T), cudaMemcpyHostToDevice, s_));
+            DM_CUDA(cudaEventRecord(ring_->ev[slot], s_));
+        }
+        return DM_OK;
+    }
+    template <typename T>
+    int copy(dm_flat *f, T **dst, const T *src, int64_t n) {
+        return put(f, dst, n, [src](T *d, int64_t lo, int64_t c) { std::memcpy(d, src + lo, c * sizeof(T)); });
+    }
+    int narrow(dm_flat *f, int32_t **dst, const int64_t *src, int64_t n) {
+        return put(f, dst, n, [src](int32_t *d, int64_t lo, int64_t c) {
+            for (int64_t i = 0; i < c; ++i) d[i] = (int32_t)src[lo + i];
+        });
+    }
+
+  private:
+    cudaStream_t s_;
+    StageRing *ring_ = nullptr;
+    int next_ = 0;
+};
 
 // Pairwise plans are cached per (device, length, stream) for the process
 // lifetime: a plan's value scratch belongs to one stream, so instances solved
@@ -1347,9 +1493,21 @@ int mma_grid_for(const dm_flat *f, bool forward, int threads, int want_per_sm, i
 // those kernels are selected (the node-parallel ones need only positions).
 static int ensure_per_copy_schedules(dm_flat *f, cudaStream_t s) {
     if (f->classic_uploaded) return DM_OK;
+    const int64_t n = f->np_fw_tasks;
+    std::vector<int32_t> fpos(n), flev(n), bpos(n), blev(n);
+    std::vector<uint8_t> flags(f->L);
+    std::vector<int32_t> pp(f->P + 1), pl(f->L);
+    DM_CUDA(cudaStreamSynchronize(s));
+    DM_CUDA(cudaMemcpy(pp.data(), f->proc_ptr, pp.size() * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(pl.data(), f->proc_layers, pl.size() * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(fpos.data(), f->fw_pos, n * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(flev.data(), f->fw_lev, n * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(bpos.data(), f->bw_pos, n * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(blev.data(), f->bw_lev, n * 4, cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(flags.data(), f->layer_flags, f->L, cudaMemcpyDeviceToHost));
     dm::MmaSchedule fw, bw;
-    dm::pack_mma_tasks(f->fw_pos_h, f->fw_pos_level, f->pp_h.data(), f->pl_h.data(), f->flags_h.data(), fw);
-    dm::pack_mma_tasks(f->bw_pos_h, f->bw_pos_level, f->pp_h.data(), f->pl_h.data(), f->flags_h.data(), bw);
+    dm::pack_mma_tasks(fpos, flev, pp.data(), pl.data(), flags.data(), fw);
+    dm::pack_mma_tasks(bpos, blev, pp.data(), pl.data(), flags.data(), bw);
     f->fw_tasks = fw.tasks;
     f->bw_tasks = bw.tasks;
     int rc;
@@ -1432,7 +1590,12 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         dm::set_error("inconsistent flat table offsets");
         return DM_ERR_INVALID;
     }
-    std::vector<int32_t> layer_bdd(L), var_count, pos_var(P, -1);
+    dm::I32Buffer layer_bdd, pos_var;  // every element written below
+    layer_bdd.resize(L);
+    pos_var.resize(P);
+    if (env_int("DM_VERBOSE", 0) >= 2)
+        std::fprintf(stderr, "  [dm_flat_create] buffers %.4f\n", host_seconds() - t_begin);
+    std::vector<int32_t> var_count;
     int64_t max_width = 0, max_degree = 0;
     {
         // diagram ranges validated in parallel; the first failing range reports
@@ -1444,6 +1607,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         for (int t = 0; t < kThreads; ++t)
             th.emplace_back([&, t] {
                 const int64_t jlo = nb * t / kThreads, jhi = nb * (t + 1) / kThreads;
+                int64_t wmax = 0;  // thread-local (widths[] would false-share)
                 for (int64_t j = jlo; j < jhi; ++j) {
                     if (bl[j + 1] <= bl[j] || lnl[bl[j] + 1] - lnl[bl[j]] != 1) {
                         codes[t] = DM_ERR_INVALID;
@@ -1458,19 +1622,10 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
                             msgs[t] = "empty layer";
                             return;
                         }
-                        widths[t] = std::max(widths[t], w);
-                        const bool last = l + 1 == bl[j + 1];
-                        for (int64_t v = lnl[l]; v < lnl[l + 1]; ++v)
-                            for (int64_t tt : {desc->zero_t[v], desc->one_t[v]}) {
-                                if (last ? (tt >= 0 || tt < -2)
-                                         : (tt == -2 || tt < -2 || (tt >= 0 && (tt < lnl[l + 1] || tt >= lnl[l + 2])))) {
-                                    codes[t] = DM_ERR_UNSUPPORTED;
-                                    msgs[t] = "arc targets must reach the next layer (or a terminal from the last layer)";
-                                    return;
-                                }
-                            }
+                        wmax = std::max(wmax, w);
                     }
                 }
+                widths[t] = wmax;
             });
         for (auto &x : th) x.join();
         for (int t = 0; t < kThreads; ++t) {
@@ -1485,128 +1640,84 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         dm::set_error("layers wider than 32 nodes are not supported by the exact averaging kernels");
         return DM_ERR_UNSUPPORTED;
     }
+    const bool vb2v = env_int("DM_VERBOSE", 0) >= 2;
+    if (vb2v) std::fprintf(stderr, "  [dm_flat_create] diagrams checked %.4f\n", host_seconds() - t_begin);
+    // variable range, then the visitation CSR (degrees, position -> variable)
+    // in parallel; the first failing range reports
+    constexpr int kVThreads = 8;
+    auto par = [&](int64_t n, auto &&fn) {
+        std::vector<std::thread> th;
+        for (int t = 0; t < kVThreads; ++t) th.emplace_back([&, t] { fn(t, n * t / kVThreads, n * (t + 1) / kVThreads); });
+        for (auto &x : th) x.join();
+    };
+    int64_t vmax[kVThreads], dmax[kVThreads] = {0}, nval[kVThreads] = {0};
+    const char *vmsg[kVThreads] = {nullptr};
+    par(L, [&](int t, int64_t lo, int64_t hi) {
+        int64_t m = -1;
+        for (int64_t l = lo; l < hi; ++l) m = std::max(m, desc->layer_var[l]);
+        vmax[t] = m;
+    });
     int64_t max_var = -1;
-    for (int64_t l = 0; l < L; ++l) max_var = std::max(max_var, desc->layer_var[l]);
+    for (int t = 0; t < kVThreads; ++t) max_var = std::max(max_var, vmax[t]);
     const int64_t V = std::max<int64_t>(max_var + 1, P);
     var_count.assign(V, 0);
-    for (int64_t p = 0; p < P; ++p) {
-        const int64_t lo = desc->proc_ptr[p], hi = desc->proc_ptr[p + 1];
-        max_degree = std::max(max_degree, hi - lo);
-        if (hi > lo) {
-            const int64_t v = desc->layer_var[desc->proc_layers[lo]];
-            pos_var[p] = (int32_t)v;
-            var_count[v] = (int32_t)(hi - lo);
+    if (vb2v) std::fprintf(stderr, "  [dm_flat_create] variables ranged %.4f\n", host_seconds() - t_begin);
+    par(P, [&](int t, int64_t plo, int64_t phi) {
+        int64_t dm_ = 0, nv_ = 0;  // thread-local (the shared arrays would false-share)
+        struct Flush {
+            int64_t &a, &b, &da, &nb;
+            ~Flush() { da = a, nb = b; }
+        } flush{dm_, nv_, dmax[t], nval[t]};
+        for (int64_t p = plo; p < phi; ++p) {
+            const int64_t lo = desc->proc_ptr[p], hi = desc->proc_ptr[p + 1];
+            if (hi < lo || hi > L) {
+                vmsg[t] = "visitation offsets must be non-decreasing and within the layers";
+                return;
+            }
+            if (hi - lo > 32) {
+                vmsg[t] = "exact averaging pass supports at most 32 diagrams per variable";
+                return;
+            }
+            dm_ = std::max(dm_, hi - lo);
+            for (int64_t q = lo; q < hi; ++q)
+                if (desc->proc_layers[q] < 0 || desc->proc_layers[q] >= L) {
+                    vmsg[t] = "visited layer out of range";
+                    return;
+                }
+            if (hi > lo) {
+                ++nv_;
+                const int64_t v = desc->layer_var[desc->proc_layers[lo]];
+                if (v < 0) {
+                    vmsg[t] = "negative variable id";
+                    return;
+                }
+                pos_var[p] = (int32_t)v;
+                var_count[v] = (int32_t)(hi - lo);
+            } else {
+                pos_var[p] = -1;
+            }
         }
+    });
+    int64_t nvalid = 0;  // positions with copies (= exact-pass tasks of the node-parallel kernels)
+    for (int t = 0; t < kVThreads; ++t) {
+        if (vmsg[t]) {
+            dm::set_error(vmsg[t]);
+            return std::strstr(vmsg[t], "at most 32") ? DM_ERR_UNSUPPORTED : DM_ERR_INVALID;
+        }
+        max_degree = std::max(max_degree, dmax[t]);
+        nvalid += nval[t];
     }
     const double t_valid = host_seconds();
-    // Independent host plans and conversions run concurrently: the two pass
-    // schedules, the sweep layout, the forward publish descriptors, the
-    // node-parallel copy records and the int32 topology.
+    // Every plan is built on the device (dm_plan.cu) while the host stages
+    // the topology: the exact-pass schedules and copy records on one stream
+    // once the visitation CSR is there, the sweep layout on another (its
+    // sizes are read back on a host thread), its fill and the forward
+    // publish descriptors once the arc targets are there.
     const bool want_np = max_width <= 8 && max_degree <= 8;
-    dm::MmaSchedule fw, bw;
-    dm::SweepLayout sl;
-    std::vector<uint64_t> relax;
-    bool relax_ok = false;
-    int rc_fw = DM_OK, rc_bw = DM_OK, rc_sl = DM_OK;
-    std::string err_fw, err_bw, err_sl;
-    std::vector<int32_t> zero32(N), one32(N), lnl32, var32, pp32, pl32, bl32;
-    double plan_s[5] = {0, 0, 0, 0, 0};  // fw, bw schedules, sweep layout, relax, records
-    std::vector<uint8_t> flags;
-    std::vector<int4> rec;
-    // plan threads keep running while the topology is converted and uploaded
-    std::vector<std::thread> th;
-    struct Joiner {
-        std::vector<std::thread> &t;
-        ~Joiner() {
-            for (auto &x : t)
-                if (x.joinable()) x.join();
-        }
-    } joiner{th};
-    {
-        auto i32 = [](const int64_t *src, int64_t n) {
-            std::vector<int32_t> v(n);
-            for (int64_t i = 0; i < n; ++i) v[i] = (int32_t)src[i];
-            return v;
-        };
-        th.emplace_back([&] {
-            const double t0 = host_seconds();
-            rc_fw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
-                                           true, fw);
-            if (rc_fw) err_fw = dm_last_error();
-            plan_s[0] = host_seconds() - t0;
-        });
-        th.emplace_back([&] {
-            const double t0 = host_seconds();
-            rc_bw = dm::build_mma_schedule(bl, nb, nullptr, desc->layer_var, L, desc->proc_ptr, desc->proc_layers, P,
-                                           false, bw);
-            if (rc_bw) err_bw = dm_last_error();
-            plan_s[1] = host_seconds() - t0;
-        });
-        th.emplace_back([&] {
-            const double t0 = host_seconds();
-            rc_sl = dm::build_sweep_layout(bl, nb, lnl, desc->zero_t, desc->one_t, sl);
-            if (rc_sl) err_sl = dm_last_error();
-            plan_s[2] = host_seconds() - t0;
-        });
-        th.emplace_back([&] {
-            const double t0 = host_seconds();
-            relax_ok = max_width <= 8 && dm::build_relax_by_layer(bl, nb, lnl, desc->zero_t, desc->one_t, relax);
-            plan_s[3] = host_seconds() - t0;
-        });
-        std::vector<std::thread> conv;
-        const int nconv = 4;
-        for (int t = 0; t < nconv; ++t)
-            conv.emplace_back([&, t] {
-                const int64_t lo = N * t / nconv, hi = N * (t + 1) / nconv;
-                for (int64_t i = lo; i < hi; ++i) {
-                    zero32[i] = (int32_t)desc->zero_t[i];
-                    one32[i] = (int32_t)desc->one_t[i];
-                }
-            });
-        conv.emplace_back([&] { bl32 = i32(bl, nb + 1); });
-        conv.emplace_back([&] { lnl32 = i32(lnl, L + 1); });
-        conv.emplace_back([&] { var32 = i32(desc->layer_var, L); });
-        conv.emplace_back([&] { pp32 = i32(desc->proc_ptr, P + 1); });
-        conv.emplace_back([&] { pl32 = i32(desc->proc_layers, L); });
-        for (auto &t : conv) t.join();
-        th.emplace_back([&] {
-                const double t0 = host_seconds();
-                struct Stamp {
-                    double t0, &out;
-                    ~Stamp() { out = host_seconds() - t0; }
-                } stamp{t0, plan_s[4]};
-                flags.assign(L, 0);
-                for (int64_t j = 0; j < nb; ++j) {
-                    flags[bl[j]] |= 1;
-                    flags[bl[j + 1] - 1] |= 2;
-                }
-                if (!want_np) return;
-                rec.resize((size_t)P * 8);
-                constexpr int kRecThreads = 6;
-                std::vector<std::thread> rt;
-                for (int t = 0; t < kRecThreads; ++t)
-                    rt.emplace_back([&, t] {
-                        const int64_t plo = P * t / kRecThreads, phi = P * (t + 1) / kRecThreads;
-                        for (int64_t p = plo; p < phi; ++p) {
-                            const int64_t lo = desc->proc_ptr[p], k = desc->proc_ptr[p + 1] - lo;
-                            for (int c = 0; c < 8; ++c) {
-                                int4 r{-1, 0, (int)((unsigned)k << 24), 0};
-                                if (c < k) {
-                                    const int64_t l = desc->proc_layers[lo + c];
-                                    const int64_t w = lnl[l + 1] - lnl[l];
-                                    const int64_t wn = (flags[l] & 2) ? 0 : lnl[l + 2] - lnl[l + 1];
-                                    r.x = (int)l;
-                                    r.y = (int)lnl[l];
-                                    r.z = (int)((unsigned)w | ((unsigned)wn << 8) | ((unsigned)flags[l] << 16) |
-                                                ((unsigned)k << 24));
-                                }
-                                rec[(size_t)p * 8 + c] = r;
-                            }
-                        }
-                    });
-                for (auto &x : rt) x.join();
-            });
-    }
+    const bool vb2 = env_int("DM_VERBOSE", 0) >= 2;
+    auto mark = [&](const char *what) {
+        if (vb2) std::fprintf(stderr, "  [dm_flat_create] %s %.4f\n", what, host_seconds() - t_begin);
+    };
     int rc = DM_OK;
     DM_CUDA(cudaSetDevice(device));
     keep_pool_memory(device);
@@ -1622,90 +1733,161 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     auto up = [&](int32_t **dst, const std::vector<int32_t> &v) {
         return upload(f.get(), dst, v.data(), (int64_t)v.size(), s);
     };
-    if ((rc = up(&f->bdd_layer_lo, bl32))) return rc;
-    if ((rc = up(&f->lnl, lnl32))) return rc;
-    if ((rc = up(&f->layer_var, var32))) return rc;
-    if ((rc = up(&f->zero_t, zero32))) return rc;
-    if ((rc = up(&f->one_t, one32))) return rc;
-    if ((rc = up(&f->proc_ptr, pp32))) return rc;
-    if ((rc = up(&f->proc_layers, pl32))) return rc;
-    if ((rc = up(&f->layer_bdd, layer_bdd))) return rc;
-    if ((rc = up(&f->pos_var, pos_var))) return rc;
-    if ((rc = up(&f->var_count, var_count))) return rc;
+    auto alloc = [&](auto **dst, int64_t n) {
+        using T = std::remove_reference_t<decltype(**dst)>;
+        return upload(f.get(), dst, (const T *)nullptr, n, s);
+    };
+    mark("validated");
+    Stager stage(device, s);
+    mark("stager");
+    if ((rc = stage.narrow(f.get(), &f->bdd_layer_lo, bl, nb + 1))) return rc;
+    if ((rc = stage.narrow(f.get(), &f->lnl, lnl, L + 1))) return rc;
+    if ((rc = stage.narrow(f.get(), &f->proc_ptr, desc->proc_ptr, P + 1))) return rc;
+    if ((rc = stage.narrow(f.get(), &f->proc_layers, desc->proc_layers, L))) return rc;
+    if ((rc = stage.copy(f.get(), &f->layer_bdd, layer_bdd.data(), L))) return rc;
+    mark("csr staged");
+    int *plan_words = nullptr;
+    if ((rc = alloc(&f->layer_flags, L))) return rc;
+    if ((rc = alloc(&f->fw_pos, P))) return rc;
+    if ((rc = alloc(&f->bw_pos, P))) return rc;
+    if ((rc = alloc(&f->fw_lev, P))) return rc;
+    if ((rc = alloc(&f->bw_lev, P))) return rc;
+    if ((rc = alloc(&plan_words, 8))) return rc;
+    if (want_np && (rc = alloc(&f->np_rec, P * 8))) return rc;
+    // device plans on their own stream, after the CSR upload
+    unsigned long long *relax_fail = nullptr;
+    if ((rc = alloc(&relax_fail, 1))) return rc;
+    // written by the sweep-layout thread: declared before `ps`, whose
+    // destructor joins that thread on every return path
+    std::vector<void *> sweep_allocs;
+    int64_t sweep_bytes = 0;
+    int rc_sl = DM_OK;
+    std::string err_sl;
+    double t_sweep = 0;
+    struct PlanStreams {
+        cudaStream_t s = nullptr, ss = nullptr;
+        cudaEvent_t ready = nullptr, done = nullptr, zo_ready = nullptr, ss_done = nullptr;
+        std::thread th;
+        ~PlanStreams() {
+            if (th.joinable()) th.join();
+            for (cudaStream_t x : {s, ss})
+                if (x) cudaStreamSynchronize(x), cudaStreamDestroy(x);
+            for (cudaEvent_t e : {ready, done, zo_ready, ss_done})
+                if (e) cudaEventDestroy(e);
+        }
+    } ps;
+    DM_CUDA(cudaStreamCreateWithFlags(&ps.s, cudaStreamNonBlocking));
+    DM_CUDA(cudaStreamCreateWithFlags(&ps.ss, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&ps.ready, &ps.done, &ps.zo_ready, &ps.ss_done})
+        DM_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    DM_CUDA(cudaMemsetAsync(relax_fail, 0, sizeof(unsigned long long), s));
+    DM_CUDA(cudaEventRecord(ps.ready, s));
+    DM_CUDA(cudaStreamWaitEvent(ps.s, ps.ready, 0));
+    DM_CUDA(cudaStreamWaitEvent(ps.ss, ps.ready, 0));
+    // sweep layout sizes on a host thread (two small read-backs)
+    ps.th = std::thread([&] {
+        const double t0 = host_seconds();
+        cudaSetDevice(device);
+        rc_sl = dm::device_sweep_layout(f->bdd_layer_lo, f->lnl, nb, f->sweep, sweep_allocs, sweep_bytes, ps.ss);
+        if (rc_sl) err_sl = dm_last_error();
+        t_sweep = host_seconds() - t0;
+    });
+    if (dm::device_layer_flags(f->layer_bdd, f->bdd_layer_lo, L, f->layer_flags, ps.s)) return DM_ERR_CUDA;
+    if (dm::device_level_orders(f->proc_ptr, f->proc_layers, f->layer_bdd, f->bdd_layer_lo, P, L, nvalid, f->fw_pos,
+                                f->fw_lev, f->bw_pos, f->bw_lev, plan_words, ps.s))
+        return DM_ERR_CUDA;
+    if (want_np && dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, P, f->np_rec, ps.s))
+        return DM_ERR_CUDA;
+    DM_CUDA(cudaEventRecord(ps.done, ps.s));
+    mark("plans queued");
+    if ((rc = stage.narrow(f.get(), &f->layer_var, desc->layer_var, L))) return rc;
+    // arc targets: narrowed and range-checked in the same pass (they must
+    // reach the next layer, or a terminal from a last layer)
+    std::atomic<bool> bad_arc{false};
+    auto narrow_arcs = [&](int32_t **dst, const int64_t *src) {
+        return stage.put(f.get(), dst, N, [&, src](int32_t *d, int64_t lo, int64_t c) {
+            int64_t l = std::upper_bound(lnl, lnl + L + 1, lo) - lnl - 1;
+            bool bad = false;
+            for (int64_t i = 0; i < c; ++i) {
+                const int64_t v = lo + i;
+                while (v >= lnl[l + 1]) ++l;
+                const int64_t tt = src[v];
+                const bool last = l + 1 == bl[layer_bdd[l] + 1];
+                bad |= last ? (tt >= 0 || tt < -2) : (tt < -2 || tt == -2 || (tt >= 0 && (tt < lnl[l + 1] || tt >= lnl[l + 2])));
+                d[i] = (int32_t)tt;
+            }
+            if (bad) bad_arc = true;
+        });
+    };
+    if ((rc = narrow_arcs(&f->zero_t, desc->zero_t))) return rc;
+    if ((rc = narrow_arcs(&f->one_t, desc->one_t))) return rc;
+    if (bad_arc) {
+        dm::set_error("arc targets must reach the next layer (or a terminal from the last layer)");
+        return DM_ERR_UNSUPPORTED;
+    }
+    if ((rc = stage.copy(f.get(), &f->pos_var, pos_var.data(), P))) return rc;
+    if ((rc = stage.copy(f.get(), &f->var_count, var_count.data(), (int64_t)var_count.size()))) return rc;
     const std::vector<int32_t> progress_init{-1, 0}, status_init{0};
     if ((rc = up(&f->progress, progress_init))) return rc;  // progress hint, task queue
     if ((rc = up(&f->status, status_init))) return rc;
-    for (auto &t : th) t.join();  // host plans (overlapped with the topology upload)
-    if (rc_fw) { dm::set_error(err_fw); return rc_fw; }
-    if (rc_bw) { dm::set_error(err_bw); return rc_bw; }
-    if (rc_sl) { dm::set_error(err_sl); return rc_sl; }
+    mark("topology staged");
+    ps.th.join();
+    mark("sweep sizes joined");
+    f->allocs.insert(f->allocs.end(), sweep_allocs.begin(), sweep_allocs.end());
+    f->bytes += sweep_bytes;
+    if (rc_sl) {
+        dm::set_error(err_sl);
+        return rc_sl == -2 ? DM_ERR_UNSUPPORTED : DM_ERR_CUDA;
+    }
     const double t_plans = host_seconds();
-    f->fw_depth = fw.depth;
-    f->bw_depth = bw.depth;
-    f->fw_tasks = fw.tasks;
-    f->bw_tasks = bw.tasks;
-    if (relax_ok) {
-        if ((rc = upload(f.get(), &f->relax_layer, relax.data(), L, s))) return rc;
-        f->relax_ok = true;
+    // arc targets staged: sweep fill and publish descriptors
+    DM_CUDA(cudaEventRecord(ps.zo_ready, s));
+    DM_CUDA(cudaStreamWaitEvent(ps.ss, ps.zo_ready, 0));
+    if (dm::device_sweep_fill(f->sweep, f->zero_t, f->one_t, ps.ss)) return DM_ERR_CUDA;
+    const bool want_relax = max_width <= 8;
+    if (want_relax) {
+        if ((rc = alloc(&f->relax_layer, L))) return rc;
+        DM_CUDA(cudaEventRecord(ps.zo_ready, s));  // the allocation is ordered on s
+        DM_CUDA(cudaStreamWaitEvent(ps.ss, ps.zo_ready, 0));
+        if (dm::device_relax(f->layer_bdd, f->bdd_layer_lo, f->lnl, f->zero_t, f->one_t, L, f->relax_layer,
+                             relax_fail, ps.ss))
+            return DM_ERR_CUDA;
     }
-    {
-        int32_t *gb, *gn, *pw, *zl, *ol;
-        int64_t *gp, *ps;
-        if ((rc = up(&gb, sl.grp_bdd))) return rc;
-        if ((rc = up(&gn, sl.grp_npos))) return rc;
-        if ((rc = up(&pw, sl.pos_width))) return rc;
-        if ((rc = upload(f.get(), &zl, sl.zl.data(), (int64_t)sl.zl.size(), s))) return rc;
-        if ((rc = upload(f.get(), &ol, sl.ol.data(), (int64_t)sl.ol.size(), s))) return rc;
-        if ((rc = upload(f.get(), &gp, sl.grp_pos_lo.data(), (int64_t)sl.grp_pos_lo.size(), s))) return rc;
-        if ((rc = upload(f.get(), &ps, sl.pos_slot.data(), (int64_t)sl.pos_slot.size(), s))) return rc;
-        f->sweep.groups = sl.groups;
-        f->sweep.max_width = (int32_t)sl.max_width;
-        f->sweep.grp_bdd = gb;
-        f->sweep.grp_npos = gn;
-        f->sweep.pos_width = pw;
-        f->sweep.grp_pos_lo = gp;
-        f->sweep.pos_slot = ps;
-        f->sweep.zl = zl;
-        f->sweep.ol = ol;
-        f->sweep.bdd_layer_lo = f->bdd_layer_lo;
-        f->sweep.lnl = f->lnl;
-    }
+    DM_CUDA(cudaEventRecord(ps.ss_done, ps.ss));
     f->mma_w = max_width <= 8 ? 8 : (max_width <= 16 ? 16 : 32);
     f->mma_k = max_degree <= 8 ? 8 : 32;
-    if (want_np) {
-        if ((rc = upload(f.get(), &f->layer_flags, flags.data(), L, s))) return rc;
-        if ((rc = upload(f.get(), &f->np_rec, rec.data(), (int64_t)rec.size(), s))) return rc;
-        if ((rc = up(&f->fw_pos, fw.pos_order))) return rc;
-        if ((rc = up(&f->bw_pos, bw.pos_order))) return rc;
-        f->np_fw_tasks = (int64_t)fw.pos_order.size();
-        f->np_bw_tasks = (int64_t)bw.pos_order.size();
-        f->np_ok = true;
-    }
+    f->np_fw_tasks = f->np_bw_tasks = nvalid;
+    f->np_ok = want_np;
+    DevPlan *dummy;
+    if ((rc = get_plan(nb, s, &dummy))) return rc;
+    if ((rc = get_plan(L, s, &dummy))) return rc;
+    DM_CUDA(cudaStreamWaitEvent(s, ps.done, 0));
+    DM_CUDA(cudaStreamWaitEvent(s, ps.ss_done, 0));
+    mark("tail queued");
+    DM_CUDA(cudaStreamSynchronize(s));  // the host staging vectors die with this scope
+    mark("synchronised");
+    int words[8];
+    unsigned long long rfail = 1;
+    DM_CUDA(cudaMemcpy(words, plan_words, sizeof(words), cudaMemcpyDeviceToHost));
+    DM_CUDA(cudaMemcpy(&rfail, relax_fail, sizeof(rfail), cudaMemcpyDeviceToHost));
+    f->relax_ok = want_relax && rfail == 0;
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 3),
                        (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
                        env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16) |
                            ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17) | ((env_int("DM_MMA_NP", 1) ? 0 : 1) << 18));
     if (rc) return rc;
-    DevPlan *dummy;
-    if ((rc = get_plan(nb, s, &dummy))) return rc;
-    if ((rc = get_plan(L, s, &dummy))) return rc;
-    DM_CUDA(cudaStreamSynchronize(s));  // the host staging vectors die with this scope
-    // kept on the host: level order of the positions (profiling) and what the
-    // per-copy kernels' task packing needs if they are selected later
-    f->fw_pos_level = std::move(fw.pos_order_level);
-    f->bw_pos_level = std::move(bw.pos_order_level);
-    f->fw_pos_h = std::move(fw.pos_order);
-    f->bw_pos_h = std::move(bw.pos_order);
-    f->pp_h = std::move(pp32);
-    f->pl_h = std::move(pl32);
-    f->flags_h = std::move(flags);
+    if (words[1] || words[3]) {
+        dm::set_error("device schedule: level walk stalled (watchdog)");
+        return DM_ERR_CUDA;
+    }
+    f->fw_depth = nvalid ? words[4] + 1 : 0;
+    f->bw_depth = nvalid ? words[5] + 1 : 0;
     if (!f->mma_np && (rc = ensure_per_copy_schedules(f.get(), s))) return rc;
     if (env_int("DM_VERBOSE", 0))
         std::fprintf(stderr,
-                     "[dm_flat_create] validate %.3fs, topology upload + plans %.3fs, plan upload %.3fs "
-                     "(plans: fw %.3f bw %.3f sweep %.3f relax %.3f records %.3f)\n",
-                     t_valid - t_begin, t_plans - t_valid, host_seconds() - t_plans, plan_s[0], plan_s[1], plan_s[2],
-                     plan_s[3], plan_s[4]);
+                     "[dm_flat_create] validate %.3fs, topology staging + device plans %.3fs, plan tail %.3fs "
+                     "(sweep layout sizes %.3f)\n",
+                     t_valid - t_begin, t_plans - t_valid, host_seconds() - t_plans, t_sweep);
     *out = f.release();
     return DM_OK;
 }
@@ -1759,10 +1941,12 @@ int dm_flat_task_levels(const dm_flat *f, int forward, int32_t *levels, int32_t 
         return DM_ERR_INVALID;
     }
     if (f->mma_np) {  // one task per position, 8 copy slots per task
-        const auto &v = forward ? f->fw_pos_level : f->bw_pos_level;
-        const auto &pos = forward ? f->fw_pos_h : f->bw_pos_h;
-        if (levels) std::memcpy(levels, v.data(), v.size() * sizeof(int32_t));
+        const int64_t n = f->np_fw_tasks;
+        DM_CUDA(cudaDeviceSynchronize());
+        if (levels) DM_CUDA(cudaMemcpy(levels, forward ? f->fw_lev : f->bw_lev, n * 4, cudaMemcpyDeviceToHost));
         if (lane_layers) {
+            std::vector<int32_t> pos(n);
+            DM_CUDA(cudaMemcpy(pos.data(), forward ? f->fw_pos : f->bw_pos, n * 4, cudaMemcpyDeviceToHost));
             std::vector<int32_t> pp(f->P + 1), pl(f->L);
             DM_CUDA(cudaMemcpy(pp.data(), f->proc_ptr, pp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
             DM_CUDA(cudaMemcpy(pl.data(), f->proc_layers, pl.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -1821,6 +2005,35 @@ int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, do
     DM_CHECK_FLAT(f);
     if (f->nb == 0) return DM_OK;
     return dm::sweep_backward(f->sweep, lam, d, gamma, B, bounds, stream);
+}
+
+int dm_step_search(const dm_flat *f, const double *lam, const double *d, double gamma_prev, double free_contribution,
+                   double shrink, double grow, double min_ascent, int max_trials, double *bounds, double *state,
+                   void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!lam || !d || !bounds || !state || max_trials < 0) {
+        dm::set_error("invalid step search arguments");
+        return DM_ERR_INVALID;
+    }
+    if (f->nb == 0) {
+        dm::set_error("step search needs at least one diagram");
+        return DM_ERR_INVALID;
+    }
+    const cudaStream_t s = (cudaStream_t)stream;
+    DevPlan *p;
+    int rc = get_plan(f->nb, s, &p);
+    if (rc) return rc;
+    const StepParams prm{free_contribution, shrink, grow, min_ascent, max_trials};
+    step_init_kernel<<<1, 1, 0, s>>>(state, gamma_prev);
+    // every trial is enqueued up front; the ones after the stop return at once
+    for (int t = 0; t <= max_trials; ++t) {
+        if ((rc = dm::sweep_backward(f->sweep, lam, d, 0.0, nullptr, bounds, stream, state))) return rc;
+        pw_leaf_kernel<false><<<blocks_for((int64_t)p->nleaves * 8, 256), 256, 0, s>>>(
+            p->nleaves, p->leaf_off, p->leaf_len, bounds, nullptr, p->vals, state + 5);
+        pw_combine_kernel<<<1, 1024, 0, s>>>(p->nleaves, p->maxh, p->height_lo, p->left, p->right, p->root, p->vals,
+                                             nullptr, state, prm, t);
+    }
+    return check_stream_error("step search");
 }
 
 int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream) {

@@ -74,6 +74,21 @@ void pack_mma_tasks(const std::vector<int32_t> &pos_order, const std::vector<int
                     const int32_t *proc_ptr, const int32_t *proc_layers, const uint8_t *layer_flags,
                     MmaSchedule &s);
 
+// The same level orders built on the device (dm_plan.cu), stream-ordered:
+// positions with copies sorted by (level, visitation index) into the first
+// `nvalid` entries of fw/bw_order, their levels into fw/bw_level (P each);
+// words (8 device ints) = {fw queue, fw status, bw queue, bw status,
+// fw depth - 1, bw depth - 1}.  Device topology is int32.
+int device_level_orders(const int32_t *proc_ptr, const int32_t *proc_layers, const int32_t *layer_bdd,
+                        const int32_t *bdd_layer_lo, int64_t P, int64_t L, int64_t nvalid, int32_t *fw_order,
+                        int32_t *fw_level, int32_t *bw_order, int32_t *bw_level, int *words, void *stream);
+// first/last-layer flags (bit 0/1) per layer
+int device_layer_flags(const int32_t *layer_bdd, const int32_t *bdd_layer_lo, int64_t L, uint8_t *flags,
+                       void *stream);
+// node-parallel copy records (int4 per position and copy slot, 8 slots)
+int device_np_records(const int32_t *proc_ptr, const int32_t *proc_layers, const int32_t *lnl, const uint8_t *flags,
+                      int64_t P, void *rec, void *stream);
+
 // Uninitialised int32 buffer (every element of the sweep targets is written
 // by the parallel fill, so a value-initialising std::vector would only add a
 // serial pass over hundreds of MB).
@@ -122,9 +137,21 @@ struct SweepDev {
     const int32_t *zl = nullptr, *ol = nullptr;
     const int32_t *bdd_layer_lo = nullptr, *lnl = nullptr;
 };
+// The interleaved layout built on the device (dm_plan.cu): sizes, groups,
+// widths and slot offsets into `sd` (device pointers registered in
+// allocs/bytes; synchronises `stream` twice for the sizes; 0, -1 CUDA error,
+// -2 too large), then device_sweep_fill writes the arc targets.
+int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, SweepDev &sd, std::vector<void *> &allocs,
+                        int64_t &bytes, void *stream);
+int device_sweep_fill(const SweepDev &sd, const int32_t *zero_t, const int32_t *one_t, void *stream);
+// forward publish descriptors on the device; *fail != 0 afterwards: unusable
+int device_relax(const int32_t *layer_bdd, const int32_t *bl, const int32_t *lnl, const int32_t *zero_t,
+                 const int32_t *one_t, int64_t L, uint64_t *desc, unsigned long long *fail, void *stream);
 // kernels.py:95-120 (B may be null: trial evaluation, bounds only; d null: plain duals)
+// ctl (device step search, dm_step_search): gamma read from ctl[0], the
+// launch returns at once when ctl[5] (stop) is set.
 int sweep_backward(const SweepDev &s, const double *lam, const double *d, double gamma, double *B,
-                   double *bounds, void *stream);
+                   double *bounds, void *stream, const double *ctl = nullptr);
 // kernels.py:123-159
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream);
 // Chunked inner product (dm_sweep.cu): partial[nchunks] scratch, counter a

@@ -27,8 +27,13 @@ template <int W, bool kTrial, bool kStore>
 __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::SweepDev s, const double *__restrict__ lam,
                                                                         const double *__restrict__ d, double gamma,
                                                                         double *__restrict__ B,
-                                                                        double *__restrict__ bounds) {
+                                                                        double *__restrict__ bounds,
+                                                                        const double *__restrict__ ctl) {
     extern __shared__ double sm[];
+    if (kTrial && ctl) {  // device step search: ctl = dm_step_search state
+        if (ctl[5] != 0.0) return;  // the search already stopped
+        gamma = ctl[0];
+    }
     const int lane = threadIdx.x & 31;
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
@@ -167,7 +172,7 @@ int fail(cudaError_t e, const char *what) {
 
 template <int W>
 int launch_backward(const dm::SweepDev &s, const double *lam, const double *d, double gamma, double *B,
-                    double *bounds, cudaStream_t st) {
+                    double *bounds, cudaStream_t st, const double *ctl) {
     const int blocks = (int)((s.groups * 32 + kSweepThreads - 1) / kSweepThreads);
     const size_t smem = 2 * W * kSweepThreads * sizeof(double);
     if (smem > 48 * 1024) {
@@ -177,13 +182,13 @@ int launch_backward(const dm::SweepDev &s, const double *lam, const double *d, d
         cudaFuncSetAttribute(sweep_backward_kernel<W, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (d && B)
-        sweep_backward_kernel<W, true, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds);
+        sweep_backward_kernel<W, true, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
     else if (d)
-        sweep_backward_kernel<W, true, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds);
+        sweep_backward_kernel<W, true, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
     else if (B)
-        sweep_backward_kernel<W, false, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds);
+        sweep_backward_kernel<W, false, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
     else
-        sweep_backward_kernel<W, false, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds);
+        sweep_backward_kernel<W, false, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DM_OK : fail(e, "sweep_backward");
 }
@@ -204,12 +209,12 @@ int launch_forward(const dm::SweepDev &s, const double *lam, double *F, double *
 namespace dm {
 
 int sweep_backward(const SweepDev &s, const double *lam, const double *d, double gamma, double *B, double *bounds,
-                   void *stream) {
+                   void *stream, const double *ctl) {
     if (s.groups == 0) return DM_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    if (s.max_width <= 8) return launch_backward<8>(s, lam, d, gamma, B, bounds, st);
-    if (s.max_width <= 16) return launch_backward<16>(s, lam, d, gamma, B, bounds, st);
-    return launch_backward<32>(s, lam, d, gamma, B, bounds, st);
+    if (s.max_width <= 8) return launch_backward<8>(s, lam, d, gamma, B, bounds, st, ctl);
+    if (s.max_width <= 16) return launch_backward<16>(s, lam, d, gamma, B, bounds, st, ctl);
+    return launch_backward<32>(s, lam, d, gamma, B, bounds, st, ctl);
 }
 
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream) {

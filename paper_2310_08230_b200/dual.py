@@ -34,6 +34,7 @@ class KernelTimer:
 
     def __init__(self):
         self.events: dict[str, list] = {}
+        self.counts: dict[str, int] = {}
 
     def begin(self, name):
         a = torch.cuda.Event(enable_timing=True)
@@ -45,6 +46,9 @@ class KernelTimer:
         name, a, b = ev
         b.record()
         self.events.setdefault(name, []).append((a, b))
+
+    def count(self, name, n):
+        self.counts[name] = self.counts.get(name, 0) + int(n)
 
     def summary(self) -> dict[str, dict]:
         torch.cuda.synchronize()
@@ -72,6 +76,7 @@ class DualState:
         self._scratch_B: torch.Tensor | None = None
         self._scratch_bounds = torch.zeros(f.num_bdds, dtype=_F64, device=d)
         self._scal = torch.zeros(8, dtype=_F64, device=d)
+        self._step_state = None
         self.f_valid = False
         self.b_valid = False
         self.bound = -np.inf
@@ -159,6 +164,24 @@ class DualState:
             self.pass_timer.end(ev)
         self.sweeps += 1
         return self._sum_bounds(self._scratch_bounds)
+
+    def search_step(self, d: torch.Tensor, gamma_prev: float, shrink: float, grow: float, min_ascent: float,
+                    max_trials: int) -> tuple[float, float, int]:
+        """find_step_size's trial sequence on the device (dm_step_search):
+        returns (gamma_best, e_best, trials run); one read-back at the end."""
+        if self._step_state is None:
+            self._step_state = torch.zeros(8, dtype=_F64, device=self.device)
+        ev = self.pass_timer.begin("step_search") if self.pass_timer else None
+        self.dev.step_search(self.lam_d, d, gamma_prev, self.free_contribution, shrink, grow, min_ascent,
+                             max_trials, self._scratch_bounds, self._step_state)
+        if ev:
+            self.pass_timer.end(ev)
+        st = self._step_state.cpu().numpy()
+        trials = int(st[6])
+        self.sweeps += trials
+        if self.pass_timer:
+            self.pass_timer.count("step_search_trials", trials)
+        return float(st[3]), float(st[2]), trials
 
     # -- dual vectors per constraint ------------------------------------------
     def lambda_of(self, constraint: int) -> np.ndarray:

@@ -92,6 +92,14 @@ class DeviceFlat:
         _native.call("dm_k_backward_trial", self._h, _ptr(lam), _ptr(d), float(gamma), _ptr(B), _ptr(bounds),
                      self._s())
 
+    def step_search(self, lam, d, gamma_prev, free_contribution, shrink, grow, min_ascent, max_trials, bounds,
+                    state):
+        """The whole find_step_size trial sequence on the device (dm_step_search)."""
+        sweep_launches = 3  # per trial: sweep, pairwise leaves, pairwise combine + decision
+        _native.call("dm_step_search", self._h, _ptr(lam), _ptr(d), float(gamma_prev), float(free_contribution),
+                     float(shrink), float(grow), float(min_ascent), int(max_trials), _ptr(bounds), _ptr(state),
+                     self._s(), launches=1 + sweep_launches * (int(max_trials) + 1))
+
     def k_forward(self, lam, F, bounds):
         _native.call("dm_k_forward", self._h, _ptr(lam), _ptr(F), _ptr(bounds), self._s())
 

@@ -264,12 +264,45 @@ def test_find_step_size_counts():  # test_qn.py:117-137
     calls = []
     orig = st.eval_step
     st.eval_step = lambda d, gm: (calls.append(1), orig(d, gm))[1]
-    gamma, improved = qn.find_step_size(st, np.zeros(4), 1.0, qn.StepConfig(min_ascent=1e-3, max_trials=5))
+    cfg = qn.StepConfig(min_ascent=1e-3, max_trials=5)
+    gamma, improved = qn.find_step_size(st, np.zeros(4), 1.0, cfg, on_device=False)
     assert not improved and len(calls) == 6
+    s0 = st.sweeps
+    assert qn.find_step_size(st, np.zeros(4), 1.0, cfg) == (gamma, improved)
+    assert st.sweeps - s0 == 6  # baseline plus K trials, on the device
     calls.clear()
     d = qn.project_direction(subgradient(st), st)
-    qn.find_step_size(st, d, 1.0, qn.StepConfig(min_ascent=-10.0))
+    cfg = qn.StepConfig(min_ascent=-10.0)
+    host = qn.find_step_size(st, d, 1.0, cfg, on_device=False)
     assert len(calls) == 2
+    s0 = st.sweeps
+    assert qn.find_step_size(st, d, 1.0, cfg) == host
+    assert st.sweeps - s0 == 2
+
+
+@pytest.mark.parametrize("name", ["ps_tetra", "ps_icosa", "random3_c3", "random7_c0", "kinked"])
+def test_device_step_search_matches_host_loop(name):
+    """dm_step_search == the host trial loop (qn.py:132-159): same gamma, same
+    verdict, same number of trial sweeps, over random directions, starting
+    steps and ascent thresholds (incl. early stops and all-trials runs)."""
+    inst = product_instance(next(c for c in CASES if c["name"] == name))
+    st = init_duals(inst)
+    mma_pass(st, FORWARD)
+    mma_pass(st, BACKWARD)
+    rng = np.random.default_rng(7)
+    for trial in range(12):
+        d = qn.project_direction(rng.standard_normal(st.lam.shape) * 10.0 ** rng.uniform(-4, 0), st)
+        d = torch.from_numpy(np.asarray(d)).to(st.device)
+        gamma0 = float(10.0 ** rng.uniform(-2, 1))
+        cfg = qn.StepConfig(min_ascent=float([0.0, 1e-9, 1e-3, 1.0, -1.0][trial % 5]),
+                            max_trials=int(rng.integers(1, 8)))
+        s0 = st.sweeps
+        host = qn.find_step_size(st, d, gamma0, cfg, on_device=False)
+        n_host = st.sweeps - s0
+        s0 = st.sweeps
+        dev = qn.find_step_size(st, d, gamma0, cfg)
+        assert dev == host
+        assert st.sweeps - s0 == n_host
 
 
 def test_solver_iteration_empty_history_is_averaging():  # test_qn.py:140-146
@@ -359,3 +392,78 @@ def test_curvature_pair_matches_separate_ops(n):
     assert y.cpu().numpy().tobytes() == y_ref.tobytes()
     assert lp.cpu().numpy().tobytes() == lam.cpu().numpy().tobytes()
     assert float(sy[0]) == solver._dot_chunked(s_ref, y_ref)
+
+
+def _host_level_order(f, forward):
+    """build_mma_schedule (dm_host.cpp) restated: level = 1 + deepest level of
+    the copies' previous (forward) / next (backward) layers; positions with
+    copies bucketed by level in visitation order."""
+    pp, pl, bl, lb = (np.asarray(getattr(f, k)) for k in ("proc_ptr", "proc_layers", "bdd_layer_lo", "layer_bdd"))
+    P = len(pp) - 1
+    last = np.zeros(len(bl) - 1, np.int64)
+    lev = np.full(P, -1, np.int64)
+    ks = range(P) if forward else range(P - 1, -1, -1)
+    for p in ks:
+        ls = pl[pp[p]:pp[p + 1]]
+        if len(ls) == 0:
+            continue
+        js = lb[ls]
+        first = ls == bl[js] if forward else ls + 1 == bl[js + 1]
+        v = int((last[js[~first]] + 1).max()) if (~first).any() else 0
+        last[js] = v
+        lev[p] = v
+    visit = np.fromiter(ks, np.int64)
+    visit = visit[lev[visit] >= 0]
+    order = visit[np.argsort(lev[visit], kind="stable")]
+    return order, lev[order]
+
+
+@pytest.mark.parametrize("name", ["ps_tetra", "ps_icosa", "ps_c1", "random3_c3", "random7_c0", "toy"])
+def test_device_level_orders_match_host_schedule(name):
+    from paper_2310_08230_b200 import _native
+
+    inst = product_instance(next(c for c in CASES if c["name"] == name))
+    st = init_duals(inst)
+    f = inst.flat
+    pp, pl = np.asarray(f.proc_ptr), np.asarray(f.proc_layers)
+    for forward in (True, False):
+        order, lev = _host_level_order(f, forward)
+        n = st.dev.info["fw_tasks" if forward else "bw_tasks"]
+        assert n == len(order)
+        assert st.dev.info["fw_depth" if forward else "bw_depth"] == (int(lev.max()) + 1 if len(lev) else 0)
+        levels = np.zeros(n, np.int32)
+        layers = np.zeros(n * 8, np.int32)
+        _native.check(_native.load().dm_flat_task_levels(st.dev.handle, int(forward), levels.ctypes.data,
+                                                        layers.ctypes.data))
+        assert levels.tolist() == lev.tolist()
+        want = np.full((n, 8), -1, np.int64)
+        for t, p in enumerate(order):
+            k = pp[p + 1] - pp[p]
+            want[t, :k] = pl[pp[p]:pp[p + 1]]
+        assert layers.reshape(n, 8).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("where", ["inner_true", "skip_layer", "last_to_node", "bad_code"])
+def test_invalid_arc_targets_are_rejected(where):
+    import copy
+
+    from paper_2310_08230_b200.errors import ProdmatchError
+    from paper_2310_08230_b200.kernels import DeviceFlat
+
+    inst = product_instance(next(c for c in CASES if c["name"] == "random3_c0"))
+    t = copy.copy(inst.flat)
+    t.zero_t, t.one_t = t.zero_t.copy(), t.one_t.copy()
+    bl, lnl = t.bdd_layer_lo, t.layer_node_lo
+    j = int(np.argmax(np.diff(bl) >= 3))  # a diagram with at least three layers
+    l0 = int(bl[j])
+    if where == "inner_true":
+        t.zero_t[lnl[l0]] = -2
+    elif where == "skip_layer":
+        t.one_t[lnl[l0]] = lnl[l0 + 2]
+    elif where == "last_to_node":
+        t.zero_t[lnl[bl[j + 1] - 1]] = 0
+    else:
+        t.one_t[lnl[l0]] = -3
+    DeviceFlat(inst.flat, torch.device("cuda:0"))  # the untouched table is accepted
+    with pytest.raises(ProdmatchError, match="arc targets"):
+        DeviceFlat(t, torch.device("cuda:0"))
