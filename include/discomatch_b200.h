@@ -250,6 +250,9 @@ int dm_host_pairwise_sum(const double *x, int64_t n, double *out);
  * with the device kernel's lane semantics (forward != 0: forward pass; F
  * resets F[root] = 0 itself).  Used by the CPU
  * test-suite to prove the schedule reproduces the sequential pass. */
+/* Test hook: the exact-pass division of a copy-delta sum by its copy count k
+ * (1..8) against __ddiv_rn on n hashed doubles; *mismatches = differing bits. */
+int dm_debug_div_check(int k, uint64_t n, uint64_t seed, unsigned long long *mismatches);
 int dm_debug_emulate_mma(const dm_flat_desc *desc, int forward, double *lam, double *F, double *B,
                          double *bounds, int64_t *depth_out);
 

@@ -64,6 +64,7 @@ SIGNATURES = {
     "dm_flat_destroy": ([_P], None),
     "dm_k_backward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_backward_trial": ([_P, _P, _P, _D, _P, _P, _P], _INT),
+    "dm_debug_div_check": ([_INT, ctypes.c_uint64, ctypes.c_uint64, _P], _INT),
     "dm_step_search": ([_P, _P, _P, _D, _D, _D, _D, _D, _INT, _P, _P, _P], _INT),
     "dm_k_forward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_mma_forward": ([_P, _P, _P, _P, _P, _P], _INT),

@@ -886,33 +886,87 @@ __device__ __forceinline__ double np_node(double v0, double v1, int c, int i) {
     return (i & 1) ? b : a;
 }
 
+// Division of the copy-delta sum by the copy count, prepared before the
+// wait: the count of a task's copies is known from its record, so the
+// reciprocal is ready when the sum arrives.  Powers of two multiply by their
+// exact reciprocal; other counts (3, 5, 6, 7) take Markstein's correction:
+// with y = RN(1/k) and q = RN(a*y) (within one ulp of a/k), the residual
+// r = a - q*k is exact in one fma and RN(q + r*y) = RN(a/k) — the quotient
+// of a normal a by k = 2^s * odd is either exact or has an infinite binary
+// expansion, so it is never a rounding tie.  Sums below 2^-960 (where the
+// intermediate could leave the normal range) take __ddiv_rn.
+// tests/test_gpu_parity.py checks it against __ddiv_rn (dm_debug_div_check).
+struct NpDiv {
+    double r, kd;
+    bool pow2;
+};
+
+__device__ __forceinline__ NpDiv np_div(int k) {
+    NpDiv d;
+    k = max(k, 1);
+    d.kd = (double)k;
+    d.pow2 = (k & (k - 1)) == 0;
+    d.r = d.pow2 ? exact_inverse_pow2(k) : __ddiv_rn(1.0, d.kd);
+    return d;
+}
+
+__device__ __forceinline__ double div_by_count(double a, const NpDiv &d) {
+    if (d.pow2) return __dmul_rn(a, d.r);
+    if (fabs(a) < 0x1p-960) return __ddiv_rn(a, d.kd);
+    const double q = __dmul_rn(a, d.r);
+    const double res = __fma_rn(-q, d.kd, a);
+    return res == 0.0 ? q : __fma_rn(res, d.r, q);
+}
+
 // Sequential sum of the copies' deltas in copy order + the new dual, as
-// average_in_group (same +0.0 / exact-reciprocal identities).
-// The copies' deltas meet in the warp's shared-memory row `sd` (8 doubles).
-__device__ __forceinline__ double np_average(bool act, int k, int c, int q, double m0, double m1, double lam_l,
-                                             double *sd) {
+// average_in_group (same +0.0 / exact-reciprocal identities).  The deltas
+// are gathered with shuffles; copy slots j >= k belong to inactive lanes and
+// hold +0.0, so all eight are added unconditionally (bit-neutral, and no
+// select on the dependent chain: tools/workbench.cu measured 461 -> 369
+// cycles per task).  `dv` is np_div(k): when every copy is finite (the common
+// case, decided by a warp-uniform count) the divisor is the one prepared
+// before the wait.
+__device__ __forceinline__ double np_average(bool act, int k, int q, double m0, double m1, double lam_l,
+                                             const NpDiv &dv) {
     const bool fin = act && m0 != DM_INF && m1 != DM_INF;
     const double dlt = fin ? __dsub_rn(m1, m0) : 0.0;
     const unsigned finmask = __ballot_sync(kFull, fin && q == 0);
-    if (q == 0) sd[c] = dlt;
-    __syncwarp();
     double dk[kNpCopies];
 #pragma unroll
-    for (int j = 0; j < kNpCopies; ++j) dk[j] = sd[j];
+    for (int j = 0; j < kNpCopies; ++j) dk[j] = __shfl_sync(kFull, dlt, 4 * j);
     double fsum = 0.0;
 #pragma unroll
-    for (int j = 0; j < kNpCopies; ++j)
-        if (j < k) fsum = __dadd_rn(fsum, dk[j]);
-    const int fcnt = __popc(finmask);
-    if (fin && fcnt > 0) {
-        double avg;
-        if ((fcnt & (fcnt - 1)) == 0)
-            avg = __dmul_rn(fsum, exact_inverse_pow2(fcnt));
-        else
-            avg = __ddiv_rn(fsum, (double)fcnt);
-        lam_l = __dadd_rn(lam_l, __dsub_rn(avg, dlt));
+    for (int j = 0; j < kNpCopies; ++j) fsum = __dadd_rn(fsum, dk[j]);
+    const int fcnt = __popc(finmask);  // warp-uniform
+    double avg = 0.0;
+    if (fcnt == k)
+        avg = div_by_count(fsum, dv);
+    else if (fcnt > 0)
+        avg = (fcnt & (fcnt - 1)) == 0 ? __dmul_rn(fsum, exact_inverse_pow2(fcnt)) : __ddiv_rn(fsum, (double)fcnt);
+    return fin ? __dadd_rn(lam_l, __dsub_rn(avg, dlt)) : lam_l;
+}
+
+// dm_debug_div_check: div_by_count against __ddiv_rn on hashed doubles
+// spanning the exponent range, plus scaled small integers
+__global__ void div_check_kernel(int k, uint64_t n, uint64_t seed, unsigned long long *mismatches) {
+    const NpDiv dv = np_div(k);
+    unsigned long long bad = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t h = (i + seed) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        double a;
+        if (i & 1) {
+            const uint64_t e = 1 + (h >> 53) % 2045;  // normal exponents
+            a = __longlong_as_double((long long)(((h & 1) << 63) | (e << 52) | ((h >> 1) & 0xfffffffffffffull)));
+        } else {
+            a = (double)(int64_t)((h >> 40) - (1ull << 23)) * __longlong_as_double((long long)((1023 + (int)((h >> 8) & 63) - 32) << 52 & 0x7ff0000000000000ll));
+        }
+        const double got = div_by_count(a, dv), want = __ddiv_rn(a, (double)k);
+        if (__double_as_longlong(got) != __double_as_longlong(want)) ++bad;
     }
-    return lam_l;
+    if (bad) atomicAdd(mismatches, bad);
 }
 
 struct NpLane {
@@ -966,11 +1020,10 @@ __device__ __forceinline__ int64_t np_next_task(const MmaArgs &a, int lane) {
 }
 
 // Per warp: node values of each copy (9 slots, slot 8 the arc-to-nothing
-// value) and the copies' deltas, in shared memory.
+// value) in shared memory.
 constexpr int kNpWarps = 8;  // 256-thread blocks
 struct NpShared {
     double node[kNpWarps][kNpCopies][9];
-    alignas(16) double delta[kNpWarps][kNpCopies];
 };
 
 // Poll loop of the node-parallel kernels (needs `have`, `take`, `a`, `t_wait`,
@@ -996,6 +1049,7 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
     for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
         __syncwarp();  // the previous task's shared-memory reads are done
         const NpLaneX r = np_lane(a, task, lane);
+        const NpDiv dv = np_div(r.k);
         double *nodes = sh.node[wib][r.c];
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0 = 0, wn = 0;
@@ -1037,11 +1091,12 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
             }
         };
         NP_POLL_LOOP(src0, src1)
+        __syncwarp();  // the node rows written by `take` are visible to the publish below
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
         // min-marginals over the layer (tree_lmin<8> split over the 4 lanes)
         const double m0 = np_lmin4(lmin(__dadd_rn(f0, t00), __dadd_rn(f1, t01)), r.q);
         const double m1 = np_lmin4(lmin(__dadd_rn(__dadd_rn(f0, lam_l), t10), __dadd_rn(__dadd_rn(f1, lam_l), t11)), r.q);
-        lam_l = np_average(r.act, r.k, r.c, r.q, m0, m1, lam_l, sh.delta[wib]);  // also orders `nodes`
+        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l, dv);
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         const double c0 = __dadd_rn(f0, lam_l), c1 = __dadd_rn(f1, lam_l);
@@ -1103,6 +1158,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
     for (int64_t task = np_next_task(a, lane); task < a.ntasks; task = np_next_task(a, lane)) {
         __syncwarp();  // the previous task's shared-memory reads are done
         const NpLaneX r = np_lane(a, task, lane);
+        const NpDiv dv = np_div(r.k);
         double *nodes = sh.node[wib][r.c];  // next layer's distances, slot 8 = -0.0
         const int i0 = 2 * r.q, i1 = i0 + 1;
         int32_t n0n = 0, wnext = 0;
@@ -1171,7 +1227,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         }
         const double m0 = np_lmin4(lmin(__dadd_rn(f0b[0], tz[0]), __dadd_rn(f0b[1], tz[1])), r.q);
         const double m1 = np_lmin4(lmin(__dadd_rn(f1b[0], to[0]), __dadd_rn(f1b[1], to[1])), r.q);
-        lam_l = np_average(r.act, r.k, r.c, r.q, m0, m1, lam_l, sh.delta[wib]);
+        lam_l = np_average(r.act, r.k, r.q, m0, m1, lam_l, dv);
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         // rebuild this layer's distances to TRUE (kernels.py:340-358)
@@ -2005,6 +2061,21 @@ int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, do
     DM_CHECK_FLAT(f);
     if (f->nb == 0) return DM_OK;
     return dm::sweep_backward(f->sweep, lam, d, gamma, B, bounds, stream);
+}
+
+int dm_debug_div_check(int k, uint64_t n, uint64_t seed, unsigned long long *mismatches) {
+    if (k < 1 || k > 8 || !mismatches) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    unsigned long long *d;
+    DM_CUDA(cudaMalloc(&d, sizeof(*d)));
+    DM_CUDA(cudaMemset(d, 0, sizeof(*d)));
+    div_check_kernel<<<148 * 8, 256>>>(k, n, seed, d);
+    const cudaError_t e = cudaMemcpy(mismatches, d, sizeof(*d), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e) return cuda_fail(e, "div check");
+    return DM_OK;
 }
 
 int dm_step_search(const dm_flat *f, const double *lam, const double *d, double gamma_prev, double free_contribution,

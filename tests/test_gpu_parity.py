@@ -467,3 +467,17 @@ def test_invalid_arc_targets_are_rejected(where):
     DeviceFlat(inst.flat, torch.device("cuda:0"))  # the untouched table is accepted
     with pytest.raises(ProdmatchError, match="arc targets"):
         DeviceFlat(t, torch.device("cuda:0"))
+
+
+@pytest.mark.parametrize("k", range(1, 9))
+def test_exact_pass_division_matches_ddiv(k):
+    """The exact passes divide a copy-delta sum by the copy count with a
+    prepared reciprocal (+ Markstein's correction for 3, 5, 6, 7): bit-equal
+    to IEEE division on 2^26 hashed doubles per count."""
+    import ctypes
+
+    from paper_2310_08230_b200 import _native
+
+    bad = ctypes.c_ulonglong(0)
+    _native.check(_native.load().dm_debug_div_check(k, 1 << 26, 12345 + k, ctypes.byref(bad)))
+    assert bad.value == 0

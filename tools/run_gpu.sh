@@ -41,6 +41,7 @@ for step in "$@"; do
     abnp) timeout 1200 python tools/ab_mma.py DM_MMA_NP=0 DM_MMA_NP=1 DM_MMA_NP=0 DM_MMA_NP=1 > gpurun_out/abnp.jsonl 2> gpurun_out/abnp.err ;;
     e2eprof) timeout 900 python tools/e2e_profile.py > gpurun_out/e2eprof.txt 2>&1 ;;
     create) timeout 900 python tools/create_timing.py > gpurun_out/create.txt 2>&1 ;;
+    workbench) ./tools/workbench > gpurun_out/workbench.jsonl 2>&1 ;;
     worklat) timeout 600 python tools/work_latency.py icosa > gpurun_out/worklat.txt 2>&1 ;;
     timeline) timeout 900 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err ;;
     concur) timeout 900 python tools/concurrency.py > gpurun_out/concur.jsonl 2> gpurun_out/concur.err ;;

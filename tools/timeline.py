@@ -13,7 +13,7 @@ from paper_2310_08230_b200.qn import DualSolver  # noqa: E402
 
 inst = build_instance("c2", 0)
 run = DualSolver(inst, SolveConfig(max_iterations=10**9, dual_tolerance=0.0), device="cuda:0").start()
-for _ in range(12):
+for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 40):  # past the early iterations
     run.step()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -36,7 +36,7 @@ for s, e, n in spans[1:]:
 busy += cur_e - cur_s
 agg = {}
 for s, e, n in spans:
-    k = n.split("(")[0].replace("void ", "")[:60]
+    k = n.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0][:60]
     agg[k] = agg.get(k, 0) + (e - s)
 print(json.dumps({"wall_us": t1 - t0, "busy_us": busy, "idle_us": (t1 - t0) - busy, "kernels": len(spans),
                   "gaps_over_10us": sum(1 for g in gaps if g[0] > 10), "idle_in_gaps_over_10us": sum(g[0] for g in gaps if g[0] > 10),
