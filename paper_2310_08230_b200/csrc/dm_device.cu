@@ -1928,7 +1928,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     DM_CUDA(cudaMemcpy(&rfail, relax_fail, sizeof(rfail), cudaMemcpyDeviceToHost));
     f->relax_ok = want_relax && rfail == 0;
     rc = configure_mma(f.get(), env_int("DM_MMA_THREADS", 256), env_int("DM_MMA_BLOCKS_PER_SM", 3),
-                       (unsigned)env_int("DM_MMA_SLEEP_NS", 0), env_int("DM_MMA_PROBE", 0),
+                       (unsigned)env_int("DM_MMA_SLEEP_NS", 32), env_int("DM_MMA_PROBE", 0),
                        env_int("DM_MMA_LOOKAHEAD", 0) | (env_int("DM_MMA_WARM", 1) << 16) |
                            ((env_int("DM_MMA_DESC", 1) ? 0 : 1) << 17) | ((env_int("DM_MMA_NP", 1) ? 0 : 1) << 18));
     if (rc) return rc;

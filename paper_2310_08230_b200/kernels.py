@@ -109,7 +109,7 @@ class DeviceFlat:
     def k_mma_backward(self, lam, F, B, bounds):
         _native.call("dm_k_mma_backward", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(bounds), self._s())
 
-    def set_mma_config(self, threads: int = 256, blocks_per_sm: int = 3, sleep_ns: int = 0, probe: bool = False,
+    def set_mma_config(self, threads: int = 256, blocks_per_sm: int = 3, sleep_ns: int = 32, probe: bool = False,
                        lookahead: int = 1 << 16):
         """Launch shape of the exact passes (see dm_flat_set_mma_config)."""
         _native.call("dm_flat_set_mma_config", self._h, int(threads), int(blocks_per_sm), int(sleep_ns), int(probe),

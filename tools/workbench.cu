@@ -242,6 +242,63 @@ __global__ void work_kernel(int iters, int k, uint64_t desc, double seed, double
     if (lane == 0) *cycles = t1 - t0;
 }
 
+// backward task chain: next-layer distances routed to the lane's arcs
+// through shared memory (kShfl = 0, as mma_np_backward_kernel) or shuffles
+template <int kShfl>
+__global__ void work_bw_kernel(int iters, int k, double seed, double *out, long long *cycles) {
+    __shared__ NpShared sh;
+    const int lane = threadIdx.x & 31, c = lane >> 2, q = lane & 3;
+    const int i0 = 2 * q, i1 = i0 + 1;
+    const bool act = c < k;
+    double *nodes = sh.node[0][c];
+    const NpDiv dv = np_div(k);
+    int iz[2] = {(i0 + 1) & 7, (i0 + 3) & 7}, io[2] = {(i0 + 2) & 7, (i0 + 5) & 7};
+    double f0b[2] = {0.5 * lane, 0.25 * lane}, f1b[2] = {1.5, 2.5}, rz[2] = {-0.0, -0.0}, ro[2] = {-0.0, -0.0};
+    double nb0 = seed + lane, nb1 = seed - lane, lam = 0.25 * lane;
+    nodes[8] = -0.0;
+    __syncwarp();
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        double tz[2], to[2];
+        if (kShfl) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int sz = 4 * c + (iz[j] >> 1), so = 4 * c + (io[j] >> 1);
+                const double za = __shfl_sync(kFull, nb0, sz), zb = __shfl_sync(kFull, nb1, sz);
+                const double oa = __shfl_sync(kFull, nb0, so), ob = __shfl_sync(kFull, nb1, so);
+                tz[j] = (iz[j] & 1) ? zb : za;
+                to[j] = (io[j] & 1) ? ob : oa;
+            }
+        } else {
+            nodes[i0] = nb0;
+            nodes[i1] = nb1;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                tz[j] = nodes[iz[j]];
+                to[j] = nodes[io[j]];
+            }
+        }
+        const double m0 = np_lmin4(lmin(__dadd_rn(f0b[0], tz[0]), __dadd_rn(f0b[1], tz[1])), q);
+        const double m1 = np_lmin4(lmin(__dadd_rn(f1b[0], to[0]), __dadd_rn(f1b[1], to[1])), q);
+        const double lam_l = np_average(act, k, q, m0, m1, lam, dv);
+        double bv[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const double cz = __dadd_rn(rz[j], tz[j]);
+            const double co = __dadd_rn(__dadd_rn(lam_l, to[j]), ro[j]);
+            bv[j] = cz <= co ? cz : co;
+        }
+        nb0 = bv[0] * 0.5;
+        nb1 = bv[1] * 0.5;
+        lam = lam_l * 0.5;
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    out[lane] = nb0 + nb1 + lam;
+    if (lane == 0) *cycles = t1 - t0;
+}
+
 }  // namespace
 
 int main() {
@@ -286,6 +343,15 @@ int main() {
                     "\"full_markstein_cycles\": %.1f, \"full_no_division_cycles\": %.1f, \"full_uniform_cycles\": %.1f, \"pow2_mul_only\": %.1f, \"table_mul_only\": %.1f, \"new_shfl\": %.1f, \"new_shfl_seq\": %.1f, \"zero_pad8\": %.1f, \"zero_pad_4_4\": %.1f}\n",
                     k, (double)h[0] / iters, (double)h[1] / iters, (double)h[2] / iters, (double)h[3] / iters,
                     (double)h[4] / iters, (double)h[5] / iters, (double)h[6] / iters, (double)h[7] / iters, (double)h[8] / iters, (double)h[9] / iters, (double)h[10] / iters, (double)h[11] / iters, (double)h[12] / iters);
+    }
+    for (int k : {4, 5}) {
+        long long h[2];
+        work_bw_kernel<0><<<1, 32>>>(iters, k, 1.0, out, cyc);
+        cudaMemcpy(&h[0], cyc, 8, cudaMemcpyDeviceToHost);
+        work_bw_kernel<1><<<1, 32>>>(iters, k, 1.0, out, cyc);
+        cudaMemcpy(&h[1], cyc, 8, cudaMemcpyDeviceToHost);
+        std::printf("{\"backward\": true, \"copies\": %d, \"smem_route_cycles\": %.1f, \"shfl_route_cycles\": %.1f}\n",
+                    k, (double)h[0] / iters, (double)h[1] / iters);
     }
     cudaError_t e = cudaDeviceSynchronize();
     if (e) std::printf("error %s\n", cudaGetErrorString(e));
