@@ -1354,6 +1354,7 @@ int upload(dm_flat *f, T **dst, const T *src, int64_t n, cudaStream_t s) {
 // for the process lifetime; concurrent creates each take their own.
 constexpr size_t kStageSlotBytes = size_t(16) << 20;
 constexpr int kStageSlots = 4;
+constexpr int kStageFillThreads = 8;
 struct StageRing {
     int device = -1;
     char *buf = nullptr;
@@ -1394,7 +1395,7 @@ class Stager {
     }
     // device array of n elements of T; element i is produced by
     // fill(T *dst, int64_t first, int64_t count) writing elements
-    // [first, first + count) to dst (run on up to 4 threads per slot)
+    // [first, first + count) to dst (run on up to kStageFillThreads threads per slot)
     template <typename T, typename Fill>
     int put(dm_flat *f, T **dst, int64_t n, Fill &&fill) {
         int rc = upload(f, dst, (const T *)nullptr, n, s_);
@@ -1414,11 +1415,11 @@ class Stager {
             const int slot = next_++ % kStageSlots;
             DM_CUDA(cudaEventSynchronize(ring_->ev[slot]));
             T *buf = (T *)(ring_->buf + slot * kStageSlotBytes);
-            const int nt = cnt * (int64_t)sizeof(T) >= (int64_t(1) << 20) ? 4 : 1;
+            const int nt = cnt * (int64_t)sizeof(T) >= (int64_t(1) << 20) ? kStageFillThreads : 1;
             if (nt == 1) {
                 fill(buf, lo, cnt);
             } else {
-                std::thread th[4];
+                std::thread th[kStageFillThreads];
                 for (int t = 0; t < nt; ++t) {
                     const int64_t a = cnt * t / nt, b = cnt * (t + 1) / nt;
                     th[t] = std::thread([&, a, b] { fill(buf + a, lo + a, b - a); });
@@ -1849,9 +1850,15 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         t_sweep = host_seconds() - t0;
     });
     if (dm::device_layer_flags(f->layer_bdd, f->bdd_layer_lo, L, f->layer_flags, ps.s)) return DM_ERR_CUDA;
+    cudaEvent_t walk_ev[2] = {nullptr, nullptr};
+    if (vb2) {
+        for (auto &e : walk_ev) cudaEventCreate(&e);
+        cudaEventRecord(walk_ev[0], ps.s);
+    }
     if (dm::device_level_orders(f->proc_ptr, f->proc_layers, f->layer_bdd, f->bdd_layer_lo, P, L, nvalid, f->fw_pos,
                                 f->fw_lev, f->bw_pos, f->bw_lev, plan_words, ps.s))
         return DM_ERR_CUDA;
+    if (vb2) cudaEventRecord(walk_ev[1], ps.s);
     if (want_np && dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, P, f->np_rec, ps.s))
         return DM_ERR_CUDA;
     DM_CUDA(cudaEventRecord(ps.done, ps.s));
@@ -1922,6 +1929,12 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     mark("tail queued");
     DM_CUDA(cudaStreamSynchronize(s));  // the host staging vectors die with this scope
     mark("synchronised");
+    if (vb2) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, walk_ev[0], walk_ev[1]);
+        std::fprintf(stderr, "  [dm_flat_create] level orders on the device: %.2f ms\n", ms);
+        for (auto &e : walk_ev) cudaEventDestroy(e);
+    }
     int words[8];
     unsigned long long rfail = 1;
     DM_CUDA(cudaMemcpy(words, plan_words, sizeof(words), cudaMemcpyDeviceToHost));

@@ -63,12 +63,19 @@ __global__ void level_init_kernel(const int32_t *proc_ptr, int64_t P, bool forwa
 
 // Persistent walk: warps take 32 consecutive visitation indices from a
 // counter; a position depends only on positions visited before it, which
-// warps that took earlier chunks hold, so the walk cannot deadlock.
+// warps that took earlier chunks hold (or the same warp), so the walk cannot
+// deadlock.  Consecutive positions mostly share diagrams, so a chunk is
+// often one dependency chain: levels resolved inside the chunk are handed
+// on through the warp's shared-memory row (one __syncwarp per step) instead
+// of a global store -> poll round trip.
+constexpr int kWalkWarps = 8;
 __global__ void __launch_bounds__(256) level_walk_kernel(const int32_t *proc_ptr, const int32_t *proc_layers,
                                                          const int32_t *layer_bdd, const int32_t *bdd_layer_lo,
                                                          const int32_t *layer_pos, int64_t P, bool forward,
                                                          int32_t *level, int *counter, int *status) {
+    __shared__ int32_t row_s[kWalkWarps][32];
     const int lane = threadIdx.x & 31;
+    volatile int32_t *row = row_s[threadIdx.x >> 5];
     while (true) {
         int base = 0;
         if (lane == 0) base = atomicAdd(counter, 32);
@@ -83,6 +90,8 @@ __global__ void __launch_bounds__(256) level_walk_kernel(const int32_t *proc_ptr
             hi = proc_ptr[p + 1];
             done = t == hi;
         }
+        row[lane] = -1;
+        __syncwarp();
         unsigned spins = 0;
         uint64_t t0 = 0;
         while (!__all_sync(kFull, done)) {
@@ -91,15 +100,19 @@ __global__ void __launch_bounds__(256) level_walk_kernel(const int32_t *proc_ptr
                     const int32_t l = proc_layers[t], j = layer_bdd[l];
                     const bool first = forward ? l == bdd_layer_lo[j] : l + 1 == bdd_layer_lo[j + 1];
                     if (first) continue;
-                    const int v = ld_relaxed_i32(level + layer_pos[forward ? l - 1 : l + 1]);
+                    const int32_t q = layer_pos[forward ? l - 1 : l + 1];
+                    const int64_t kq = forward ? q : P - 1 - q;
+                    const int v = kq >= base ? row[kq - base] : ld_relaxed_i32(level + q);
                     if (v < 0) break;
                     lev = max(lev, v + 1);
                 }
                 if (t == hi) {
                     st_relaxed_i32(level + p, lev);
+                    row[lane] = lev;
                     done = true;
                 }
             }
+            __syncwarp();
             if ((++spins & 255u) == 0) {
                 const uint64_t now = now_ns();
                 if (t0 == 0) t0 = now;
@@ -306,44 +319,73 @@ int device_level_orders(const int32_t *proc_ptr, const int32_t *proc_layers, con
     cudaError_t e;
     if ((e = cudaMemsetAsync(words, 0, 8 * sizeof(int), s))) return fail(e, "memset");
     if (P == 0 || nvalid == 0) return 0;
-    int32_t *layer_pos = nullptr, *order_in = nullptr, *lev = nullptr;
-    void *tmp = nullptr;
+    // the two directions walk concurrently on two streams; each walk is
+    // latency-bound and its polls contend in L2, so it runs on a small grid
+    // (DM_WALK_DIV: 1/32 of the resident blocks)
+    int32_t *layer_pos = nullptr, *order_in[2] = {nullptr, nullptr}, *lev[2] = {nullptr, nullptr};
+    void *tmp[2] = {nullptr, nullptr};
     size_t tmp_bytes = 0;
     if ((e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (const int32_t *)nullptr, (int32_t *)nullptr,
                                              (const int32_t *)nullptr, (int32_t *)nullptr, (int)P, 0, 31, s)))
         return fail(e, "sort size");
-    if ((e = cudaMallocAsync((void **)&layer_pos, std::max<int64_t>(L, 1) * 4, s)) ||
-        (e = cudaMallocAsync((void **)&order_in, P * 4, s)) || (e = cudaMallocAsync((void **)&lev, P * 4, s)) ||
-        (e = cudaMallocAsync(&tmp, tmp_bytes, s)))
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking)) ||
+        (e = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming)) ||
+        (e = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming)))
+        return fail(e, "stream");
+    struct Cleanup {
+        cudaStream_t s2;
+        cudaEvent_t *ev;
+        ~Cleanup() {
+            if (s2) cudaStreamDestroy(s2);  // released once its queued work completes
+            for (int i = 0; i < 2; ++i)
+                if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+    } cleanup{s2, ev};
+    if ((e = cudaMallocAsync((void **)&layer_pos, std::max<int64_t>(L, 1) * 4, s)))
         return fail(e, "allocation");
+    for (int d = 0; d < 2; ++d)
+        if ((e = cudaMallocAsync((void **)&order_in[d], P * 4, s)) || (e = cudaMallocAsync((void **)&lev[d], P * 4, s)) ||
+            (e = cudaMallocAsync(&tmp[d], tmp_bytes, s)))
+            return fail(e, "allocation");
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_walk_kernel, 256, 0);
+    const char *wd = std::getenv("DM_WALK_DIV");
+    const int walk_div = std::max(wd ? std::atoi(wd) : 32, 1);  // measured: 65 ms at 1 -> 12 ms at 16..128 (C2)
     layer_pos_kernel<<<grid_for(P, 256), 256, 0, s>>>(proc_ptr, proc_layers, P, layer_pos);
+    if ((e = cudaEventRecord(ev[0], s)) || (e = cudaStreamWaitEvent(s2, ev[0], 0))) return fail(e, "event");
     int rc = 0;
     for (int dir = 0; dir < 2 && rc == 0; ++dir) {
         const bool forward = dir == 0;
+        const cudaStream_t sd = forward ? s : s2;
         int32_t *order = forward ? fw_order : bw_order, *lv = forward ? fw_level : bw_level;
-        level_init_kernel<<<grid_for(P, 256), 256, 0, s>>>(proc_ptr, P, forward, order_in, lev);
-        level_walk_kernel<<<sms * std::max(per_sm, 1), 256, 0, s>>>(
-            proc_ptr, proc_layers, layer_bdd, bdd_layer_lo, layer_pos, P, forward, lev, words + 2 * dir,
+        level_init_kernel<<<grid_for(P, 256), 256, 0, sd>>>(proc_ptr, P, forward, order_in[dir], lev[dir]);
+        level_walk_kernel<<<std::max(sms * per_sm / walk_div, 1), 256, 0, sd>>>(
+            proc_ptr, proc_layers, layer_bdd, bdd_layer_lo, layer_pos, P, forward, lev[dir], words + 2 * dir,
             words + 2 * dir + 1);
         // keys in visitation order (lv is scratch until the sorted keys land in it)
-        gather_levels_kernel<<<grid_for(P, 256), 256, 0, s>>>(order_in, lev, P, lv);
+        gather_levels_kernel<<<grid_for(P, 256), 256, 0, sd>>>(order_in[dir], lev[dir], P, lv);
         if ((e = cudaGetLastError())) {
             rc = fail(e, "launch");
             break;
         }
-        if ((e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, lv, lev, order_in, order, (int)P, 0, 31, s)) ||
-            (e = cudaMemcpyAsync(lv, lev, P * 4, cudaMemcpyDeviceToDevice, s)) ||
-            (e = cudaMemcpyAsync(words + 4 + dir, lv + nvalid - 1, 4, cudaMemcpyDeviceToDevice, s)))
+        if ((e = cub::DeviceRadixSort::SortPairs(tmp[dir], tmp_bytes, lv, lev[dir], order_in[dir], order, (int)P, 0,
+                                                 31, sd)) ||
+            (e = cudaMemcpyAsync(lv, lev[dir], P * 4, cudaMemcpyDeviceToDevice, sd)) ||
+            (e = cudaMemcpyAsync(words + 4 + dir, lv + nvalid - 1, 4, cudaMemcpyDeviceToDevice, sd)))
             rc = fail(e, "sort");
     }
+    if (!rc && ((e = cudaEventRecord(ev[1], s2)) || (e = cudaStreamWaitEvent(s, ev[1], 0)))) rc = fail(e, "event");
+    if (rc) cudaStreamSynchronize(s2);
     cudaFreeAsync(layer_pos, s);
-    cudaFreeAsync(order_in, s);
-    cudaFreeAsync(lev, s);
-    cudaFreeAsync(tmp, s);
+    for (int d = 0; d < 2; ++d) {
+        cudaFreeAsync(order_in[d], s);
+        cudaFreeAsync(lev[d], s);
+        cudaFreeAsync(tmp[d], s);
+    }
     return rc;
 }
 
