@@ -150,6 +150,10 @@ int dm_flat_set_mma_config(dm_flat *flat, int threads, int blocks_per_sm, int sl
  * DAG level of every task (and optionally the lanes_per_task lane layers per task) of
  * the forward/backward schedule. */
 int dm_flat_set_trace(dm_flat *flat, unsigned long long *trace);
+/* Stream-ordered copy of the exact passes' watchdog word into a device
+ * double (0 = fine): lets the host check it together with other scalars in
+ * one read-back; dm_flat_status then reports and clears a fired watchdog. */
+int dm_flat_status_to(const dm_flat *flat, double *slot, void *stream);
 int dm_flat_task_levels(const dm_flat *flat, int forward, int32_t *levels, int32_t *lane_layers);
 void dm_flat_destroy(dm_flat *flat);
 

@@ -65,6 +65,7 @@ SIGNATURES = {
     "dm_k_backward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_backward_trial": ([_P, _P, _P, _D, _P, _P, _P], _INT),
     "dm_debug_div_check": ([_INT, ctypes.c_uint64, ctypes.c_uint64, _P], _INT),
+    "dm_flat_status_to": ([_P, _P, _P], _INT),
     "dm_step_search": ([_P, _P, _P, _D, _D, _D, _D, _D, _INT, _P, _P, _P], _INT),
     "dm_k_forward": ([_P, _P, _P, _P, _P], _INT),
     "dm_k_mma_forward": ([_P, _P, _P, _P, _P, _P], _INT),
@@ -133,7 +134,8 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_k_mma_backward", "dm_k_min_marginals", "dm_k_argmin", "dm_init_duals",
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
-                  "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search"}
+                  "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search",
+                  "dm_flat_status_to"}
 launch_count = 0
 
 

@@ -404,6 +404,10 @@ __global__ void pw_combine_kernel(int32_t nleaves, int32_t maxh, const int32_t *
     }
 }
 
+// the exact passes' watchdog word as a double, next to the bound sums the
+// host reads in one copy (dm_flat_status_to)
+__global__ void status_to_slot_kernel(const int *status, double *slot) { *slot = (double)*status; }
+
 __global__ void step_init_kernel(double *ctl, double gamma) {
     ctl[0] = gamma;
     for (int i = 1; i < 8; ++i) ctl[i] = 0.0;
@@ -2032,6 +2036,16 @@ int dm_flat_task_levels(const dm_flat *f, int forward, int32_t *levels, int32_t 
     if (levels) std::memcpy(levels, v.data(), v.size() * sizeof(int32_t));
     if (lane_layers) std::memcpy(lane_layers, w.data(), w.size() * sizeof(int32_t));
     return DM_OK;
+}
+
+int dm_flat_status_to(const dm_flat *f, double *slot, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!slot) {
+        dm::set_error("invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    status_to_slot_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(f->status, slot);
+    return check_stream_error("status copy");
 }
 
 int dm_flat_status(dm_flat *f, void *stream) {

@@ -87,11 +87,16 @@ class DualState:
         self._scratch_B: torch.Tensor | None = None
         self._scratch_bounds = torch.zeros(f.num_bdds, dtype=_F64, device=d)
         self._scal = torch.zeros(8, dtype=_F64, device=d)
+        # device scalars read back together: bound sums [0, 8), the passes'
+        # watchdog word [8], the curvature product s.y [9]
+        self._slots = torch.zeros(16, dtype=_F64, device=d)
+        self._pending: list[int] = []  # bound slots not yet read, in order
+        self._status_pending = False
         self._step_state = None
         self.f_valid = False
         self.b_valid = False
-        self.bound = -np.inf
-        self.best_bound = -np.inf
+        self._bound = -np.inf
+        self._best_bound = -np.inf
         self.sweeps = 0  # full-table sweep equivalents (2 arcs per node each)
         self.pass_timer: KernelTimer | None = None
         self._bgen = 0  # generation of the distance-to-TRUE table B
@@ -104,6 +109,8 @@ class DualState:
     # -- host views -------------------------------------------------------
     @property
     def lam(self) -> np.ndarray:
+        if self._status_pending:
+            self.read_scalars()  # never hand out duals of an aborted pass
         return to_host(self.lam_d)
 
     @property
@@ -116,9 +123,59 @@ class DualState:
         return float(self._scal[0].item()) + self.free_contribution
 
     def _set_bound(self) -> None:
-        self.bound = self._sum_bounds(self._bounds)
-        if self.bound > self.best_bound:
-            self.best_bound = self.bound
+        """Queue the bound of the current distance table (numpy-order sum on
+        the device); the host reads it, with the other queued scalars, the
+        next time one is needed (``read_scalars``)."""
+        if len(self._pending) == 8:
+            self.read_scalars()
+        i = len(self._pending)
+        dev_sum(self._bounds, self._slots[i:i + 1])
+        self._pending.append(i)
+
+    def _check_status_later(self) -> None:
+        """Queue the exact passes' watchdog word (read by ``read_scalars``)."""
+        self.dev.status_to(self._slots[8:9])
+        self._status_pending = True
+
+    def read_scalars(self) -> np.ndarray:
+        """One read-back of the queued device scalars: applies the queued
+        bounds in order (bound = latest, best_bound = running max, as the
+        eager bookkeeping would) and raises if a pass's watchdog fired."""
+        vals = self._slots.cpu().numpy()
+        if self._status_pending:
+            self._status_pending = False
+            if vals[8] != 0.0:
+                self._pending = []
+                self.dev.check_status()  # raises with the library's message (and clears the word)
+        for i in self._pending:
+            b = float(vals[i]) + self.free_contribution
+            self._bound = b
+            if b > self._best_bound:
+                self._best_bound = b
+        self._pending = []
+        return vals
+
+    @property
+    def bound(self) -> float:
+        if self._pending or self._status_pending:
+            self.read_scalars()
+        return self._bound
+
+    @bound.setter
+    def bound(self, v: float) -> None:
+        self._pending = []
+        self._bound = v
+
+    @property
+    def best_bound(self) -> float:
+        if self._pending or self._status_pending:
+            self.read_scalars()
+        return self._best_bound
+
+    @best_bound.setter
+    def best_bound(self, v: float) -> None:
+        self._pending = []
+        self._best_bound = v
 
     def refresh_backward(self) -> None:
         self.dev.k_backward(self.lam_d, self.B, self._bounds)
@@ -268,7 +325,7 @@ def mma_pass(state: DualState, direction: str) -> DualState:
         raise ValueError(f"unknown pass direction {direction!r}")
     state.sweeps += 2
     state._set_bound()
-    state.dev.check_status()  # fail loudly if the pass's watchdog fired
+    state._check_status_later()  # a fired watchdog raises at the next read-back
     return state
 
 

@@ -122,6 +122,10 @@ class DeviceFlat:
         """Raise if an exact pass was aborted by its watchdog (synchronises)."""
         _native.call("dm_flat_status", self._h, self._s())
 
+    def status_to(self, slot):
+        """Watchdog word -> device double, stream-ordered (no synchronisation)."""
+        _native.call("dm_flat_status_to", self._h, _ptr(slot), self._s())
+
     def k_min_marginals(self, lam, F, B, m0, m1):
         _native.call("dm_k_min_marginals", self._h, _ptr(lam), _ptr(F), _ptr(B), _ptr(m0), _ptr(m1), self._s())
 
