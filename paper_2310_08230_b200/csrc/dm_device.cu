@@ -51,6 +51,19 @@ __device__ __forceinline__ double ld_relaxed(const double *p) {
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return __longlong_as_double((long long)v);
 }
+// p[0], p[1] as one 16-byte relaxed load when p is 16-byte aligned and the
+// pair is adjacent (two 8-byte loads otherwise)
+__device__ __forceinline__ void ld_relaxed_pair(const double *p0, const double *p1, double &v0, double &v1) {
+    if (p1 == p0 + 1 && ((uintptr_t)p0 & 15) == 0) {
+        unsigned long long a, b;
+        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p0) : "memory");
+        v0 = __longlong_as_double((long long)a);
+        v1 = __longlong_as_double((long long)b);
+    } else {
+        v0 = ld_relaxed(p0);
+        v1 = ld_relaxed(p1);
+    }
+}
 // Loads p[min(i, n-1)] for i < 8 (n >= 1) in ONE asm block of unpredicated
 // loads, so that all of them are in flight before the first sentinel check
 // (separately predicated loads get interleaved with the checks by the
@@ -1034,11 +1047,13 @@ struct NpShared {
 // `spins`).  A value read as non-sentinel is final (each is written once per
 // pass).  (Two interleaved poll streams offset by half a round trip measured
 // 15% slower: the doubled poll traffic costs more than the earlier detection.)
-#define NP_POLL_LOOP(SRC0, SRC1)                                                        \
+#define NP_POLL_LOOP(SRC0, SRC1, PAIR)                                                        \
     while (true) {                                                                      \
         if (!have) {                                                                    \
             const uint64_t t_issue = a.trace ? global_ns() : 0;                         \
-            const double v0 = ld_relaxed(SRC0), v1 = ld_relaxed(SRC1);                  \
+            double v0, v1;                                                              \
+            if (PAIR) ld_relaxed_pair(SRC0, SRC1, v0, v1);                              \
+            else v0 = ld_relaxed(SRC0), v1 = ld_relaxed(SRC1);                          \
             take(v0, v1, t_issue);                                                      \
         }                                                                               \
         if (__all_sync(kFull, have)) break;                                             \
@@ -1094,7 +1109,7 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
                 np_trace(a, task, r.c, r.q, 5, t_issue);
             }
         };
-        NP_POLL_LOOP(src0, src1)
+        NP_POLL_LOOP(src0, src1, true)  // 16-byte polls where aligned: forward 4.41 -> 4.33 ms
         __syncwarp();  // the node rows written by `take` are visible to the publish below
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
         // min-marginals over the layer (tree_lmin<8> split over the 4 lanes)
@@ -1219,7 +1234,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 np_trace(a, task, r.c, r.q, 5, t_issue);
             }
         };
-        NP_POLL_LOOP(src0, src1)
+        NP_POLL_LOOP(src0, src1, false)  // (16-byte polls measured 4.91 -> 4.97 ms here)
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 2, global_ns());
         // route the next layer's distances to this lane's arcs (slot 8: -0.0)
         __syncwarp();
