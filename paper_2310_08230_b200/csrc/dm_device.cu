@@ -1799,6 +1799,18 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     keep_pool_memory(device);
     cudaStream_t s = (cudaStream_t)stream;
     auto f = std::make_unique<dm_flat>();
+    // on any error return: the device blocks allocated so far go back to the
+    // pool (destroyed after the staging ring and plan streams below, which
+    // synchronise their work first)
+    struct FreeOnError {
+        std::unique_ptr<dm_flat> &f;
+        ~FreeOnError() {
+            if (!f) return;
+            cudaDeviceSynchronize();
+            for (void *p : f->allocs) cudaFreeAsync(p, 0);
+            cudaGetLastError();
+        }
+    } free_on_error{f};
     f->device = device;
     f->nb = nb;
     f->L = L;
