@@ -187,13 +187,14 @@ __global__ void k_argmin_kernel(int32_t nb, const int32_t *__restrict__ bdd_laye
 // (one byte per node: (next-layer slot << 1) | bit, an L2-resident table):
 // one dependent byte load per layer instead of two table lookups.
 __global__ void k_argmin_walk_kernel(int32_t nb, const int32_t *__restrict__ bdd_layer_lo,
-                                     const int32_t *__restrict__ lnl, const uint8_t *__restrict__ dec,
+                                     const int32_t *__restrict__ lnl, const uint64_t *__restrict__ dec,
                                      double *__restrict__ bits) {
+    (void)lnl;
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= nb) return;
     int32_t slot = 0;  // the root
     for (int32_t l = bdd_layer_lo[j]; l < bdd_layer_lo[j + 1]; ++l) {
-        const int32_t code = dec[lnl[l] + slot];
+        const int32_t code = (int32_t)(dec[l] >> (8 * slot)) & 0xff;
         bits[l] = (double)(code & 1);
         slot = code >> 1;
     }
@@ -462,7 +463,7 @@ struct MmaArgs {
     // per position p, 8 copy records {layer, first node, w | wn<<8 | flags<<16 | k<<24, 0}
     const int4 *np_rec;
     int *task_counter;  // dynamic task queue of the node-parallel kernels
-    uint8_t *dec;       // node-parallel backward: per node (chosen next-layer slot << 1) | bit
+    uint64_t *dec;      // node-parallel backward: per layer, byte i = node i's (chosen next-layer slot << 1) | bit
 };
 
 // Progress gating: a warp whose task is far ahead of the wavefront watches a
@@ -1250,6 +1251,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         if (r.act && r.q == 0) a.lam[r.l] = lam_l;
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 3, global_ns());
         // rebuild this layer's distances to TRUE (kernels.py:340-358)
+        uint32_t db = 0;  // this lane's two decision bytes
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int i = i0 + j;
@@ -1261,12 +1263,18 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 st_relaxed(a.B + r.nlo + i, bv);
                 // the argmin walk's decision at this node (kernels.py:402-431 on
                 // the final duals and distances: same operands, same compare)
-                if (a.dec) {
-                    const int32_t t = zero_wins ? zt[j] : ot[j];
-                    a.dec[r.nlo + i] = (uint8_t)(((t >= 0 ? t - n0n : 0) << 1) | (zero_wins ? 0 : 1));
-                }
+                const int32_t t = zero_wins ? zt[j] : ot[j];
+                db |= (uint32_t)(((t >= 0 ? t - n0n : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * j);
                 if (i == 0 && r.first) a.bounds[a.layer_bdd[r.l]] = bv;  // kernels.py:359-361
             }
+        }
+        if (a.dec) {
+            // the copy's eight decision bytes meet in lane q == 0: one aligned
+            // 8-byte store per layer instead of a byte store per node
+            uint64_t w = (uint64_t)db << (16 * r.q);
+            w |= __shfl_xor_sync(kFull, w, 1);
+            w |= __shfl_xor_sync(kFull, w, 2);
+            if (r.act && r.q == 0) a.dec[r.l] = w;
         }
         if (a.trace && r.act) np_trace(a, task, r.c, r.q, 4, global_ns());
     }
@@ -1307,7 +1315,7 @@ struct dm_flat {
     int32_t *fw_pos = nullptr, *bw_pos = nullptr;
     uint8_t *layer_flags = nullptr;
     int4 *np_rec = nullptr;
-    uint8_t *dec = nullptr;          // decisions of the last node-parallel backward pass
+    uint64_t *dec = nullptr;         // decisions of the last node-parallel backward pass (one word per layer)
     const double *dec_B = nullptr;   // ... and the distance table it wrote (nullptr: none)
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
     int32_t *fw_lev = nullptr, *bw_lev = nullptr;  // levels of fw_pos / bw_pos (device)
@@ -2211,9 +2219,9 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     if (f->mma_np && !forward) {
         dm_flat *m = const_cast<dm_flat *>(f);
         if (!m->dec) {
-            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)std::max<int64_t>(f->N, 1), s));
+            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)std::max<int64_t>(f->L, 1) * 8, s));
             m->allocs.push_back(m->dec);
-            m->bytes += (size_t)std::max<int64_t>(f->N, 1);
+            m->bytes += (size_t)std::max<int64_t>(f->L, 1) * 8;
         }
         args.dec = m->dec;
         m->dec_B = B;
