@@ -120,6 +120,18 @@ __device__ __forceinline__ void st_relaxed(double *p, double x) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(x))
                  : "memory");
 }
+// p[0] = x0 (if n > 0), p[1] = x1 (if n > 1): one 16-byte relaxed store when
+// both are written and p is 16-byte aligned
+__device__ __forceinline__ void st_relaxed_pair(double *p, double x0, double x1, int n) {
+    if (n > 1 && ((uintptr_t)p & 15) == 0) {
+        asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(__double_as_longlong(x0)),
+                     "l"(__double_as_longlong(x1))
+                     : "memory");
+    } else {
+        if (n > 0) st_relaxed(p, x0);
+        if (n > 1) st_relaxed(p + 1, x1);
+    }
+}
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1122,14 +1134,17 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
         const double c0 = __dadd_rn(f0, lam_l), c1 = __dadd_rn(f1, lam_l);
         if (D) {
             // targets 2q, 2q+1 of the next layer from the per-layer source nibbles
+            double out[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int u = i0 + j;
                 const int zi = (int)(desc >> (8 * u)) & 15, oi = (int)(desc >> (8 * u + 4)) & 15;
                 const double A = nodes[zi < 8 ? zi : 8];                  // slot 8: +INF
                 const double C = __dadd_rn(nodes[oi < 8 ? oi : 8], lam_l);  // +INF + lam = +INF
-                if (r.act && !r.last && u < wn) st_relaxed(a.F + n0 + u, (C < A || (C == A && oi < zi)) ? C : A);
+                out[j] = (C < A || (C == A && oi < zi)) ? C : A;
             }
+            // one 16-byte store where the pair is aligned: 4.33 -> 4.17 ms
+            if (r.act && !r.last) st_relaxed_pair(a.F + n0 + i0, out[0], out[1], min(wn - i0, 2));
         } else {
             // generic scatter: every target is the leftmost minimum over (node
             // ascending, zero arc, one arc), gathered from all 8 nodes
@@ -1260,7 +1275,7 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
                 const double co = __dadd_rn(__dadd_rn(lam_l, to[j]), ro[j]);
                 const bool zero_wins = cz <= co;
                 const double bv = zero_wins ? cz : co;
-                st_relaxed(a.B + r.nlo + i, bv);
+                st_relaxed(a.B + r.nlo + i, bv);  // (16-byte pair stores measured 4.87 -> 5.09 ms here)
                 // the argmin walk's decision at this node (kernels.py:402-431 on
                 // the final duals and distances: same operands, same compare)
                 const int32_t t = zero_wins ? zt[j] : ot[j];

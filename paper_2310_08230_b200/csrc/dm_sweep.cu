@@ -88,8 +88,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
             vbase = s.lnl[l];
             wl = s.lnl[l + 1] - vbase;
         }
+        double vv[W];
 #pragma unroll
         for (int i = 0; i < W; ++i) {
+            vv[i] = 0.0;
             if (i < w) {
                 const int32_t a = z[i], b = o[i];
                 const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nb[a * kSweepThreads]);
@@ -97,7 +99,26 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
                     b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[b * kSweepThreads]));
                 const double v = (c0 <= c1) ? c0 : c1;
                 cur[i * kSweepThreads] = v;
-                if (kStore && i < wl) B[vbase + i] = v;
+                vv[i] = v;
+            }
+        }
+        if (kStore && wl > 0) {
+            // the layer's distances are wl consecutive doubles of this lane's
+            // diagram: 16-byte stores on the aligned pairs (each lane writes a
+            // different diagram, so every store is its own transaction)
+            const int odd = vbase & 1;
+            if (odd) B[vbase] = vv[0];
+#pragma unroll
+            for (int i = 0; i + 1 < W; i += 2) {
+                const int e = i + odd;  // first element of the aligned pair
+                if (e + 1 < wl) {
+                    double2 pr;
+                    pr.x = odd ? vv[(i + 1) % W] : vv[i];
+                    pr.y = odd ? vv[(i + 2) % W] : vv[i + 1];
+                    *reinterpret_cast<double2 *>(B + vbase + e) = pr;
+                } else if (e < wl) {
+                    B[vbase + e] = odd ? vv[(i + 1) % W] : vv[i];
+                }
             }
         }
         double *t = nb;

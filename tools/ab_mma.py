@@ -36,7 +36,13 @@ for _ in range(20):
     st.dev.k_backward_trial(st.lam_d, d, 0.37, None, bnd)
 e[1].record(); torch.cuda.synchronize()
 trial_ms = e[0].elapsed_time(e[1]) / 20
-print(json.dumps({"lib": os.environ.get("DM_LIB_PATH", os.environ.get("AB_SPEC")), "trial_ms": trial_ms, "fw_ms": min(r[0] for r in res), "bw_ms": min(r[1] for r in res),
+e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+torch.cuda.synchronize(); e[0].record()
+for _ in range(20):
+    st.dev.k_backward(st.lam_d, st.B, bnd)
+e[1].record(); torch.cuda.synchronize()
+refresh_ms = e[0].elapsed_time(e[1]) / 20
+print(json.dumps({"lib": os.environ.get("DM_LIB_PATH", os.environ.get("AB_SPEC")), "trial_ms": trial_ms, "refresh_ms": refresh_ms, "fw_ms": min(r[0] for r in res), "bw_ms": min(r[1] for r in res),
                   "lam_hash": __import__("hashlib").sha256(st.lam.tobytes()).hexdigest()[:16]}))
 '''
 
