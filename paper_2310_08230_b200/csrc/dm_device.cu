@@ -1009,7 +1009,7 @@ struct NpLaneX : NpLane {
     int32_t wn;  // width of the next layer (0 for a last layer)
 };
 
-// Two dependent loads per task: its position, then the copy's packed record.
+// One load per task and copy: the packed record, stored in task order.
 // watchdog with a lazily taken start time (no %globaltimer read per task)
 __device__ __forceinline__ bool np_watchdog(const MmaArgs &a, uint64_t &t_start, unsigned &spins) {
     if ((++spins & 63u) != 0) return false;
@@ -1027,8 +1027,7 @@ __device__ __forceinline__ NpLaneX np_lane(const MmaArgs &a, int64_t task, int l
     NpLaneX r;
     r.c = lane >> 2;
     r.q = lane & 3;
-    const int32_t p = a.task_pos[task];
-    const int4 rec = a.np_rec[(int64_t)p * kNpCopies + r.c];
+    const int4 rec = a.np_rec[task * kNpCopies + r.c];  // records stored in this pass's task order
     const unsigned m = (unsigned)rec.z;
     r.k = (int)(m >> 24);
     r.act = r.c < r.k;
@@ -1329,7 +1328,7 @@ struct dm_flat {
     bool np_ok = false, mma_np = false;
     int32_t *fw_pos = nullptr, *bw_pos = nullptr;
     uint8_t *layer_flags = nullptr;
-    int4 *np_rec = nullptr;
+    int4 *np_rec_fw = nullptr, *np_rec_bw = nullptr;  // copy records in each pass's task order
     uint64_t *dec = nullptr;         // decisions of the last node-parallel backward pass (one word per layer)
     const double *dec_B = nullptr;   // ... and the distance table it wrote (nullptr: none)
     int64_t np_fw_tasks = 0, np_bw_tasks = 0;
@@ -1864,7 +1863,7 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
     if ((rc = alloc(&f->fw_lev, P))) return rc;
     if ((rc = alloc(&f->bw_lev, P))) return rc;
     if ((rc = alloc(&plan_words, 8))) return rc;
-    if (want_np && (rc = alloc(&f->np_rec, P * 8))) return rc;
+    if (want_np && ((rc = alloc(&f->np_rec_fw, nvalid * 8)) || (rc = alloc(&f->np_rec_bw, nvalid * 8)))) return rc;
     // device plans on their own stream, after the CSR upload
     unsigned long long *relax_fail = nullptr;
     if ((rc = alloc(&relax_fail, 1))) return rc;
@@ -1913,7 +1912,10 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
                                 f->fw_lev, f->bw_pos, f->bw_lev, plan_words, ps.s))
         return DM_ERR_CUDA;
     if (vb2) cudaEventRecord(walk_ev[1], ps.s);
-    if (want_np && dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, P, f->np_rec, ps.s))
+    if (want_np && (dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, f->fw_pos, nvalid,
+                                          f->np_rec_fw, ps.s) ||
+                    dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, f->bw_pos, nvalid,
+                                          f->np_rec_bw, ps.s)))
         return DM_ERR_CUDA;
     DM_CUDA(cudaEventRecord(ps.done, ps.s));
     mark("plans queued");
@@ -2229,7 +2231,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.proc_ptr = f->proc_ptr;
     args.proc_layers = f->proc_layers;
     args.layer_flags = f->layer_flags;
-    args.np_rec = f->np_rec;
+    args.np_rec = forward ? f->np_rec_fw : f->np_rec_bw;
     args.dec = nullptr;
     if (f->mma_np && !forward) {
         dm_flat *m = const_cast<dm_flat *>(f);

@@ -85,9 +85,10 @@ int device_level_orders(const int32_t *proc_ptr, const int32_t *proc_layers, con
 // first/last-layer flags (bit 0/1) per layer
 int device_layer_flags(const int32_t *layer_bdd, const int32_t *bdd_layer_lo, int64_t L, uint8_t *flags,
                        void *stream);
-// node-parallel copy records (int4 per position and copy slot, 8 slots)
+// node-parallel copy records (int4 per task and copy slot, 8 slots): task t
+// is position order[t] (order null: t itself), P tasks
 int device_np_records(const int32_t *proc_ptr, const int32_t *proc_layers, const int32_t *lnl, const uint8_t *flags,
-                      int64_t P, void *rec, void *stream);
+                      const int32_t *order, int64_t P, void *rec, void *stream);
 
 // Uninitialised int32 buffer (every element of the sweep targets is written
 // by the parallel fill, so a value-initialising std::vector would only add a

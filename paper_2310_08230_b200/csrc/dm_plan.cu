@@ -136,9 +136,9 @@ __global__ void layer_flags_kernel(const int32_t *layer_bdd, const int32_t *bdd_
 // width | next width << 8 | flags << 16 | copies << 24, 0}; unused slots
 // {-1, 0, copies << 24, 0} (the node-parallel kernels' np_lane)
 __global__ void np_records_kernel(const int32_t *proc_ptr, const int32_t *proc_layers, const int32_t *lnl,
-                                  const uint8_t *flags, int64_t P, int4 *rec) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P * 8; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = i >> 3;
+                                  const uint8_t *flags, const int32_t *order, int64_t n, int4 *rec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * 8; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = order ? order[i >> 3] : i >> 3;
         const int c = (int)(i & 7);
         const int32_t lo = proc_ptr[p], k = proc_ptr[p + 1] - lo;
         int4 r{-1, 0, (int)((unsigned)k << 24), 0};
@@ -293,10 +293,11 @@ int device_layer_flags(const int32_t *layer_bdd, const int32_t *bdd_layer_lo, in
 }
 
 int device_np_records(const int32_t *proc_ptr, const int32_t *proc_layers, const int32_t *lnl, const uint8_t *flags,
-                      int64_t P, void *rec, void *stream) {
+                      const int32_t *order, int64_t P, void *rec, void *stream) {
     const cudaStream_t s = (cudaStream_t)stream;
     if (P > 0)
-        np_records_kernel<<<grid_for(P * 8, 256), 256, 0, s>>>(proc_ptr, proc_layers, lnl, flags, P, (int4 *)rec);
+        np_records_kernel<<<grid_for(P * 8, 256), 256, 0, s>>>(proc_ptr, proc_layers, lnl, flags, order, P,
+                                                               (int4 *)rec);
     const cudaError_t e = cudaGetLastError();
     if (e) set_error(std::string("copy records: ") + cudaGetErrorString(e));
     return e ? -1 : 0;
