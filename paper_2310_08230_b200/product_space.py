@@ -157,6 +157,89 @@ def smooth_features(mesh_ref: Mesh, dim: int, seed: int, noise: float = 0.0,
     return feats
 
 
+def geodesic_sphere(freq: int) -> Mesh:
+    """Class-I geodesic sphere: every icosahedron face cut into a freq x freq
+    triangular grid, projected to the unit sphere (20 freq^2 faces: 500 at
+    freq 5, 980 at freq 7; genus 0, consistently outward-oriented)."""
+    ico = icosphere(0)
+    key, verts, faces = {}, [], []
+
+    def vid(p):
+        p = p / np.linalg.norm(p)
+        k = tuple(np.round(p, 9))
+        if k not in key:
+            key[k] = len(verts)
+            verts.append(p)
+        return key[k]
+
+    for a, b, c in ico.faces.tolist():
+        A, B, C = ico.vertices[a], ico.vertices[b], ico.vertices[c]
+        idx = {(i, j): vid((i * A + j * B + (freq - i - j) * C) / freq)
+               for i in range(freq + 1) for j in range(freq + 1 - i)}
+        for i in range(freq):
+            for j in range(freq - i):
+                faces.append([idx[i, j], idx[i + 1, j], idx[i, j + 1]])
+                if i + j < freq - 1:
+                    faces.append([idx[i + 1, j], idx[i + 1, j + 1], idx[i, j + 1]])
+    return Mesh(np.asarray(verts, dtype=np.float64), np.asarray(faces, dtype=np.int64))
+
+
+def humanoid(mesh: Mesh) -> Mesh:
+    """Radial map of a sphere to a humanoid-like genus-0 body: flattened
+    torso with five Gaussian lobes (head, two arms, two legs)."""
+    x = mesh.vertices
+    dirs = np.array([[0, 1, 0], [0.95, 0.3, 0], [-0.95, 0.3, 0], [0.35, -0.94, 0], [-0.35, -0.94, 0]])
+    dirs = dirs / np.linalg.norm(dirs, axis=1, keepdims=True)
+    amp = np.array([0.6, 1.1, 1.1, 1.3, 1.3])
+    wid = np.array([0.10, 0.05, 0.05, 0.06, 0.06])
+    r = 1.0 + (amp[None] * np.exp(-(1.0 - x @ dirs.T) / wid[None])).sum(1)
+    y = x * r[:, None]
+    y[:, 2] *= 0.5
+    return Mesh(y, mesh.faces.copy())
+
+
+def cotan_laplacian(mesh: Mesh) -> np.ndarray:
+    """Dense cotangent stiffness matrix (V x V; meshes here have < 1000 vertices)."""
+    x, f = mesh.vertices, mesh.faces
+    W = np.zeros((len(x), len(x)))
+    for k in range(3):
+        i, j, o = f[:, (k + 1) % 3], f[:, (k + 2) % 3], f[:, k]
+        u, v = x[i] - x[o], x[j] - x[o]
+        cot = np.einsum("ij,ij->i", u, v) / np.linalg.norm(np.cross(u, v), axis=1)
+        np.add.at(W, (i, j), 0.5 * cot)
+        np.add.at(W, (j, i), 0.5 * cot)
+    return np.diag(W.sum(1)) - W
+
+
+def heat_kernel_signature(mesh: Mesh, dim: int = 16, eigs: int = 60) -> np.ndarray:
+    """Spectral descriptors: log heat kernel signature at ``dim`` log-spaced
+    times from the first ``eigs`` Laplace-Beltrami eigenpairs (lumped mixed
+    areas as mass), area-normalised per time, centred per time, rounded to
+    1e-6 so that the last-bit differences of LAPACK/BLAS builds and thread
+    counts do not reach the costs (the builder output is hashed bitwise)."""
+    L = cotan_laplacian(mesh)
+    a = mixed_vertex_areas(mesh)
+    s = 1.0 / np.sqrt(a)
+    lam, phi = np.linalg.eigh(s[:, None] * L * s[None, :])
+    lam, phi = lam[:eigs], (s[:, None] * phi)[:, :eigs]
+    ts = np.geomspace(4 * np.log(10) / lam[eigs - 1], 4 * np.log(10) / lam[1], dim)
+    h = (phi ** 2) @ np.exp(-lam[:, None] * ts[None])
+    h = np.log(h / (a[:, None] * h).sum(0, keepdims=True))
+    return np.round(h - h.mean(0), 6)
+
+
+def knn_allowed(feat_m: np.ndarray, feat_n: np.ndarray, k: int) -> np.ndarray:
+    """Symmetric k-NN pruning in descriptor space: vertex
+    pair (i, j) is kept when j is among i's k nearest or i among j's."""
+    D = ((feat_m[:, None, :] - feat_n[None, :, :]) ** 2).sum(-1)
+    al = np.zeros(D.shape, bool)
+    nm = np.argsort(D, 1, kind="stable")[:, :k]
+    nn = np.argsort(D, 0, kind="stable")[:k].T
+    al[np.repeat(np.arange(D.shape[0]), k), nm.ravel()] = True
+    al[nn.ravel(), np.repeat(np.arange(D.shape[1]), k)] = True
+    return al
+
+
 def _edge_triples(edges: np.ndarray) -> np.ndarray:
     a, b = edges[:, 0], edges[:, 1]
     pats = [(a, a, b), (a, b, a), (b, a, a), (a, b, b), (b, a, b), (b, b, a)]
@@ -342,8 +425,21 @@ def synthetic_pair(config: str, seed: int = 0):
 
     'tetra' / 'icosa'  — SPEC acceptance anchors (|P| = 368, ratio ~22);
     'c1'  — icosphere subdiv-1 pair (80 x 80), random 16-D descriptors;
-    'c2'  — deformed icosphere subdiv-2 pair (320 x 320), smooth descriptors.
+    'c2'  — deformed icosphere subdiv-2 pair (320 x 320), smooth descriptors;
+    'c3'  — deformed humanoid-like genus-0 pair (500 x 500), heat kernel
+            signatures next to the smooth descriptors (k-NN pruned, see
+            ``PRUNING_K``);
+    'c4'  — the same at 980 x 980 triangles (the ~1000 x 1000 instance).
     """
+    if config in ("c3", "c4"):
+        base = geodesic_sphere(5 if config == "c3" else 7)
+        body = humanoid(base)
+        M = deform(body, seed * 2 + 1)
+        N = deform(body, seed * 2 + 2)
+        sm = [smooth_features(base, 16, seed, noise=0.3, noise_seed=seed * 2 + s) for s in (1, 2)]
+        fm = np.hstack([heat_kernel_signature(M), sm[0]])
+        fn = np.hstack([heat_kernel_signature(N), sm[1]])
+        return M, N, fm, fn
     if config == "tetra":
         v = np.array([[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]], np.float64)
         f = np.array([[0, 1, 2], [0, 3, 1], [0, 2, 3], [1, 3, 2]], np.int64)
@@ -365,3 +461,16 @@ def synthetic_pair(config: str, seed: int = 0):
     else:
         raise ValueError(f"unknown config {config!r}")
     return M, N, fm, fn
+
+
+# k of the symmetric k-NN pruning per config (None: full product space)
+PRUNING_K = {"c3": 10, "c4": 16}
+
+
+def synthetic_product_space(config: str, seed: int = 0) -> ProductSpace:
+    """The product-space ILP of a BASELINE config, pruned where the config
+    says so (C3/C4: k-NN in descriptor space)."""
+    M, N, fm, fn = synthetic_pair(config, seed)
+    k = PRUNING_K.get(config)
+    allowed = knn_allowed(fm, fn, k) if k else None
+    return build_product_space(M, N, fm, fn, allowed=allowed)

@@ -36,8 +36,7 @@ def csr_hash(p: ps.ProductSpace) -> str:
 
 
 def product_space(cfg: str, seed: int = 0) -> ps.ProductSpace:
-    M, N, fm, fn = ps.synthetic_pair(cfg, seed)
-    return ps.build_product_space(M, N, fm, fn)
+    return ps.synthetic_product_space(cfg, seed)
 
 
 def product_case(cfg: str, seed: int = 0):

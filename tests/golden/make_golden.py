@@ -84,7 +84,29 @@ def record(name, costs, rows, chunk, iters_mma, iters_hyb, extra=None):
     return out
 
 
+def append_product_cases(configs):
+    """Record further product-space cases and merge them into golden.json
+    (``python tests/golden/make_golden.py c3``); existing cases are kept."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
+    with open(path) as fh:
+        doc = json.load(fh)
+    for cfg, chunk, im, ih in configs:
+        costs, rows, meta = product_case(cfg)
+        case = record(f"ps_{cfg}", costs, rows, chunk, im, ih, meta)
+        doc["cases"] = [c for c in doc["cases"] if c["name"] != case["name"]] + [case]
+    with open(path, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    print(path)
+
+
+# C3 (k-NN pruned humanoid-like pair, 500 x 500): a few iterations of each mode
+EXTRA = {"c3": ("c3", 128, 3, 4)}
+
+
 def main():
+    if len(sys.argv) > 1:
+        append_product_cases([EXTRA[c] for c in sys.argv[1:]])
+        return
     cases = []
     for seed in range(10):
         costs, rows = random_rows(seed)

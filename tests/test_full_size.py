@@ -11,6 +11,8 @@ GPU.  The oracle cannot run these sizes in seconds; instead:
   the full argmin sweep, bit for bit;
 * the device step search equals the host trial loop;
 * bounds never decrease across exact passes (test_dual.py:114-133).
+
+The same properties run on C4 (980 x 980 triangles, k-NN pruned, 3.5 M nodes).
 """
 
 import numpy as np
@@ -24,11 +26,13 @@ from paper_2310_08230_b200.dual import BACKWARD, FORWARD, dual_objective, init_d
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def c2():
+@pytest.fixture(scope="module", params=["c2", "c4"])
+def c2(request):
+    """The full single-GPU workloads: C2 (full product space) and C4 (the
+    ~1000 x 1000-triangle k-NN pruned pair)."""
     from bench import build_instance
 
-    return build_instance("c2", 0)
+    return build_instance(request.param, 0)
 
 
 def _feasibility(st):

@@ -1,0 +1,69 @@
+"""BASELINE configs C3/C4 (k-NN pruned humanoid-like pairs): mesh, descriptor
+and pruning invariants, on the CPU.  Their solver parity is the golden case
+``ps_c3`` (real-reference outputs, tests/golden/golden.json) and the
+full-size GPU properties on C4 (tests/test_full_size.py)."""
+
+import numpy as np
+import pytest
+
+from paper_2310_08230_b200 import product_space as ps
+
+
+@pytest.mark.parametrize("freq", [1, 2, 5, 7])
+def test_geodesic_sphere_is_closed_genus0(freq):
+    m = ps.geodesic_sphere(freq)
+    assert m.num_faces == 20 * freq * freq
+    assert m.num_vertices == 10 * freq * freq + 2
+    e = m.edges()
+    assert m.num_vertices - len(e) + m.num_faces == 2  # Euler characteristic of a sphere
+    f = m.faces
+    directed = np.concatenate([f[:, [0, 1]], f[:, [1, 2]], f[:, [2, 0]]])
+    # consistently oriented closed manifold: each directed edge once, its reverse once
+    assert len(np.unique(directed, axis=0)) == len(directed)
+    key = {tuple(x) for x in directed.tolist()}
+    assert all((b, a) in key for a, b in key)
+    x = m.vertices
+    n = np.cross(x[f[:, 1]] - x[f[:, 0]], x[f[:, 2]] - x[f[:, 0]])
+    assert ((n * x[f].mean(1)).sum(1) > 0).all()  # outward
+
+
+def test_heat_kernel_signature_is_intrinsic_and_quantised():
+    body = ps.humanoid(ps.geodesic_sphere(3))
+    h = ps.heat_kernel_signature(body)
+    assert h.shape == (body.num_vertices, 16)
+    assert np.array_equal(h, np.round(h, 6))
+    # rigid motions leave it unchanged (up to the quantisation step)
+    q, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((3, 3)))
+    moved = ps.Mesh(body.vertices @ q.T + 3.0, body.faces)
+    assert np.abs(ps.heat_kernel_signature(moved) - h).max() <= 2e-6
+
+
+def test_knn_allowed_is_symmetric_union():
+    rng = np.random.default_rng(1)
+    a, b = rng.standard_normal((30, 4)), rng.standard_normal((25, 4))
+    al = ps.knn_allowed(a, b, 3)
+    D = ((a[:, None] - b[None]) ** 2).sum(-1)
+    for i in range(30):
+        assert set(np.argsort(D[i])[:3]) <= set(np.flatnonzero(al[i]))
+    for j in range(25):
+        assert set(np.argsort(D[:, j])[:3]) <= set(np.flatnonzero(al[:, j]))
+    assert al.sum() <= 3 * (30 + 25)
+
+
+@pytest.mark.parametrize("config", ["c3", "c4"])
+def test_pruned_configs_keep_every_face_row_and_ground_truth(config):
+    p = ps.synthetic_product_space(config)
+    M, N, fm, fn = ps.synthetic_pair(config)
+    assert M.num_faces == N.num_faces == (500 if config == "c3" else 980)
+    empty = (p.row_ptr[1:] == p.row_ptr[:-1])[p.num_boundary_rows:]
+    assert not empty.any()  # every A^M / A^N projection row keeps candidates
+    full = len(M.faces) * len(N.faces) * 3
+    assert p.num_variables < full // 4  # pruned
+    # the identity correspondence (both meshes deform the same body) survives
+    # the pruning for (almost) every vertex
+    al = ps.knn_allowed(fm, fn, ps.PRUNING_K[config])
+    assert al[np.arange(len(al)), np.arange(len(al))].mean() > 0.95
+    # and its tri-tri variables are all present
+    tt = (p.kind == ps.TRI_TRI) & (p.m == p.n).all(1)  # identity corner map
+    gt_faces = np.flatnonzero(al[M.faces, N.faces].all(1))
+    assert np.array_equal(np.unique(p.face_m[tt]), gt_faces)
