@@ -248,10 +248,12 @@ def aggregate_work_time(work: float, ms: float, world: int, device=None):
 VISIBILITY_NS = 267.0
 
 
-def _traffic(kernel):
+def _traffic(kernel, config="c2"):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture summary (profiles/traffic.json, tools/ncu_summary.py), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    capture summary of this config (profiles/traffic.json for C2,
+    profiles/traffic_<config>.json otherwise; tools/ncu_summary.py), or None."""
+    name = "traffic.json" if config == "c2" else f"traffic_{config}.json"
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
     try:
         with open(path) as f:
             tr = json.load(f)
@@ -357,8 +359,7 @@ def run_b200(args, rank, world, local_rank):
             a = kernels[dom]["achieved_gbs"]
             roof = {"bound": "hbm", "kernel": dom, "achieved": round(a, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(a / hbm, 4),
-                    # the committed ncu capture is of the C2 workload
-                    "traffic": _traffic(dom) if args.config == "c2" else None,
+                    "traffic": _traffic(dom, args.config),
                     "algorithmic_bytes": kernels[dom]["bytes_per_launch"],
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
             if dom.startswith("mma"):
