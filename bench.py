@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--ttg-max-iters", type=int, default=150)
     ap.add_argument("--batch", type=int, default=0, help="also time K independent instances via qn.solve_batch")
     ap.add_argument("--batch-iters", type=int, default=30)
+    ap.add_argument("--streams", type=int, default=8, help="concurrent solves per GPU for --config c5")
     return ap.parse_args()
 
 
@@ -513,8 +514,8 @@ def run_c5(args, rank, world, local_rank):
     """Config C5: a batch of 64 independent ~500-triangle pairs (the C3
     generator, seeds 0..63), instance-sharded over ranks (rank r solves
     seeds r, r+N, ...; no collective on the data path).  One step = the
-    rank's share of the batch solved through qn.solve_batch (4 concurrent
-    streams) from the lowered HOST instances (device upload and every plan
+    rank's share of the batch solved through qn.solve_batch (--streams
+    concurrent solves) from the lowered HOST instances (device upload and every plan
     build included), --batch-iters hybrid iterations per instance; warm-up =
     W solves of the rank's first instance."""
     import torch
@@ -545,7 +546,7 @@ def run_c5(args, rank, world, local_rank):
         start.record()
         arcs = 0
         for _ in range(args.steps):
-            res = solve_batch(insts, cfg, device=dev, concurrency=4)
+            res = solve_batch(insts, cfg, device=dev, concurrency=args.streams)
             arcs += sum(r.state.arc_updates for r in res)
         end.record()
         torch.cuda.synchronize()
@@ -565,7 +566,7 @@ def run_c5(args, rank, world, local_rank):
         "instances_per_s": n_inst / (max_ms / 1e3),
         "config": {"workload": f"c5: batch of {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}; "
                                f"{args.batch_iters} hybrid iterations per instance from host arrays",
-                   "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), 4 streams per GPU",
+                   "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), {args.streams} streams per GPU",
                    "l2": "each solve uploads its instance (inputs not L2-resident across steps)"},
         "gpu_launches": _native.launch_count - l0,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d,
