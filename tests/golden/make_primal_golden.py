@@ -46,7 +46,7 @@ def h(a) -> str:
     return hashlib.sha256(a.dtype.str.encode() + a.tobytes()).hexdigest()[:32]
 
 
-def record(name, costs, rows, chunk, iters, extra=None):
+def record(name, costs, rows, chunk, iters, extra=None, recover=True):
     t0 = time.time()
     inst = IlpInstance.from_rows(np.asarray(costs, np.float64), [make_row(*r) for r in rows])
     if chunk:
@@ -74,6 +74,9 @@ def record(name, costs, rows, chunk, iters, extra=None):
             "dropped": int(inst.num_constraints - residual.num_constraints),
             "flat": {k: h(getattr(fl, k)) for k in FLAT_FIELDS},
         }
+    if not recover:  # time-budgeted branch and bound: not reproducible, fixes only
+        out["seconds"] = round(time.time() - t0, 2)
+        return out
     sol = recover_primal(inst, st, SolveConfig(max_seconds=60.0))
     out["recover"] = {"status": sol.status, "ladder_stage": sol.ladder_stage}
     if sol.assignment is not None:
@@ -87,7 +90,27 @@ def record(name, costs, rows, chunk, iters, extra=None):
     return out
 
 
+def append_fix_only(configs):
+    """``python tests/golden/make_primal_golden.py c3``: record fix_and_reduce
+    residuals of larger product spaces (their recover_primal runs into the
+    branch and bound's time budget, so it is not recorded) and merge them
+    into primal.json."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "primal.json")
+    with open(path) as fh:
+        doc = json.load(fh)
+    for cfg in configs:
+        costs, rows, meta = product_case(cfg)
+        case = record(f"ps_{cfg}", costs, rows, 128, 20, meta, recover=False)
+        doc["cases"] = [c for c in doc["cases"] if c["name"] != case["name"]] + [case]
+    with open(path, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    print(path)
+
+
 def main():
+    if len(sys.argv) > 1:
+        append_fix_only(sys.argv[1:])
+        return
     cases = []
     for seed in range(10):
         costs, rows = random_rows(seed)

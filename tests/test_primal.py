@@ -96,6 +96,8 @@ def test_recover_primal_matches_reference(case):
         assert len(partial) == g["num_fixed"]
         for k in FLAT_FIELDS:
             assert h(getattr(residual.flat, k)) == g["flat"][k], (frac, k)
+    if "recover" not in case:  # fix-only case (reference B&B hit its time budget)
+        return
     sol = primal.recover_primal(ours, st, SolveConfig(max_seconds=60.0))
     want = case["recover"]
     assert sol.status == want["status"]
