@@ -23,10 +23,10 @@ for rep in range(3):
     st = init_duals(inst, device="cuda:0", flat=flat)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    res = solve(inst, SolveConfig(mode="hybrid", max_iterations=10, dual_tolerance=0.0), device="cuda:0", state=st)
+    res = solve(inst, SolveConfig(mode="hybrid", max_iterations=50, dual_tolerance=0.0), device="cuda:0", state=st)
     lam = res.state.lam
     torch.cuda.synchronize()
     t3 = time.perf_counter()
-    print(f"rep {rep}: FlatBdds {t1 - t0:.3f}s init_duals {t2 - t1:.3f}s solve(10) {t3 - t2:.3f}s total {t3 - t0:.3f}s",
+    print(f"rep {rep}: FlatBdds {t1 - t0:.3f}s init_duals {t2 - t1:.3f}s solve(50) {t3 - t2:.3f}s total {t3 - t0:.3f}s",
           flush=True)
     del flat, st, res
