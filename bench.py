@@ -510,6 +510,11 @@ def run_reference(args, rank):
 C5_INSTANCES = 64
 
 
+def c5_seeds(rank: int, world: int) -> list:
+    """Rank r's share of the C5 batch: seeds r, r+N, ... (every seed exactly once)."""
+    return list(range(rank, C5_INSTANCES, world))
+
+
 def run_c5(args, rank, world, local_rank):
     """Config C5: a batch of 64 independent ~500-triangle pairs (the C3
     generator, seeds 0..63), instance-sharded over ranks (rank r solves
@@ -526,7 +531,7 @@ def run_c5(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    seeds = list(range(rank, C5_INSTANCES, world))
+    seeds = c5_seeds(rank, world)
     insts = [build_instance("c3", args.seed + s) for s in seeds]
     cfg = SolveConfig(mode="hybrid", max_iterations=args.batch_iters, dual_tolerance=0.0)
     h2d = sum(sum(getattr(i.flat, k).nbytes for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd",

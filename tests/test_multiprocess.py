@@ -57,3 +57,13 @@ def test_instance_sharding_aggregation_gloo():
         assert out[r][3] == pytest.approx(max(times))
     # different seeds -> different instances -> different bounds
     assert out[0][4] != out[1][4]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_c5_batch_shards_every_instance_once(world):
+    import bench
+
+    shares = [bench.c5_seeds(r, world) for r in range(world)]
+    flat = sorted(s for sh in shares for s in sh)
+    assert flat == list(range(bench.C5_INSTANCES))
+    assert max(map(len, shares)) - min(map(len, shares)) <= 1
