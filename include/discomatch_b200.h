@@ -192,6 +192,37 @@ int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bi
  * pass wrote; DM_ERR_INVALID otherwise.  Bit-identical to dm_k_argmin there. */
 int dm_k_argmin_from_pass(const dm_flat *flat, const double *B, double *bits, void *stream);
 
+/* --- deferred (throughput) averaging schedule ------------------------------
+ * FastDOG's parallel deferred min-marginal averaging (the GPU solver the
+ * paper builds on: PAPER.md:282,4924), which the reference replaced by the
+ * sequential Gauss-Seidel passes above (kernels.py:162-362)
+ * — selected by SolveConfig(mma_schedule="deferred").  Every diagram is
+ * processed independently within a pass; per copy with finite min-marginals
+ *   lam' = (lam - omega*M) + avg_in,  mbar = omega*M     (M = m1 - m0)
+ * and lam' = lam + avg_in, mbar = +inf otherwise; dm_dfr_average turns one
+ * pass's escrow mbar into the next pass's avg_in (per-variable mean of the
+ * finite mbar over the copies, in copy order; 0 for non-finite copies).
+ * mbar == NULL: no min-marginal step (a sweep that only adds avg_in: the
+ * flush that makes the duals feasible again, or a plain refresh);
+ * avg_in == NULL: nothing to add.
+ * Distance tables are INTERLEAVED (dm_dfr_table_size elements; node slot i of
+ * layer position k of a diagram's lane in the sweep layout), which only these
+ * entry points and dm_dfr_to_nodes read.  bounds[j] = optimum of diagram j
+ * under the resulting duals. */
+int dm_dfr_table_size(const dm_flat *f, int64_t *elements);
+/* forward pass: needs B_il exact for lam when mbar != NULL; writes F_il */
+int dm_dfr_forward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *B_il,
+                   double *F_il, double *mbar, double *bounds, void *stream);
+/* backward pass: needs F_il exact for lam when mbar != NULL; writes B_il and,
+ * with record_decisions (layers <= 8 nodes), the argmin decisions that
+ * dm_k_argmin_from_pass(f, B_il, ...) walks */
+int dm_dfr_backward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *F_il,
+                    double *B_il, double *mbar, double *bounds, int record_decisions, void *stream);
+/* segmented reduction over the variable CSR (proc_ptr / proc_layers) */
+int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *stream);
+/* interleaved table -> FlatBdds node order */
+int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream);
+
 /* --- vectors over dual coordinates / variables ----------------------------- */
 /* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream);

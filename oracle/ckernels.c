@@ -389,3 +389,136 @@ done:
     free(reach); free(co); free(idx);
     return result;
 }
+
+/* ------------------------------------------------------------------------
+ * Deferred (throughput) averaging schedule — restates the B200 path's
+ * FastDOG-style parallel deferred min-marginal averaging
+ * (paper_2310_08230_b200/csrc/dm_deferred.cu; the reference package has no
+ * parallel MMA: kernels.py:162-362 is the sequential pass
+ * and PAPER.md:4924 defer to FastDOG).  Per diagram, layer by layer, with
+ * the reference's min-marginal and distance formulas (kernels.py:207-228,
+ * 104-120, 142-159); per copy with finite m0, m1:
+ *     lam' = (lam - omega*(m1-m0)) + avg[l],  mbar[l] = omega*(m1-m0)
+ * else lam' = lam + avg[l], mbar[l] = +inf; avg == NULL: nothing added;
+ * mbar == NULL: no min-marginal step.  F and B are in node order here.
+ * ---------------------------------------------------------------------- */
+static double dfr_update(double lam_l, const double *avg, i64 l, double m0, double m1, double omega,
+                         double *mbar) {
+    if (m0 < INFINITY && m1 < INFINITY) {
+        double wm = omega * (m1 - m0);
+        lam_l = lam_l - wm;
+        if (avg) lam_l = lam_l + avg[l];
+        mbar[l] = wm;
+    } else {
+        if (avg) lam_l = lam_l + avg[l];
+        mbar[l] = INFINITY;
+    }
+    return lam_l;
+}
+
+static void dfr_marginals(i64 l, const i64 *lnl, const i64 *zero_t, const i64 *one_t, double lam_l,
+                          const double *F, const double *B, double *m0o, double *m1o) {
+    double m0 = INFINITY, m1 = INFINITY;
+    for (i64 v = lnl[l]; v < lnl[l + 1]; ++v) {
+        double fv = F[v];
+        if (fv == INFINITY) continue;
+        i64 a = zero_t[v], b = one_t[v];
+        double c0 = a == TGT_TRUE ? fv : (a == TGT_FALSE ? INFINITY : fv + B[a]);
+        if (c0 < m0) m0 = c0;
+        double c1 = b == TGT_TRUE ? fv + lam_l : (b == TGT_FALSE ? INFINITY : (fv + lam_l) + B[b]);
+        if (c1 < m1) m1 = c1;
+    }
+    *m0o = m0;
+    *m1o = m1;
+}
+
+void oracle_dfr_forward(i64 nb, const i64 *bdd_layer_lo, const i64 *lnl, const i64 *zero_t, const i64 *one_t,
+                        double omega, double *lam, const double *avg, const double *B, double *F, double *mbar,
+                        double *bounds) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 j = 0; j < nb; ++j) {
+        i64 l_lo = bdd_layer_lo[j], l_hi = bdd_layer_lo[j + 1];
+        i64 root = lnl[l_lo];
+        for (i64 v = root; v < lnl[l_lo + 1]; ++v) F[v] = INFINITY;
+        F[root] = 0.0;
+        double tb = INFINITY;
+        for (i64 l = l_lo; l < l_hi; ++l) {
+            double lam_l = lam[l];
+            if (mbar) {
+                double m0, m1;
+                dfr_marginals(l, lnl, zero_t, one_t, lam_l, F, B, &m0, &m1);
+                lam_l = dfr_update(lam_l, avg, l, m0, m1, omega, mbar);
+            } else if (avg) {
+                lam_l = lam_l + avg[l];
+            }
+            lam[l] = lam_l;
+            if (l + 1 < l_hi)
+                for (i64 w = lnl[l + 1]; w < lnl[l + 2]; ++w) F[w] = INFINITY;
+            for (i64 v = lnl[l]; v < lnl[l + 1]; ++v) {
+                double fv = F[v];
+                if (fv == INFINITY) continue;
+                i64 a = zero_t[v], b = one_t[v];
+                if (a >= 0) {
+                    if (fv < F[a]) F[a] = fv;
+                } else if (a == TGT_TRUE) {
+                    if (fv < tb) tb = fv;
+                }
+                double c = fv + lam_l;
+                if (b >= 0) {
+                    if (c < F[b]) F[b] = c;
+                } else if (b == TGT_TRUE) {
+                    if (c < tb) tb = c;
+                }
+            }
+        }
+        bounds[j] = tb;
+    }
+}
+
+void oracle_dfr_backward(i64 nb, const i64 *bdd_layer_lo, const i64 *lnl, const i64 *zero_t, const i64 *one_t,
+                         double omega, double *lam, const double *avg, const double *F, double *B, double *mbar,
+                         double *bounds) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (i64 j = 0; j < nb; ++j) {
+        i64 l_lo = bdd_layer_lo[j], l_hi = bdd_layer_lo[j + 1];
+        for (i64 l = l_hi - 1; l >= l_lo; --l) {
+            double lam_l = lam[l];
+            if (mbar) {
+                double m0, m1;
+                dfr_marginals(l, lnl, zero_t, one_t, lam_l, F, B, &m0, &m1);
+                lam_l = dfr_update(lam_l, avg, l, m0, m1, omega, mbar);
+            } else if (avg) {
+                lam_l = lam_l + avg[l];
+            }
+            lam[l] = lam_l;
+            for (i64 v = lnl[l]; v < lnl[l + 1]; ++v) {
+                i64 a = zero_t[v], b = one_t[v];
+                double c0 = a == TGT_TRUE ? 0.0 : (a == TGT_FALSE ? INFINITY : B[a]);
+                double c1 = b == TGT_TRUE ? lam_l : (b == TGT_FALSE ? INFINITY : lam_l + B[b]);
+                B[v] = (c0 <= c1) ? c0 : c1;
+            }
+        }
+        bounds[j] = B[lnl[l_lo]];
+    }
+}
+
+/* one pass's escrow -> next pass's per-copy average (copy order sums) */
+void oracle_dfr_average(i64 P, const i64 *proc_ptr, const i64 *proc_layers, const double *mbar, double *avg) {
+#pragma omp parallel for schedule(static)
+    for (i64 p = 0; p < P; ++p) {
+        double s = 0.0;
+        i64 c = 0;
+        for (i64 t = proc_ptr[p]; t < proc_ptr[p + 1]; ++t) {
+            double x = mbar[proc_layers[t]];
+            if (x != INFINITY) {
+                s = s + x;
+                ++c;
+            }
+        }
+        double mean = c ? s / (double)c : 0.0;
+        for (i64 t = proc_ptr[p]; t < proc_ptr[p + 1]; ++t) {
+            i64 l = proc_layers[t];
+            avg[l] = mbar[l] != INFINITY ? mean : 0.0;
+        }
+    }
+}

@@ -43,6 +43,9 @@ class _Lib:
                 "oracle_k_min_marginals": ([_I] + [_P] * 8, None),
                 "oracle_k_argmin": ([_I] + [_P] * 7, None),
                 "oracle_equality_tables": ([_I, _P, _I, _P, _P, _P], _I),
+                "oracle_dfr_forward": ([_I, _P, _P, _P, _P, _D] + [_P] * 6, None),
+                "oracle_dfr_backward": ([_I, _P, _P, _P, _P, _D] + [_P] * 6, None),
+                "oracle_dfr_average": ([_I, _P, _P, _P, _P], None),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(h, name)

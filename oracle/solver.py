@@ -143,6 +143,30 @@ class OracleDual:
         self.sweeps += 2
         self._set_bound()
 
+    def deferred_round(self, omega):
+        """The B200 path's deferred (FastDOG) averaging round
+        (DualState.deferred_round, csrc/dm_deferred.cu) on node-order tables:
+        forward pass (escrow), average, backward pass (adds it, new escrow),
+        average, flush sweep."""
+        f = self.flat
+        if not self.b_valid:
+            self.refresh_backward()
+        P = len(f.proc_ptr) - 1
+        mbar = np.zeros(f.num_layers)
+        avg = np.zeros(f.num_layers)
+        geo = (f.num_bdds, ptr(f.bdd_layer_lo), ptr(f.layer_node_lo), ptr(f.zero_t), ptr(f.one_t))
+        lib.oracle_dfr_forward(*geo, float(omega), ptr(self.lam), None, ptr(self.B), ptr(self.F), ptr(mbar),
+                               ptr(self.bounds))
+        lib.oracle_dfr_average(P, ptr(f.proc_ptr), ptr(f.proc_layers), ptr(mbar), ptr(avg))
+        lib.oracle_dfr_backward(*geo, float(omega), ptr(self.lam), ptr(avg), ptr(self.F), ptr(self.B), ptr(mbar),
+                                ptr(self.bounds))
+        lib.oracle_dfr_average(P, ptr(f.proc_ptr), ptr(f.proc_layers), ptr(mbar), ptr(avg))
+        lib.oracle_dfr_backward(*geo, 0.0, ptr(self.lam), ptr(avg), None, ptr(self.B), None, ptr(self.bounds))
+        self.sweeps += 5
+        self.f_valid, self.b_valid = False, True
+        self._set_bound()
+        return mbar, avg
+
     def subgradient(self):
         """dual.py:189-201"""
         f = self.flat
@@ -226,8 +250,10 @@ def step_search(st: OracleDual, d, gamma_prev, shrink, grow, trials, min_ascent)
 def solve(inst: OracleInstance, mode="hybrid", max_iterations=2000, dual_tolerance=1e-10,
           curvature_eps=1e-8, grow=1.1, shrink=0.8, trials=5, ascent_rel=1e-6,
           initial_step=1.0, memory=10, max_seconds=None, dot="blas", flat=None,
-          clock=time.perf_counter, threads=None):
-    """qn.py:184-259; returns (state, records[(it, kind, bound, t)], stop_reason)."""
+          clock=time.perf_counter, threads=None, schedule="exact", damping=0.5, stall_window=None):
+    """qn.py:184-259; returns (state, records[(it, kind, bound, t)], stop_reason).
+    ``schedule="deferred"`` replaces the two exact passes of every iteration by
+    the B200 path's deferred averaging round (OracleDual.deferred_round)."""
     if threads is not None:
         lib.oracle_set_threads(int(threads))
     dotf = _dot_blas if dot == "blas" else _dot_chunked
@@ -251,8 +277,11 @@ def solve(inst: OracleInstance, mode="hybrid", max_iterations=2000, dual_toleran
             if better:
                 st.shift(gamma * d)
                 used = True
-        st.mma(True)
-        st.mma(False)
+        if schedule == "deferred":
+            st.deferred_round(damping)
+        else:
+            st.mma(True)
+            st.mma(False)
         bound = st.objective()
         records.append((it, "hybrid" if used else "mma", bound, clock() - t0))
         if it == 1:
@@ -266,9 +295,17 @@ def solve(inst: OracleInstance, mode="hybrid", max_iterations=2000, dual_toleran
                 hist.appendleft((s, y, 1.0 / sy, sy))
             lam_prev = st.lam.copy()
             g_prev = g_now
-        if bound - records[-2][2] < dual_tolerance * max(1.0, abs(bound)):
-            reason = "dual_tolerance"
-            break
+        k = stall_window if stall_window is not None else (8 if schedule == "deferred" else 1)
+        if k == 1:
+            if bound - records[-2][2] < dual_tolerance * max(1.0, abs(bound)):
+                reason = "dual_tolerance"
+                break
+        elif it >= k:  # best-bound gain over the last k iterations (SolveConfig.stall_window)
+            recent = max(r[2] for r in records[-k:])
+            before = max(r[2] for r in records[:-k])
+            if recent - before < dual_tolerance * max(1.0, abs(bound)):
+                reason = "dual_tolerance"
+                break
         if max_seconds is not None and clock() - t0 > max_seconds:
             reason = "max_seconds"
             break

@@ -1,0 +1,437 @@
+// Deferred (throughput) min-marginal averaging schedule — the parallel MMA of
+// FastDOG (Abbas & Swoboda 2022) that the paper runs on its GPU
+// ("for parallel min-marginal averaging we use the dual
+// optimisation algorithm of [FastDOG]"); the reference package replaced it by
+// a sequential Gauss-Seidel sweep (kernels.py:162-362).
+//
+// Within one pass every diagram is independent: at layer l of diagram j the
+// pass computes the copy's min-marginal difference M with the distances of
+// its own diagram only (the opposite-direction table is still exact there,
+// since no later layer of j has changed in this pass), moves the dual by
+// -omega*M and keeps omega*M in escrow (mbar[l]); the copy also receives the
+// average escrow its variable's copies left in the PREVIOUS pass (avg[l]).
+// So the sum over a variable's copies of (lam + mbar) stays equal to its
+// cost.  dfr_average_kernel turns one pass's escrow into the next pass's
+// per-copy average (a segmented reduction over the variable CSR), and a pass
+// without the min-marginal step (mbar == null) redistributes the last escrow
+// and rebuilds the table: after it the duals are feasible again.
+//
+//   lam' = (lam - omega*M) + avg      copies with finite m0, m1 (mbar = omega*M)
+//   lam' =  lam + avg                 otherwise                (mbar = +inf)
+//   avg  = (sum of finite mbar over the variable's copies, in copy order)
+//          / (their count), 0.0 for non-finite copies
+//
+// M is taken on the duals BEFORE the deferred average is added (FastDOG's
+// order).  Arithmetic is binary64 with explicit roundings (-fmad=false), the
+// per-diagram order is the reference's (m0/m1 as kernels.py:207-228,
+// distances as kernels.py:104-120 / 142-159), so oracle/ckernels.c
+// (oracle_dfr_*) reproduces every output bit for bit.
+//
+// Layout: the interleaved sweep layout (dm_layout.cpp) — 32 diagrams of
+// similar shape per warp, one lane per diagram, node slot (k, i) of lane t at
+// element (pos_slot[k] + i) * 32 + t.  The passes keep BOTH distance tables
+// in that layout (F_il / B_il), so every table access of a warp is one
+// 128-byte row per node slot; only lam / avg / mbar are per-lane gathers
+// (consecutive layers of one diagram, so a lane walks its own cache lines).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "dm_internal.h"
+
+#define DM_INF __longlong_as_double(0x7ff0000000000000LL)
+
+namespace {
+
+constexpr int kThreads = 128;
+
+struct DfrArgs {
+    dm::SweepDev s;
+    double omega;
+    double *lam;
+    const double *avg;   // null: no deferred average to add
+    const double *in;    // opposite-direction table (interleaved), null without the MM step
+    double *out;         // this direction's table (interleaved)
+    double *mbar;        // escrow out (null: no min-marginal step)
+    double *bounds;      // per-diagram optimum of the resulting duals
+    uint64_t *dec;       // backward only: argmin decisions, one word per layer (W <= 8)
+};
+
+__device__ __forceinline__ double c_zero(int32_t a, double fv, const double *nb) {
+    return a == dm::kTrue ? fv : (a == dm::kFalse ? DM_INF : __dadd_rn(fv, nb[a * kThreads]));
+}
+__device__ __forceinline__ double c_one(int32_t b, double fl, const double *nb) {  // fl = fv + lam
+    return b == dm::kTrue ? fl : (b == dm::kFalse ? DM_INF : __dadd_rn(fl, nb[b * kThreads]));
+}
+
+// the dual update of one copy (see the header); returns lam'
+template <bool kAvg>
+__device__ __forceinline__ double dfr_update(double lam_l, double a_l, double m0, double m1, double omega,
+                                             double *mbar_slot) {
+    if (m0 < DM_INF && m1 < DM_INF) {
+        const double wm = __dmul_rn(omega, __dsub_rn(m1, m0));
+        lam_l = __dsub_rn(lam_l, wm);
+        if (kAvg) lam_l = __dadd_rn(lam_l, a_l);
+        *mbar_slot = wm;
+    } else {
+        if (kAvg) lam_l = __dadd_rn(lam_l, a_l);
+        *mbar_slot = DM_INF;
+    }
+    return lam_l;
+}
+
+// Backward direction: positions k = 0 (every lane's last layer) .. K-1.
+template <int W, bool kMM, bool kAvg, bool kDec>
+__global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
+    extern __shared__ double sm[];
+    const dm::SweepDev &s = a.s;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = s.bdd_layer_lo[j];
+        nj = s.bdd_layer_lo[j + 1] - l0;
+    }
+    const int32_t K = s.grp_npos[g];
+    const int64_t p0 = s.grp_pos_lo[g];
+    double *nb = sm + threadIdx.x;                  // distances of position k-1 (next layer)
+    double *cur = sm + W * kThreads + threadIdx.x;  // position k
+    // register double buffer: position k+1's arcs, F row and duals load while k computes
+    int32_t za[W], oa[W];
+    double fa[W];
+    double lam_n = 0.0, avg_n = 0.0;
+    int32_t w_n = 0;
+    int64_t slot_n = 0;
+    auto fetch = [&](int32_t k) {
+        w_n = s.pos_width[p0 + k];
+        slot_n = s.pos_slot[p0 + k];
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w_n) {
+                const int64_t e = (slot_n + i) * 32 + lane;
+                za[i] = s.zl[e];
+                oa[i] = s.ol[e];
+                if (kMM) fa[i] = a.in[e];
+            }
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            lam_n = a.lam[l];
+            if (kAvg) avg_n = a.avg[l];
+        }
+    };
+    if (K > 0) fetch(0);
+    for (int32_t k = 0; k < K; ++k) {
+        const int32_t w = w_n;
+        const int64_t slot = slot_n;
+        int32_t z[W], o[W];
+        double f[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            z[i] = za[i];
+            o[i] = oa[i];
+            if (kMM) f[i] = fa[i];
+        }
+        const bool act = k < nj;
+        const int32_t l = l0 + nj - 1 - k;
+        double lam_l = act ? lam_n : 0.0;
+        const double a_l = avg_n;
+        if (k + 1 < K) fetch(k + 1);
+        if (act && (kMM || kAvg)) {
+            if (kMM) {
+                double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+                for (int i = 0; i < W; ++i)
+                    if (i < w) {
+                        const double c0 = c_zero(z[i], f[i], nb);
+                        const double c1 = c_one(o[i], __dadd_rn(f[i], lam_l), nb);
+                        if (c0 < m0) m0 = c0;
+                        if (c1 < m1) m1 = c1;
+                    }
+                lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, a.mbar + l);
+            } else {
+                lam_l = __dadd_rn(lam_l, a_l);
+            }
+            a.lam[l] = lam_l;
+        }
+        uint64_t word = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w) {
+                const int32_t za_ = z[i], ob = o[i];
+                const double c0 = za_ == dm::kTrue ? 0.0 : (za_ == dm::kFalse ? DM_INF : nb[za_ * kThreads]);
+                const double c1 =
+                    ob == dm::kTrue ? lam_l : (ob == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[ob * kThreads]));
+                const bool zero_wins = c0 <= c1;
+                const double v = zero_wins ? c0 : c1;
+                cur[i * kThreads] = v;
+                a.out[(slot + i) * 32 + lane] = v;
+                if (kDec && W <= 8) {
+                    const int32_t t = zero_wins ? za_ : ob;
+                    word |= (uint64_t)((((t >= 0) ? t : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * i);
+                }
+            }
+        if (kDec && W <= 8 && act) a.dec[l] = word;
+        double *t = nb;
+        nb = cur;
+        cur = t;
+        if (act && k == nj - 1) a.bounds[j] = nb[0];  // root layer: single node
+    }
+}
+
+// Forward direction: positions k = K-1 .. 0; lanes whose diagram is shorter
+// than the group's longest idle until their root position.
+template <int W, bool kMM, bool kAvg>
+__global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
+    extern __shared__ double sm[];
+    const dm::SweepDev &s = a.s;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = s.bdd_layer_lo[j];
+        nj = s.bdd_layer_lo[j + 1] - l0;
+    }
+    const int32_t K = s.grp_npos[g];
+    const int64_t p0 = s.grp_pos_lo[g];
+    double *cur = sm + threadIdx.x;                  // distances from the root, position k
+    double *nxt = sm + W * kThreads + threadIdx.x;   // position k-1
+    double *bn = sm + 2 * W * kThreads + threadIdx.x;  // B of position k-1 (kMM)
+    double tb = DM_INF;
+    // register double buffer for position k-1
+    int32_t za[W], oa[W];
+    double ba[W];
+    double lam_n = 0.0, avg_n = 0.0;
+    int32_t w_n = 0, wb_n = 0;
+    int64_t slot_n = 0;
+    auto fetch = [&](int32_t k) {  // k < nj
+        w_n = s.pos_width[p0 + k];
+        slot_n = s.pos_slot[p0 + k];
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w_n) {
+                const int64_t e = (slot_n + i) * 32 + lane;
+                za[i] = s.zl[e];
+                oa[i] = s.ol[e];
+            }
+        const int32_t l = l0 + nj - 1 - k;
+        lam_n = a.lam[l];
+        if (kAvg) avg_n = a.avg[l];
+        if (kMM) {
+            wb_n = k > 0 ? s.pos_width[p0 + k - 1] : 0;
+            const int64_t sb = k > 0 ? s.pos_slot[p0 + k - 1] : 0;
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                if (u < wb_n) ba[u] = a.in[(sb + u) * 32 + lane];
+        }
+    };
+    if (nj > 0) fetch(nj - 1);
+    for (int32_t k = K - 1; k >= 0; --k) {
+        if (k >= nj) continue;
+        const int32_t w = w_n;
+        const int64_t slot = slot_n;
+        const int32_t wn = k > 0 ? s.pos_width[p0 + k - 1] : 0;
+        int32_t z[W], o[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            z[i] = za[i];
+            o[i] = oa[i];
+        }
+        if (kMM) {
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                if (u < wb_n) bn[u * kThreads] = ba[u];
+        }
+        double lam_l = lam_n;
+        const double a_l = avg_n;
+        if (k > 0) fetch(k - 1);
+        const int32_t l = l0 + nj - 1 - k;
+        if (k == nj - 1) {  // root layer: F[root] = 0 (kernels.py:187-193)
+            cur[0] = 0.0;
+#pragma unroll
+            for (int i = 1; i < W; ++i) cur[i * kThreads] = DM_INF;
+        }
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w) a.out[(slot + i) * 32 + lane] = cur[i * kThreads];
+        if (kMM) {
+            double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < w) {
+                    const double fv = cur[i * kThreads];
+                    const double c0 = c_zero(z[i], fv, bn);
+                    const double c1 = c_one(o[i], __dadd_rn(fv, lam_l), bn);
+                    if (c0 < m0) m0 = c0;
+                    if (c1 < m1) m1 = c1;
+                }
+            lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, a.mbar + l);
+            a.lam[l] = lam_l;
+        } else if (kAvg) {
+            lam_l = __dadd_rn(lam_l, a_l);
+            a.lam[l] = lam_l;
+        }
+        // push this layer's distances into the next one (kernels.py:241-269)
+#pragma unroll
+        for (int u = 0; u < W; ++u)
+            if (u < wn) nxt[u * kThreads] = DM_INF;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w) {
+                const double fv = cur[i * kThreads];
+                if (fv == DM_INF) continue;
+                const int32_t za_ = z[i], ob = o[i];
+                if (za_ >= 0) {
+                    if (fv < nxt[za_ * kThreads]) nxt[za_ * kThreads] = fv;
+                } else if (za_ == dm::kTrue) {
+                    if (fv < tb) tb = fv;
+                }
+                const double c = __dadd_rn(fv, lam_l);
+                if (ob >= 0) {
+                    if (c < nxt[ob * kThreads]) nxt[ob * kThreads] = c;
+                } else if (ob == dm::kTrue) {
+                    if (c < tb) tb = c;
+                }
+            }
+        double *t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    if (j >= 0) a.bounds[j] = tb;
+}
+
+// One pass's escrow -> the next pass's per-copy average: thread per
+// visitation position (variable), copies summed in copy order.
+__global__ void dfr_average_kernel(int32_t P, const int32_t *__restrict__ proc_ptr,
+                                   const int32_t *__restrict__ proc_layers, const double *__restrict__ mbar,
+                                   double *__restrict__ avg) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
+    if (hi == lo) return;
+    constexpr int kReg = 8;  // copies held in registers; the rest re-read
+    double v[kReg];
+    int32_t ls[kReg];
+    double sum = 0.0;
+    int32_t cnt = 0;
+    for (int32_t t = lo; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        const double x = mbar[l];
+        if (t - lo < kReg) {
+            v[t - lo] = x;
+            ls[t - lo] = l;
+        }
+        if (x != DM_INF) {
+            sum = __dadd_rn(sum, x);
+            ++cnt;
+        }
+    }
+    const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
+    for (int32_t t = lo; t < hi; ++t) {
+        double x;
+        int32_t l;
+        if (t - lo < kReg) {
+            x = v[t - lo];
+            l = ls[t - lo];
+        } else {
+            l = proc_layers[t];
+            x = mbar[l];
+        }
+        avg[l] = x != DM_INF ? mean : 0.0;
+    }
+}
+
+// interleaved table -> reference node order (tests, and consumers of F / B)
+__global__ void dfr_to_nodes_kernel(dm::SweepDev s, const double *__restrict__ x_il, double *__restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    if (j < 0) return;
+    const int32_t l0 = s.bdd_layer_lo[j], nj = s.bdd_layer_lo[j + 1] - l0;
+    const int64_t p0 = s.grp_pos_lo[g];
+    for (int32_t k = 0; k < nj; ++k) {
+        const int32_t l = l0 + nj - 1 - k;
+        const int32_t v0 = s.lnl[l], w = s.lnl[l + 1] - v0;
+        const int64_t slot = s.pos_slot[p0 + k];
+        for (int32_t i = 0; i < w; ++i) x[v0 + i] = x_il[(slot + i) * 32 + lane];
+    }
+}
+
+int fail(cudaError_t e, const char *what) {
+    dm::set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return DM_ERR_CUDA;
+}
+
+template <typename Kern>
+int launch(Kern kern, const DfrArgs &a, size_t smem, cudaStream_t st, const char *what) {
+    const int blocks = (int)((a.s.groups * 32 + kThreads - 1) / kThreads);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<blocks, kThreads, smem, st>>>(a);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, what);
+}
+
+template <int W>
+int backward_w(const DfrArgs &a, cudaStream_t st) {
+    const size_t smem = 2 * W * kThreads * sizeof(double);
+    const bool mm = a.mbar != nullptr, avg = a.avg != nullptr, dec = a.dec != nullptr && W <= 8;
+    if (mm && avg) return launch(dfr_backward_kernel<W, true, true, false>, a, smem, st, "dfr_backward");
+    if (mm) return launch(dfr_backward_kernel<W, true, false, false>, a, smem, st, "dfr_backward");
+    if (avg && dec) return launch(dfr_backward_kernel<W, false, true, true>, a, smem, st, "dfr_backward");
+    if (avg) return launch(dfr_backward_kernel<W, false, true, false>, a, smem, st, "dfr_backward");
+    if (dec) return launch(dfr_backward_kernel<W, false, false, true>, a, smem, st, "dfr_backward");
+    return launch(dfr_backward_kernel<W, false, false, false>, a, smem, st, "dfr_backward");
+}
+
+template <int W>
+int forward_w(const DfrArgs &a, cudaStream_t st) {
+    const size_t smem = 3 * W * kThreads * sizeof(double);
+    const bool mm = a.mbar != nullptr, avg = a.avg != nullptr;
+    if (mm && avg) return launch(dfr_forward_kernel<W, true, true>, a, smem, st, "dfr_forward");
+    if (mm) return launch(dfr_forward_kernel<W, true, false>, a, smem, st, "dfr_forward");
+    if (avg) return launch(dfr_forward_kernel<W, false, true>, a, smem, st, "dfr_forward");
+    return launch(dfr_forward_kernel<W, false, false>, a, smem, st, "dfr_forward");
+}
+
+}  // namespace
+
+namespace dm {
+
+int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const double *avg, const double *in,
+             double *out, double *mbar, double *bounds, uint64_t *dec, void *stream) {
+    if (s.groups == 0) return DM_OK;
+    DfrArgs a{s, omega, lam, avg, in, out, mbar, bounds, forward ? nullptr : dec};
+    cudaStream_t st = (cudaStream_t)stream;
+    if (forward) {
+        if (s.max_width <= 8) return forward_w<8>(a, st);
+        if (s.max_width <= 16) return forward_w<16>(a, st);
+        return forward_w<32>(a, st);
+    }
+    if (s.max_width <= 8) return backward_w<8>(a, st);
+    if (s.max_width <= 16) return backward_w<16>(a, st);
+    return backward_w<32>(a, st);
+}
+
+int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *avg,
+                void *stream) {
+    if (P == 0) return DM_OK;
+    constexpr int kT = 256;
+    dfr_average_kernel<<<(int)((P + kT - 1) / kT), kT, 0, (cudaStream_t)stream>>>((int32_t)P, proc_ptr, proc_layers,
+                                                                                   mbar, avg);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, "dfr_average");
+}
+
+int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream) {
+    if (s.groups == 0) return DM_OK;
+    const int blocks = (int)((s.groups * 32 + kThreads - 1) / kThreads);
+    dfr_to_nodes_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(s, x_il, x);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, "dfr_to_nodes");
+}
+
+}  // namespace dm

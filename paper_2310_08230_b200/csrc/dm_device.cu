@@ -2296,6 +2296,68 @@ int dm_k_argmin_from_pass(const dm_flat *f, const double *B, double *bits, void 
     return check_stream_error("k_argmin_walk");
 }
 
+// --- deferred (throughput) averaging schedule: dm_deferred.cu -------------
+int dm_dfr_table_size(const dm_flat *f, int64_t *elements) {
+    DM_CHECK_FLAT(f);
+    if (!elements) {
+        dm::set_error("dm_dfr_table_size: null output");
+        return DM_ERR_INVALID;
+    }
+    *elements = f->sweep.slots * 32;
+    return DM_OK;
+}
+
+int dm_dfr_forward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *B_il,
+                   double *F_il, double *mbar, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!lam || !F_il || !bounds || (mbar && !B_il)) {
+        dm::set_error("dm_dfr_forward: lam, F_il, bounds (and B_il with mbar) are required");
+        return DM_ERR_INVALID;
+    }
+    if (f->dec_B == F_il) const_cast<dm_flat *>(f)->dec_B = nullptr;
+    return dm::dfr_pass(f->sweep, true, omega, lam, avg_in, B_il, F_il, mbar, bounds, nullptr, stream);
+}
+
+int dm_dfr_backward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *F_il,
+                    double *B_il, double *mbar, double *bounds, int record_decisions, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!lam || !B_il || !bounds || (mbar && !F_il)) {
+        dm::set_error("dm_dfr_backward: lam, B_il, bounds (and F_il with mbar) are required");
+        return DM_ERR_INVALID;
+    }
+    dm_flat *m = const_cast<dm_flat *>(f);
+    uint64_t *dec = nullptr;
+    if (record_decisions && f->sweep.max_width <= 8 && f->L > 0) {
+        if (!m->dec) {
+            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)f->L * 8, (cudaStream_t)stream));
+            m->allocs.push_back(m->dec);
+            m->bytes += (size_t)f->L * 8;
+        }
+        dec = m->dec;
+    }
+    const int rc = dm::dfr_pass(f->sweep, false, omega, lam, avg_in, F_il, B_il, mbar, bounds, dec, stream);
+    m->dec_B = (rc == DM_OK && dec) ? B_il : (m->dec_B == B_il ? nullptr : m->dec_B);
+    return rc;
+}
+
+int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!mbar || !avg_in) {
+        dm::set_error("dm_dfr_average: null vector");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, avg_in, stream);
+}
+
+int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!x_il || !x) {
+        dm::set_error("dm_dfr_to_nodes: null table");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_to_nodes(f->sweep, x_il, x, stream);
+}
+
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {
     DM_CHECK_FLAT(f);
     if (f->L == 0) return DM_OK;

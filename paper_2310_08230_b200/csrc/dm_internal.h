@@ -131,7 +131,7 @@ bool build_relax_by_layer(const int64_t *bdd_layer_lo, int64_t nb, const int64_t
 // Device view of a SweepLayout plus the reference-layout offsets the sweeps
 // need to read duals and write distances (dm_sweep.cu).
 struct SweepDev {
-    int64_t groups = 0;
+    int64_t groups = 0, slots = 0;  // slots * 32 = elements of an interleaved table
     int32_t max_width = 0;
     const int32_t *grp_bdd = nullptr, *grp_npos = nullptr, *pos_width = nullptr;
     const int64_t *grp_pos_lo = nullptr, *pos_slot = nullptr;
@@ -164,6 +164,15 @@ constexpr int64_t kDotChunk = 4096;
 // s = lam - lam_prev, y = g_prev - g, lam_prev = lam and sy = s . y (chunked-dot order), one pass
 int curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
                    double *y, int64_t n, double *partial, double *sy, void *stream);
+// Deferred (throughput) averaging schedule (dm_deferred.cu): one pass over
+// every diagram, forward or backward, on interleaved tables; mbar == null:
+// no min-marginal step (a sweep that only adds avg); avg == null: nothing to
+// add; dec (backward, W <= 8): argmin decision words per layer.
+int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const double *avg, const double *in,
+             double *out, double *mbar, double *bounds, uint64_t *dec, void *stream);
+int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *avg,
+                void *stream);
+int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream);
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
 

@@ -490,6 +490,7 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
             break;
         }
         sd.max_width = (int32_t)host[1];
+        sd.slots = slots;
         if ((e = dalloc(&zl, slots * 32, s, allocs, bytes)) || (e = dalloc(&ol, slots * 32, s, allocs, bytes))) break;
         e = cudaGetLastError();
         mark("allocated");

@@ -13,6 +13,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from .config import SCHEDULE_DEFERRED, SCHEDULE_EXACT
 from .ilp import IlpInstance
 from .kernels import DeviceFlat, FlatBdds, dev_axpy_host, dev_sum
 
@@ -73,7 +74,11 @@ class KernelTimer:
 class DualState:
     """Per-constraint duals plus cached sweep distances, resident on a GPU."""
 
-    def __init__(self, instance: IlpInstance, flat: FlatBdds | None = None, device=None):
+    def __init__(self, instance: IlpInstance, flat: FlatBdds | None = None, device=None,
+                 schedule: str = SCHEDULE_EXACT):
+        if schedule not in (SCHEDULE_EXACT, SCHEDULE_DEFERRED):
+            raise ValueError(f"unknown averaging schedule {schedule!r}")
+        self.schedule = schedule
         self.instance = instance
         self.flat = flat if flat is not None else FlatBdds(instance)
         self.dev: DeviceFlat = self.flat.device(device)
@@ -102,6 +107,15 @@ class DualState:
         self._bgen = 0  # generation of the distance-to-TRUE table B
         self._argmin_cache = None
         self._dec_gen = -1  # B generation whose argmin decisions the last backward pass recorded
+        if schedule == SCHEDULE_DEFERRED:
+            # the deferred schedule keeps its distance tables in the sweep
+            # layout (dm_dfr_*): f_valid / b_valid then refer to F_il / B_il,
+            # and the node-order F / B are filled from them on demand
+            n = self.dev.dfr_table_size()
+            self.F_il = torch.zeros(n, dtype=_F64, device=d)
+            self.B_il = torch.zeros(n, dtype=_F64, device=d)
+            self.mbar = torch.zeros(f.num_layers, dtype=_F64, device=d)  # escrow of the last pass
+            self.avg = torch.zeros(f.num_layers, dtype=_F64, device=d)  # its per-copy average
         free = instance.unconstrained_variables()
         self.free_values = {int(v): (0 if instance.costs[v] >= 0 else 1) for v in free}
         self.free_contribution = float(np.minimum(instance.costs[free], 0.0).sum()) if len(free) else 0.0
@@ -177,17 +191,83 @@ class DualState:
         self._pending = []
         self._best_bound = v
 
+    @property
+    def deferred(self) -> bool:
+        return self.schedule == SCHEDULE_DEFERRED
+
     def refresh_backward(self) -> None:
-        self.dev.k_backward(self.lam_d, self.B, self._bounds)
+        if self.deferred:
+            self.dev.dfr_backward(0.0, self.lam_d, None, None, self.B_il, None, self._bounds, record_decisions=True)
+            self._bgen += 1
+            if self.dev.dfr_records_decisions:
+                self._dec_gen = self._bgen
+        else:
+            self.dev.k_backward(self.lam_d, self.B, self._bounds)
+            self._bgen += 1
         self.sweeps += 1
-        self._bgen += 1
         self.b_valid = True
         self._set_bound()
 
     def refresh_forward(self) -> None:
-        self.dev.k_forward(self.lam_d, self.F, self._bounds)
+        if self.deferred:
+            self.dev.dfr_forward(0.0, self.lam_d, None, None, self.F_il, None, self._bounds)
+        else:
+            self.dev.k_forward(self.lam_d, self.F, self._bounds)
         self.sweeps += 1
         self.f_valid = True
+        self._set_bound()
+
+    def node_tables(self, need_f: bool = True, need_b: bool = True) -> tuple[torch.Tensor, torch.Tensor]:
+        """Node-order (FlatBdds) F and B valid for the current duals; under
+        the deferred schedule they are converted from the interleaved tables."""
+        if need_f and not self.f_valid:
+            self.refresh_forward()
+        if need_b and not self.b_valid:
+            self.refresh_backward()
+        if self.deferred:
+            if need_f:
+                self.dev.dfr_to_nodes(self.F_il, self.F)
+            if need_b:
+                self.dev.dfr_to_nodes(self.B_il, self.B)
+        return self.F, self.B
+
+    def deferred_round(self, omega: float) -> None:
+        """One round of the deferred (FastDOG) schedule: a forward and a
+        backward averaging pass over all diagrams in parallel, each copy's
+        escrow redistributed by the next pass, and a final sweep that adds the
+        backward pass's escrow and rebuilds B (dm_deferred.cu).  The duals are
+        feasible again afterwards; the bound of the new duals is queued."""
+        if not self.deferred:
+            raise ValueError("deferred_round needs a state built with schedule='deferred'")
+        timer = self.pass_timer
+        if not self.b_valid:
+            self.refresh_backward()
+        ev = timer.begin("dfr_forward") if timer else None
+        self.dev.dfr_forward(omega, self.lam_d, None, self.B_il, self.F_il, self.mbar, self._bounds)
+        if ev:
+            timer.end(ev)
+        ev = timer.begin("dfr_average") if timer else None
+        self.dev.dfr_average(self.mbar, self.avg)
+        if ev:
+            timer.end(ev)
+        ev = timer.begin("dfr_backward") if timer else None
+        self.dev.dfr_backward(omega, self.lam_d, self.avg, self.F_il, self.B_il, self.mbar, self._bounds)
+        if ev:
+            timer.end(ev)
+        ev = timer.begin("dfr_average") if timer else None
+        self.dev.dfr_average(self.mbar, self.avg)
+        if ev:
+            timer.end(ev)
+        ev = timer.begin("dfr_flush") if timer else None
+        self.dev.dfr_backward(0.0, self.lam_d, self.avg, None, self.B_il, None, self._bounds, record_decisions=True)
+        if ev:
+            timer.end(ev)
+        self._bgen += 1
+        if self.dev.dfr_records_decisions:
+            self._dec_gen = self._bgen
+        self.sweeps += 5
+        self.b_valid = True
+        self.f_valid = False
         self._set_bound()
 
     def shift_lambda(self, delta) -> None:
@@ -266,13 +346,10 @@ class DualState:
         return res
 
     def min_marginal_table_device(self) -> tuple[torch.Tensor, torch.Tensor]:
-        if not self.f_valid:
-            self.refresh_forward()
-        if not self.b_valid:
-            self.refresh_backward()
+        F, B = self.node_tables()
         m0 = torch.empty(self.flat.num_layers, dtype=_F64, device=self.device)
         m1 = torch.empty_like(m0)
-        self.dev.k_min_marginals(self.lam_d, self.F, self.B, m0, m1)
+        self.dev.k_min_marginals(self.lam_d, F, B, m0, m1)
         return m0, m1
 
     def min_marginal_table(self) -> tuple[np.ndarray, np.ndarray]:
@@ -281,9 +358,10 @@ class DualState:
         return m0.cpu().numpy(), m1.cpu().numpy()
 
 
-def init_duals(instance: IlpInstance, device=None, flat: FlatBdds | None = None) -> DualState:
+def init_duals(instance: IlpInstance, device=None, flat: FlatBdds | None = None,
+               schedule: str = SCHEDULE_EXACT) -> DualState:
     """Spread every cost uniformly over the constraints containing it (dual.py:137-144)."""
-    state = DualState(instance, flat=flat, device=device)
+    state = DualState(instance, flat=flat, device=device, schedule=schedule)
     costs = torch.as_tensor(np.ascontiguousarray(instance.costs, dtype=np.float64), device=state.device)
     state.dev.init_duals(costs, state.lam_d)
     state.refresh_backward()
@@ -299,6 +377,8 @@ def dual_objective(state: DualState) -> float:
 
 def mma_pass(state: DualState, direction: str) -> DualState:
     """One exact averaging pass over all variables (dual.py:154-186)."""
+    if state.deferred:
+        raise ValueError("mma_pass is the exact schedule; a deferred-schedule state averages with deferred_round")
     timer = state.pass_timer
     if direction == FORWARD:
         if not state.b_valid:
@@ -342,9 +422,11 @@ def subgradient_device(state: DualState) -> torch.Tensor:
         return cached[1]
     bits = torch.empty(state.flat.num_layers, dtype=_F64, device=state.device)
     if state._dec_gen == state._bgen:
-        state.dev.k_argmin_from_pass(state.B, bits)  # decisions of the pass that wrote B
+        # decisions of the pass that wrote B
+        state.dev.k_argmin_from_pass(state.B_il if state.deferred else state.B, bits)
     else:
-        state.dev.k_argmin(state.lam_d, state.B, bits)
+        _, B = state.node_tables(need_f=False)
+        state.dev.k_argmin(state.lam_d, B, bits)
     state._argmin_cache = (state._bgen, bits)
     return bits
 

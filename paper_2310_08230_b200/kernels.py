@@ -141,6 +141,30 @@ class DeviceFlat:
         """Whether the exact backward pass records argmin decisions (node-parallel kernels)."""
         return int(self.info.get("lanes_per_task", 32)) == 8
 
+    # --- deferred (throughput) averaging schedule: dm_dfr_* ------------------
+    def dfr_table_size(self) -> int:
+        n = ctypes.c_int64()
+        _native.check(_native.load().dm_dfr_table_size(self._h, ctypes.byref(n)), "dm_dfr_table_size")
+        return int(n.value)
+
+    def dfr_forward(self, omega, lam, avg, B_il, F_il, mbar, bounds):
+        _native.call("dm_dfr_forward", self._h, float(omega), _ptr(lam), _ptr(avg), _ptr(B_il), _ptr(F_il),
+                     _ptr(mbar), _ptr(bounds), self._s())
+
+    def dfr_backward(self, omega, lam, avg, F_il, B_il, mbar, bounds, record_decisions=False):
+        _native.call("dm_dfr_backward", self._h, float(omega), _ptr(lam), _ptr(avg), _ptr(F_il), _ptr(B_il),
+                     _ptr(mbar), _ptr(bounds), int(bool(record_decisions)), self._s())
+
+    def dfr_average(self, mbar, avg):
+        _native.call("dm_dfr_average", self._h, _ptr(mbar), _ptr(avg), self._s())
+
+    def dfr_to_nodes(self, x_il, x):
+        _native.call("dm_dfr_to_nodes", self._h, _ptr(x_il), _ptr(x), self._s())
+
+    @property
+    def dfr_records_decisions(self) -> bool:
+        return int(self.info.get("max_width", 99)) <= 8
+
     # --- per-variable vectors ------------------------------------------------
     def init_duals(self, costs_by_var, lam):
         _native.call("dm_init_duals", self._h, _ptr(costs_by_var), _ptr(lam), self._s())

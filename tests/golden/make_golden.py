@@ -84,15 +84,20 @@ def record(name, costs, rows, chunk, iters_mma, iters_hyb, extra=None):
     return out
 
 
-def append_product_cases(configs):
+def append_product_cases(configs, fname="golden.json"):
     """Record further product-space cases and merge them into golden.json
-    (``python tests/golden/make_golden.py c3``); existing cases are kept."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
-    with open(path) as fh:
-        doc = json.load(fh)
-    for cfg, chunk, im, ih in configs:
-        costs, rows, meta = product_case(cfg)
-        case = record(f"ps_{cfg}", costs, rows, chunk, im, ih, meta)
+    (``python tests/golden/make_golden.py c3``) or, for the full-size bench
+    configs, golden_large.json (``python tests/golden/make_golden.py --large``);
+    existing cases are kept."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), fname)
+    doc = {"generator": "tests/golden/make_golden.py", "reference": "prodmatch 0.1.0", "numpy": np.__version__,
+           "cases": []}
+    if os.path.exists(path):
+        with open(path) as fh:
+            doc = json.load(fh)
+    for name, cfg, seed, chunk, im, ih in configs:
+        costs, rows, meta = product_case(cfg, seed)
+        case = record(name, costs, rows, chunk, im, ih, meta)
         doc["cases"] = [c for c in doc["cases"] if c["name"] != case["name"]] + [case]
     with open(path, "w") as fh:
         json.dump(doc, fh, indent=1)
@@ -100,10 +105,18 @@ def append_product_cases(configs):
 
 
 # C3 (k-NN pruned humanoid-like pair, 500 x 500): a few iterations of each mode
-EXTRA = {"c3": ("c3", 128, 3, 4)}
+EXTRA = {"c3": ("ps_c3", "c3", 0, 128, 3, 4)}
+# The benched configs at full size (bench.py's default C2 line, the north
+# star's C4 target, two members of the C5 batch = C3-generator seeds):
+# 3 mma-only and 8-10 hybrid iterations each -> golden_large.json
+LARGE = [("ps_c2", "c2", 0, 128, 3, 8), ("ps_c4", "c4", 0, 128, 3, 10),
+         ("ps_c5_s17", "c3", 17, 128, 3, 8), ("ps_c5_s42", "c3", 42, 128, 3, 8)]
 
 
 def main():
+    if sys.argv[1:] == ["--large"]:
+        append_product_cases(LARGE, "golden_large.json")
+        return
     if len(sys.argv) > 1:
         append_product_cases([EXTRA[c] for c in sys.argv[1:]])
         return
