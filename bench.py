@@ -41,8 +41,8 @@ UNIT = "arc-updates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="c2")
     ap.add_argument("--seed", type=int, default=0)
@@ -51,7 +51,11 @@ def parse():
     ap.add_argument("--no-ttg", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--e2e-iters", type=int, default=50)
-    ap.add_argument("--ttg-max-iters", type=int, default=150)
+    ap.add_argument("--schedule", choices=["exact", "deferred"], default="exact",
+                    help="averaging schedule of the headline line (the other one is reported as an extra key)")
+    ap.add_argument("--no-extras", action="store_true", help="headline only: no other-schedule / C4 / C5 keys")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=300.0, help="wall budget (s) of a CPU time-to-gap run")
     ap.add_argument("--batch", type=int, default=0, help="also time K independent instances via qn.solve_batch")
     ap.add_argument("--batch-iters", type=int, default=30)
     ap.add_argument("--streams", type=int, default=8, help="concurrent solves per GPU for --config c5")
@@ -89,7 +93,37 @@ def build_instance(config: str, seed: int):
     log(f"[bench] {config} seed {seed}: product space {t1 - t:.1f}s, lowering {t2 - t1:.1f}s, "
         f"{inst.num_variables} vars, {inst.flat.num_bdds} bdds, {inst.flat.num_layers} layers, "
         f"{inst.flat.num_nodes} nodes")
+    inst._rows_hash = rows_hash(p)
     return inst
+
+
+def rows_hash(p) -> str:
+    import hashlib
+
+    m = hashlib.sha256()
+    for a in (p.row_ptr, p.row_var, p.row_coef, p.row_rhs, p.costs):
+        import numpy as np
+
+        a = np.ascontiguousarray(a)
+        m.update(a.dtype.str.encode() + a.tobytes())
+    return m.hexdigest()[:32]
+
+
+def oracle_instance(config: str, seed: int):
+    """The CPU arm's instance, lowered by the ORACLE's restatement of the
+    reference pipeline (rows -> equality diagrams -> 128-chunk split -> flat
+    table, oracle/model.py), so the reference arm never maps the product
+    library; the lowering is golden-pinned against the real reference
+    (tests/test_oracle_golden.py, tests/test_large_parity.py)."""
+    from oracle import model
+    from paper_2310_08230_b200 import product_space as ps
+
+    t = time.perf_counter()
+    p = ps.synthetic_product_space(config, seed)
+    oi = model.split_instance(model.instance_from_rows(p.costs, p.rows()), 128)
+    of = model.flatten(oi)
+    log(f"[bench] oracle lowering of {config} seed {seed}: {time.perf_counter() - t:.1f}s, {of.num_nodes} nodes")
+    return oi, of, rows_hash(p)
 
 
 def oracle_twin(inst):
@@ -101,31 +135,9 @@ def oracle_twin(inst):
     return model.from_flat_table(inst.costs, inst.variable_order, f.constraint_counts, arrays)
 
 
-def cpu_reference_run(inst, warmup: int, steps: int):
-    """The reference algorithm (C port of the numba kernels + numpy driver) on
-    the host: untimed warm-up iterations, then ``steps`` timed iterations.
-    Returns (arc_updates/s, seconds per iteration, threads)."""
-    from oracle import solver
-    from oracle.clib import lib
-
-    threads = os.cpu_count() or 1
-    lib.oracle_set_threads(threads)
-    oi, of = oracle_twin(inst)
-    gen = _oracle_iterations(oi, of)
-    for _ in range(warmup):
-        next(gen)
-    st = next(gen)  # yields state after each iteration
-    s0 = st.sweeps
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        st = next(gen)
-    dt = time.perf_counter() - t0
-    arcs = (st.sweeps - s0) * 2 * of.num_nodes
-    return arcs / dt, dt / steps, threads
-
-
-def _oracle_iterations(oi, of):
-    """Generator form of oracle.solver.solve (qn.py:211-259), hybrid mode."""
+def _oracle_iterations(oi, of, schedule="exact"):
+    """Generator form of oracle.solver.solve (qn.py:211-259), hybrid mode;
+    yields (state, bound) after init and after every iteration."""
     from collections import deque
 
     from oracle import solver
@@ -138,7 +150,7 @@ def _oracle_iterations(oi, of):
     g_prev = st.subgradient()
     gamma = 1.0
     it = 0
-    yield st
+    yield st, first
     while True:
         it += 1
         if hist:
@@ -147,8 +159,11 @@ def _oracle_iterations(oi, of):
             gamma, better = solver.step_search(st, d, gamma, 0.8, 1.1, 5, min_ascent)
             if better:
                 st.shift(gamma * d)
-        st.mma(True)
-        st.mma(False)
+        if schedule == "deferred":
+            st.deferred_round(0.5)
+        else:
+            st.mma(True)
+            st.mma(False)
         bound = st.objective()
         if it == 1:
             min_ascent = 1e-6 * (bound - first)
@@ -160,7 +175,85 @@ def _oracle_iterations(oi, of):
             hist.appendleft((s, y, 1.0 / sy, sy))
         lam_prev = st.lam.copy()
         g_prev = g_now
-        yield st
+        yield st, bound
+
+
+def cpu_reference_run(oi, of, warmup: int, steps: int, d_star=None, gap=1e-3, budget_s=240.0, threads=None):
+    """The reference algorithm (C port of the numba kernels + numpy driver,
+    exact passes single-threaded as in the reference) on the host, from a
+    fresh init: ``warmup`` untimed iterations, ``steps`` timed ones, then
+    (if ``d_star`` is given) on until the relative gap to d_star is <= gap or
+    the wall budget runs out.  Returns a dict: arc-updates/s and ms per
+    iteration of the timed window, and the measured time to the gap (clock
+    from init, the same definition as the GPU arm)."""
+    from oracle.clib import lib
+
+    threads = threads or os.cpu_count() or 1
+    lib.oracle_set_threads(threads)
+    t0 = time.perf_counter()
+    gen = _oracle_iterations(oi, of)
+    st, b = next(gen)
+    hit = (0, 0.0) if d_star is not None and d_star - b <= gap * abs(d_star) else None
+    it = 0
+    s0 = tw0 = None
+    out = {"threads": threads}
+    while True:
+        if it == warmup:
+            s0, tw0 = st.sweeps, time.perf_counter()
+        if it == warmup + steps:
+            dt = time.perf_counter() - tw0
+            out["value"] = (st.sweeps - s0) * 2 * of.num_nodes / dt
+            out["ms_per_iteration"] = dt / steps * 1e3
+            out["timed_iterations"] = f"{warmup + 1}..{warmup + steps}"
+        done_timing = it >= warmup + steps
+        if done_timing and (d_star is None or hit is not None or time.perf_counter() - t0 > budget_s):
+            break
+        st, b = next(gen)
+        it += 1
+        if d_star is not None and hit is None and d_star - b <= gap * abs(d_star):
+            hit = (it, time.perf_counter() - t0)
+    if d_star is not None:
+        out["time_to_gap"] = {"value": hit[1] if hit else None, "iterations": hit[0] if hit else None,
+                              "unit": "s", "gap": gap, "d_star": d_star, "measured": True,
+                              "budget_s": budget_s, "iterations_run": it, "last_bound": b,
+                              "clock": "host perf_counter from init_duals start (instance lowered)"}
+    return out
+
+
+DSTAR_PATH = os.path.join(ROOT, "profiles", "dstar.json")
+
+
+def d_star_for(config: str, seed: int, rhash: str):
+    """Best known dual bound of the instance (profiles/dstar.json: long runs of
+    both schedules on a B200, plus a certified primal where one exists), or
+    None when the file has no entry for this exact instance (rows hash)."""
+    try:
+        with open(DSTAR_PATH) as fh:
+            table = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    e = table.get(f"{config}:{seed}")
+    if not e or e.get("rows_hash") != rhash:
+        return None
+    return e
+
+
+def gpu_time_to_gap(inst, dev, schedule, d_star, gap=1e-3, max_iterations=None):
+    """Measured time to a relative gap to d_star: qn.solve from init_duals on
+    the resident instance (upload and plans outside the clock), host clock."""
+    from paper_2310_08230_b200.config import SolveConfig
+    from paper_2310_08230_b200.dual import init_duals
+    from paper_2310_08230_b200.qn import solve
+
+    st = init_duals(inst, device=dev, schedule=schedule)
+    cfg = SolveConfig(mode="hybrid", mma_schedule=schedule,
+                      max_iterations=max_iterations or (300 if schedule == "exact" else 1500))
+    res = solve(inst, cfg, device=dev, state=st)
+    hit = next((r for r in res.records if d_star is not None and d_star - r.dual_objective <= gap * abs(d_star)),
+               None)
+    return {"value": hit.time_s if hit else None, "iterations": hit.iteration if hit else None, "unit": "s",
+            "gap": gap, "best_bound": res.best_bound, "solve_iterations": res.iterations, "stop": res.stop_reason,
+            "ms_per_iteration_solve": res.records[-1].time_s / max(res.iterations, 1) * 1e3}, res
 
 
 class ClockSampler:
@@ -249,12 +342,14 @@ def aggregate_work_time(work: float, ms: float, world: int, device=None):
 VISIBILITY_NS = 267.0
 
 
-def _traffic(kernel, config="c2"):
+def _traffic(kernel, config="c2", schedule="exact"):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture summary of this config (profiles/traffic.json for C2,
-    profiles/traffic_<config>.json otherwise; tools/ncu_summary.py), or None."""
-    name = "traffic.json" if config == "c2" else f"traffic_{config}.json"
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+    capture summary of this config (profiles/traffic_<config>[_deferred].json,
+    tools/ncu_summary.py), or None."""
+    name = f"traffic_{config}" + ("_deferred" if schedule == "deferred" else "") + ".json"
+    if config == "c2" and schedule == "exact":
+        name = "traffic.json"
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             tr = json.load(f)
@@ -263,183 +358,258 @@ def _traffic(kernel, config="c2"):
     # the exact passes run their node-parallel instantiation when the instance allows it
     cands = [kernel.replace("mma_", "mma_np_"), kernel] if kernel.startswith("mma_") else [kernel]
     for cand in cands:
+        if cand in tr:
+            return tr[cand]
         for name, b in tr.items():
-            if name.startswith(cand + "_kernel") or name.startswith(cand + "<") or name == cand:
+            if name.startswith(cand + "_kernel") or name.startswith(cand + "<"):
                 return b
     return None
 
 
 def algorithmic_bytes(flat):
-    """Per-launch algorithmic HBM bytes."""
+    """Per-launch algorithmic HBM bytes of each timed kernel (DESIGN.md
+    'Kernels, their bound, algorithmic bytes')."""
     N, L, nb = flat.num_nodes, flat.num_layers, flat.num_bdds
+    P = len(flat.proc_ptr) - 1
     return {
-        # arcs 8 + own distance read 8 + target distance read 8 + produced distance 8 + sentinel prime 8
-        # per node; lam r/w 16 + task slot 8 + layer offset 4 per layer; bound 8 per diagram
+        # exact passes: arcs 8 + own distance read 8 + target distance read 8 + produced distance 8 +
+        # sentinel prime 8 per node; lam r/w 16 + task slot 8 + layer offset 4 per layer; bound 8 per diagram
         "mma": 40 * N + 28 * L + 8 * nb,
-        # interleaved arcs 8 per node (next-layer distances stay in shared memory, trial writes no table);
-        # lam 8 + d 8 per layer; bound 8 + offsets 8 per diagram
+        # trial sweep: interleaved arcs 8 per node (next-layer distances stay in shared memory, no table
+        # written); lam 8 + d 8 per layer; bound 8 + offsets 8 per diagram
         "backward_trial": 8 * N + 16 * L + 16 * nb,
+        # deferred passes (interleaved tables): arcs 8 + opposite table read 8 + own table write 8 per node;
+        # lam r/w 16 + escrow write 8 (+ average read 8, backward) per layer; bound 8 per diagram
+        "dfr_forward": 24 * N + 24 * L + 8 * nb,
+        "dfr_backward": 24 * N + 32 * L + 8 * nb,
+        # flush sweep: arcs 8 + table write 8 per node; lam r/w 16 + average read 8 + decision word 8 per layer
+        "dfr_flush": 16 * N + 32 * L + 8 * nb,
+        # segmented average: escrow read 8 + copy index 4 + average write 8 per layer; CSR offset 4 per variable
+        "dfr_average": 20 * L + 4 * P,
     }
 
 
-def run_b200(args, rank, world, local_rank):
+def _bytes_for(name, abytes):
+    if name.startswith("mma"):
+        return abytes["mma"]
+    if name == "step_search":
+        return abytes["backward_trial"]
+    return abytes.get(name)
+
+
+def timed_steps(args, inst, dev, schedule, world, rank, local_rank, clocks=True):
+    """W untimed + K timed hybrid iterations (DualSolver.step, the loop body
+    of qn.solve) of one schedule on the resident instance; CUDA-event timing
+    on the launching stream, per-kernel event pairs for the roofline."""
     import torch
 
     from paper_2310_08230_b200 import _native
     from paper_2310_08230_b200.config import SolveConfig
     from paper_2310_08230_b200.dual import KernelTimer
-    from paper_2310_08230_b200.qn import DualSolver, solve
+    from paper_2310_08230_b200.qn import DualSolver
 
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    inst = build_instance(args.config, args.seed + rank)
-    cfg = SolveConfig(mode="hybrid", max_iterations=10**9, dual_tolerance=0.0)
+    cfg = SolveConfig(mode="hybrid", max_iterations=10**9, dual_tolerance=0.0, mma_schedule=schedule)
     run = DualSolver(inst, cfg, device=dev).start()
     st = run.state
-    info = st.dev.info
-    log(f"[bench] rank {rank}: exact-pass DAG depth fw {info['fw_depth']} bw {info['bw_depth']}, "
-        f"tasks {info['fw_tasks']}, grid {info['mma_grid']}x{info['mma_block']}")
-    # the clock sampler (nvidia-smi) starts before the warm-up: its start-up
-    # touches the driver and must not fall inside the timed region
-    with ClockSampler(local_rank) as clk:
-        time.sleep(1.0)
-        for _ in range(args.warmup):
-            run.step()
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        timer = KernelTimer()
-        st.pass_timer = timer
-        s0 = st.sweeps
-        l0 = _native.launch_count
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local_rank) if clocks else None
+    if clk:
+        clk.__enter__()
+        time.sleep(1.0)  # nvidia-smi start-up outside the timed region
+    for _ in range(args.warmup):
+        run.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    timer = KernelTimer()
+    st.pass_timer = timer
+    s0, l0 = st.sweeps, _native.launch_count
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
         clk.mark()
-        torch.cuda.synchronize()
-        start.record()
-        step_wall = []
-        for _ in range(args.steps):
-            t_s = time.perf_counter()
-            sw0 = st.sweeps
-            run.step()
-            step_wall.append((round((time.perf_counter() - t_s) * 1e3, 2), st.sweeps - sw0))
-        end.record()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        run.step()
+    end.record()
+    torch.cuda.synchronize()
+    if clk:
         clk.mark()
-        log(f"[bench] per-step host wall ms / sweeps: {step_wall}")
+        clk.__exit__(None, None, None)
     if world > 1:
         torch.distributed.barrier()
     st.pass_timer = None
     ms = start.elapsed_time(end)
     arcs = (st.sweeps - s0) * 2 * st.flat.num_nodes
-    launches = _native.launch_count - l0
-    kt = timer.summary()
-
     total_arcs, max_ms = aggregate_work_time(arcs, ms, world, dev)
-    value = total_arcs / (max_ms / 1e3)
+    kt = timer.summary()
+    abytes = algorithmic_bytes(st.flat)
+    hbm = _peaks().get("hbm_gbs", 6650.0)
+    kernels = {}
+    for name, k in kt.items():
+        if name == "step_search":
+            # one event pair around the device trial sequence: per-trial figures
+            # over the trials that ran (sweep + bound sum + decision)
+            trials = max(timer.counts.get("step_search_trials", 0), 1)
+            k = dict(k, searches=k["launches"], launches=trials, avg_ms=k["total_ms"] / trials)
+        bpl = _bytes_for(name, abytes)
+        kernels[name] = dict(k, bytes_per_launch=bpl, share_of_step=k["total_ms"] / ms)
+        if bpl:
+            a = bpl / (k["avg_ms"] * 1e-3) / 1e9
+            kernels[name].update(achieved_gbs=round(a, 1), frac=round(a / hbm, 4))
+    return {"value": total_arcs / (max_ms / 1e3), "ms_per_iteration": max_ms / args.steps, "kernels": kernels,
+            "launches": _native.launch_count - l0, "clocks": clk.summary() if clk else None, "state": st,
+            "info": st.dev.info, "hbm": hbm}
 
+
+def roofline_of(t, config, schedule):
+    """Roofline object for the dominant kernel of a timed_steps result."""
+    kernels = t["kernels"]
+    dom = max(kernels, key=lambda n: kernels[n]["total_ms"]) if kernels else None
+    if not dom or not kernels[dom].get("bytes_per_launch"):
+        return None
+    k = kernels[dom]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": k["achieved_gbs"], "peak": t["hbm"], "unit": "GB/s",
+            "frac": k["frac"], "traffic": _traffic(dom, config, schedule),
+            "algorithmic_bytes": k["bytes_per_launch"],
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if _peaks() else "fallback 6650 GB/s"}
+    if dom.startswith("mma"):
+        # the exact passes are bound by their dependency chain, not by bytes
+        depth = t["info"]["fw_depth"] if dom == "mma_forward" else t["info"]["bw_depth"]
+        ns = k["avg_ms"] * 1e6 / depth
+        roof["critical_path"] = {"levels": depth, "ns_per_level": round(ns, 1), "visibility_floor_ns": VISIBILITY_NS,
+                                 "frac": round(VISIBILITY_NS / ns, 4),
+                                 "note": "per level >= one-way store->poll visibility between SMs (tools/pingpong.cu)"}
+    return roof
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    inst = build_instance(args.config, args.seed + rank)
+    sched = args.schedule
+    t = timed_steps(args, inst, dev, sched, world, rank, local_rank)
+    st, info = t["state"], t["info"]
+    log(f"[bench] rank {rank}: exact-pass DAG depth fw {info['fw_depth']} bw {info['bw_depth']}, "
+        f"{sched} schedule {t['ms_per_iteration']:.3f} ms/iteration")
     result = None
     if rank == 0:
-        abytes = algorithmic_bytes(st.flat)
-        peaks = _peaks()
-        hbm = peaks.get("hbm_gbs", 6650.0)
-        kernels = {}
-        for name, k in kt.items():
-            if name == "step_search":
-                # one event pair around the device trial sequence: per-trial
-                # figures over the trials that ran (sweep + bound sum + decision)
-                trials = max(timer.counts.get("step_search_trials", 0), 1)
-                k = dict(k, searches=k["launches"], launches=trials, avg_ms=k["total_ms"] / trials)
-                bpl = abytes["backward_trial"]
-            else:
-                bpl = abytes["mma" if name.startswith("mma") else name]
-            kernels[name] = dict(k, bytes_per_launch=bpl, achieved_gbs=bpl / (k["avg_ms"] * 1e-3) / 1e9,
-                                 share_of_step=k["total_ms"] / ms)
-        dom = max(kernels, key=lambda n: kernels[n]["total_ms"]) if kernels else None
-        roof = None
-        if dom:
-            a = kernels[dom]["achieved_gbs"]
-            roof = {"bound": "hbm", "kernel": dom, "achieved": round(a, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(a / hbm, 4),
-                    "traffic": _traffic(dom, args.config),
-                    "algorithmic_bytes": kernels[dom]["bytes_per_launch"],
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
-            if dom.startswith("mma"):
-                # the exact passes are bound by their dependency chain, not by bytes
-                depth = info["fw_depth"] if dom == "mma_forward" else info["bw_depth"]
-                ns = kernels[dom]["avg_ms"] * 1e6 / depth
-                roof["critical_path"] = {
-                    "levels": depth, "ns_per_level": round(ns, 1),
-                    "visibility_floor_ns": VISIBILITY_NS,
-                    "frac": round(VISIBILITY_NS / ns, 4),
-                    "note": "per level >= one-way store->poll visibility between SMs (tools/pingpong.cu)"}
         result = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args.config) + ", 128-chunk split, hybrid L-BFGS+exact MMA iteration; one instance per GPU",
-                       "variables": inst.num_variables, "bdds": st.flat.num_bdds, "dual_coords": st.flat.num_layers,
-                       "nodes": st.flat.num_nodes, "fw_depth": info["fw_depth"], "bw_depth": info["bw_depth"],
-                       "l2": "working set 1.4 GB > 126 MB L2 (no flush needed)",
-                       "parallelism": f"instance-sharded x{world}"},
-            "gpu_launches": launches,
-            "kernels": kernels,
-            "roofline": roof,
-            "clocks": clk.summary(),
+            "metric": METRIC, "value": t["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t["ms_per_iteration"], "ms_per_iteration": t["ms_per_iteration"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload(args.config) + f", 128-chunk split, one hybrid L-BFGS + {sched}-schedule "
+                                                           "averaging iteration per step; one instance per GPU",
+                       "schedule": sched, "variables": inst.num_variables, "bdds": st.flat.num_bdds,
+                       "dual_coords": st.flat.num_layers, "nodes": st.flat.num_nodes,
+                       "fw_depth": info["fw_depth"], "bw_depth": info["bw_depth"],
+                       "l2": "working set > 126 MB L2 (no flush needed)" if st.flat.num_nodes > 4_000_000
+                       else "working set partly L2-resident", "parallelism": f"instance-sharded x{world}"},
+            "gpu_launches": t["launches"], "kernels": t["kernels"], "roofline": roofline_of(t, args.config, sched),
+            "clocks": t["clocks"],
         }
-    # time to 1e-3 relative dual gap (gap vs the run's best bound; host clock incl. init)
-    if rank == 0 and not args.no_ttg:
-        res = solve(inst, SolveConfig(mode="hybrid", max_iterations=args.ttg_max_iters), device=dev, state=st)
-        d_star = res.best_bound
-        ttg = None
-        for r in res.records:
-            if (d_star - r.dual_objective) <= 1e-3 * abs(d_star):
-                ttg = r
-                break
-        result["time_to_gap"] = {"value": ttg.time_s if ttg else None, "unit": "s", "gap": 1e-3,
-                                 "iterations": ttg.iteration if ttg else None, "d_star": d_star,
-                                 "d_star_iterations": res.iterations, "stop": res.stop_reason,
-                                 "clock": "host perf_counter from solve() start, duals resident"}
-    if rank == 0 and not args.no_ttg and args.config == "c2":
-        result["c4_time_to_gap"] = c4_time_to_gap(args, dev)
-    if rank == 0 and not args.no_e2e:
-        result["e2e"] = e2e_run(args, inst, dev)
-    if rank == 0 and args.batch > 1:
+    if rank != 0:
+        return None
+    del t, st
+    if not args.no_extras:
+        other = "deferred" if sched == "exact" else "exact"
+        o = timed_steps(args, inst, dev, other, 1, 0, local_rank, clocks=False)
+        result[other] = {"value": o["value"], "unit": UNIT, "ms_per_iteration": o["ms_per_iteration"],
+                         "kernels": o["kernels"], "roofline": roofline_of(o, args.config, other),
+                         "gpu_launches": o["launches"], "steps": args.steps, "warmup": args.warmup}
+        del o
+    if not args.no_ttg:
+        result["time_to_gap"] = time_to_gap_both(inst, dev, args.config, args.seed)
+        if args.config == "c2" and not args.no_extras:
+            c4 = build_instance("c4", args.seed)
+            result["c4"] = {"workload": workload("c4"), "nodes": c4.flat.num_nodes,
+                            "time_to_gap": time_to_gap_both(c4, dev, "c4", args.seed)}
+            del c4
+    if args.config == "c2" and not args.no_extras and not args.no_c5:
+        result["c5"] = c5_summary(args, dev)
+    if not args.no_e2e:
+        result["e2e"] = e2e_run(args, inst, dev, sched)
+    if args.batch > 1:
         result["batch"] = batch_run(args, inst, dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, spi, thr = cpu_reference_run(inst, 1, args.cpu_iters)
-        result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
-                                  "sample": f"{args.cpu_iters} hybrid iterations of the same {args.config} instance "
-                                            f"after 1 warm-up iteration ({spi:.2f} s/iteration); C port of the numba "
-                                            "kernels, exact passes single-threaded as in the reference"}
-        if result.get("time_to_gap", {}).get("iterations"):
-            result["time_to_gap"]["cpu_projected_s"] = spi * result["time_to_gap"]["iterations"]
+    if world == 1 and not args.no_cpu_baseline:
+        oi, of = oracle_twin(inst)
+        c = cpu_reference_run(oi, of, 1, args.cpu_iters)
+        result["cpu_baseline"] = {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": "port",
+                                  "ms_per_iteration": c["ms_per_iteration"],
+                                  "sample": f"{args.cpu_iters} hybrid iterations (exact schedule) of the same "
+                                            f"{args.config} instance after 1 warm-up iteration; C port of the numba "
+                                            "kernels, exact passes single-threaded as in the reference; the full "
+                                            "measured CPU run (same steps, time to gap) is bench.py --impl reference"}
     return result
 
 
-def c4_time_to_gap(args, dev):
-    """The north star's single-instance target next to the C2 line: the
-    ~1000 x 1000-triangle k-NN pruned pair (C4) on this GPU, time to a 1e-3
-    relative gap to the run's best bound (same definition and clock as
-    ``time_to_gap``: from solve() start, instance resident)."""
+def time_to_gap_both(inst, dev, config, seed):
+    """Measured time to a 1e-3 relative gap for both schedules, against the
+    best known dual bound d* (profiles/dstar.json) or, without an entry for
+    this instance, the best bound either solve reached."""
+    e = d_star_for(config, seed, getattr(inst, "_rows_hash", ""))
+    d_star = e["d_star"] if e else None
+    out = {}
+    runs = {}
+    for s in ("exact", "deferred"):
+        out[s], runs[s] = gpu_time_to_gap(inst, dev, s, d_star)
+    if d_star is None:  # re-read the records against the better of the two runs
+        d_star = max(r.best_bound for r in runs.values())
+        for s, res in runs.items():
+            hit = next((r for r in res.records if d_star - r.dual_objective <= 1e-3 * abs(d_star)), None)
+            out[s]["value"] = hit.time_s if hit else None
+            out[s]["iterations"] = hit.iteration if hit else None
+        out["d_star_source"] = "best bound of the two solves in this run (no profiles/dstar.json entry)"
+    else:
+        out["d_star_source"] = e["source"]
+    out["d_star"] = d_star
+    out["clock"] = "host perf_counter from qn.solve start; instance resident, upload and plans outside the clock"
+    return out
+
+
+def e2e_run(args, inst, dev, schedule="exact"):
+    """Same metric through the public API from HOST buffers: every step
+    uploads the lowered instance (FlatBdds.device: topology + schedules),
+    runs qn.solve for --e2e-iters iterations and reads the duals back."""
+    import numpy as np
+    import torch
+
     from paper_2310_08230_b200.config import SolveConfig
     from paper_2310_08230_b200.dual import init_duals
+    from paper_2310_08230_b200.kernels import FlatBdds
     from paper_2310_08230_b200.qn import solve
 
-    inst = build_instance("c4", args.seed)
-    st = init_duals(inst, device=dev)  # upload + plans, outside the clock
-    res = solve(inst, SolveConfig(mode="hybrid", max_iterations=args.ttg_max_iters), device=dev, state=st)
-    d_star = res.best_bound
-    hit = next((r for r in res.records if (d_star - r.dual_objective) <= 1e-3 * abs(d_star)), None)
-    return {"value": hit.time_s if hit else None, "unit": "s", "gap": 1e-3, "iterations": hit.iteration if hit else None,
-            "d_star": d_star, "d_star_iterations": res.iterations, "stop": res.stop_reason,
-            "workload": workload("c4"), "nodes": st.flat.num_nodes}
+    f = inst.flat
+    h2d = sum(getattr(f, k).nbytes for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "zero_t", "one_t",
+                                             "proc_ptr", "proc_layers")) + inst.costs.nbytes
+    reps = []
+    arcs = iters = 0
+    for rep in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        flat = FlatBdds(inst)
+        state = init_duals(inst, device=dev, flat=flat, schedule=schedule)
+        res = solve(inst, SolveConfig(mode="hybrid", max_iterations=args.e2e_iters, dual_tolerance=0.0,
+                                      mma_schedule=schedule), device=dev, state=state)
+        lam = res.state.lam  # D2H
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if rep:
+            reps.append(dt)
+            arcs, iters = res.state.arc_updates, res.iterations
+        d2h = lam.nbytes + 8 * len(res.records)
+        del flat, state, res
+    sec = float(np.median(reps))
+    return {"value": arcs / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "seconds_per_step": sec, "ms_per_iteration": sec / max(iters, 1) * 1e3, "schedule": schedule,
+            "step": f"qn.solve({args.e2e_iters} hybrid iterations) from host arrays incl. device upload + "
+                    "schedule build + duals read back"}
 
 
 def batch_run(args, inst, dev):
-    """C5-style throughput on one GPU: --batch independent instances (seeds
-    seed..seed+K-1, the first being the bench instance) solved one after
-    another vs through qn.solve_batch (two concurrent streams); same
-    iteration count, duals required identical."""
+    """--batch K independent instances (seeds seed..seed+K-1) solved one after
+    another vs through qn.solve_batch; same iteration count, duals identical."""
     import torch
 
     from paper_2310_08230_b200.config import SolveConfig
@@ -460,48 +630,54 @@ def batch_run(args, inst, dev):
     arcs = sum(r.state.arc_updates for r in bat)
     return {"instances": len(insts), "iterations": args.batch_iters, "concurrency": 2,
             "sequential_s": t_seq, "batch_s": t_bat, "value": arcs / t_bat, "unit": UNIT,
-            "sequential_value": arcs / t_seq, "identical_to_sequential": same,
-            "step": "qn.solve from the lowered host instances incl. device upload, per instance"}
+            "sequential_value": arcs / t_seq, "identical_to_sequential": same}
 
 
-def e2e_run(args, inst, dev):
-    """Same metric through the public API from HOST buffers: every step
-    uploads the lowered instance (FlatBdds.device: topology + schedules),
-    runs qn.solve for --e2e-iters iterations and reads the duals back."""
-    import numpy as np
+C5_INSTANCES = 64
+
+
+def c5_instances(seeds):
+    return [build_instance("c3", s) for s in seeds]
+
+
+def c5_solve(insts, dev, schedule, streams):
+    """One C5 step: every instance solved from its lowered HOST arrays (device
+    upload and plans included) to the reference's stopping rule, ``streams``
+    solves in flight (qn.solve_batch).  Returns (seconds, results)."""
     import torch
 
     from paper_2310_08230_b200.config import SolveConfig
-    from paper_2310_08230_b200.kernels import FlatBdds
-    from paper_2310_08230_b200.qn import solve
+    from paper_2310_08230_b200.qn import solve_batch
 
-    f = inst.flat
-    h2d = sum(getattr(f, k).nbytes for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "zero_t", "one_t",
-                                             "proc_ptr", "proc_layers")) + inst.costs.nbytes
-    reps = []
-    arcs = 0
-    for rep in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        inst._flat_dev = None
-        flat = FlatBdds(inst)
-        from paper_2310_08230_b200.dual import init_duals
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = solve_batch(insts, SolveConfig(mode="hybrid", mma_schedule=schedule), device=dev, concurrency=streams)
+    torch.cuda.synchronize()
+    return time.perf_counter() - t, res
 
-        state = init_duals(inst, device=dev, flat=flat)
-        res = solve(inst, SolveConfig(mode="hybrid", max_iterations=args.e2e_iters, dual_tolerance=0.0),
-                    device=dev, state=state)
-        lam = res.state.lam  # D2H
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if rep:
-            reps.append(dt)
-            arcs = res.state.arc_updates
-        d2h = lam.nbytes + 8 * len(res.records)
-        del flat, state, res
-    sec = float(np.median(reps))
-    return {"value": arcs / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "seconds_per_step": sec, "step": f"qn.solve({args.e2e_iters} hybrid iterations) from host arrays incl. "
-                                             "device upload + schedule build"}
+
+def c5_summary(args, dev, reps=3):
+    """Config C5 on this GPU (the default line's extra key): 64 independent
+    ~500-triangle pairs, each solved to the stopping rule; median of ``reps``
+    repetitions after one warm-up, and their spread."""
+    import numpy as np
+
+    insts = c5_instances(range(args.seed, args.seed + C5_INSTANCES))
+    out = {"workload": f"c5: {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}, solved from host arrays "
+                       "(upload + plans included) to the reference's stopping rule", "streams": args.streams}
+    for schedule in ("exact", "deferred"):
+        c5_solve(insts[:8], dev, schedule, args.streams)  # warm-up
+        times, iters = [], 0
+        for _ in range(reps):
+            sec, res = c5_solve(insts, dev, schedule, args.streams)
+            times.append(sec)
+            iters = sum(r.iterations for r in res)
+            bounds = [r.best_bound for r in res]
+        med = float(np.median(times))
+        out[schedule] = {"instances_per_s": C5_INSTANCES / med, "seconds": med, "runs_s": times,
+                         "spread": (max(times) - min(times)) / med, "iterations_total": iters,
+                         "mean_best_bound": float(np.mean(bounds))}
+    return out
 
 
 def _peaks():
@@ -513,19 +689,45 @@ def _peaks():
 
 
 def run_reference(args, rank):
+    """--impl reference: the reference algorithm (exact schedule, hybrid) on
+    the host's cores through the C oracle port, on an instance lowered by the
+    oracle's own restatement of the reference pipeline — the product library
+    is never loaded (``native_so_loaded`` says so).  Same --steps / --warmup
+    as the GPU arm (iterations W+1..W+K timed), then on to the measured time
+    to the 1e-3 gap against the same d* as the GPU arm."""
     if rank != 0:
         return None
-    # C5's instances are C3-generator pairs: the CPU arm times one of them
-    inst = build_instance("c3" if args.config == "c5" else args.config, args.seed)
-    steps = min(args.steps, 5)
-    v, spi, thr = cpu_reference_run(inst, min(args.warmup, 1), steps)
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-            "warmup": min(args.warmup, 1), "ms_per_step": spi * 1e3, "higher_is_better": True, "scaling": "weak",
+    config = "c3" if args.config == "c5" else args.config
+    oi, of, rh = oracle_instance(config, args.seed)
+    e = d_star_for(config, args.seed, rh)
+    c = cpu_reference_run(oi, of, args.warmup, args.steps, d_star=e["d_star"] if e else None,
+                          budget_s=args.cpu_budget)
+    line = {"impl": "reference", "metric": METRIC, "value": c["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": c["ms_per_iteration"],
+            "ms_per_iteration": c["ms_per_iteration"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args.config) + ", 128-chunk split, hybrid iteration (same as the b200 arm)"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
-                             "sample": f"{steps} hybrid iterations after {min(args.warmup, 1)} warm-up (bounded sample)"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": workload(config) + ", 128-chunk split, one hybrid L-BFGS + exact-schedule "
+                                                      "averaging iteration per step (the reference algorithm)",
+                       "schedule": "exact", "timed_iterations": c["timed_iterations"]},
+            "cpu_baseline": {"value": c["value"], "unit": UNIT, "cores": c["threads"], "kind": "port",
+                             "sample": f"iterations {c['timed_iterations']} of a hybrid solve from init of the "
+                                       f"{config} instance; C port of the numba kernels (exact passes single-"
+                                       "threaded as in the reference, sweeps on all host threads), numpy/OpenBLAS "
+                                       "driver"},
+            "e2e": {"value": c["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if "time_to_gap" in c:
+        line["time_to_gap"] = dict(c["time_to_gap"], d_star_source=e["source"])
+    if config == "c2" and not args.no_extras and not args.no_ttg:
+        oi4, of4, rh4 = oracle_instance("c4", args.seed)
+        e4 = d_star_for("c4", args.seed, rh4)
+        if e4:
+            c4 = cpu_reference_run(oi4, of4, 0, 1, d_star=e4["d_star"], budget_s=args.cpu_budget)
+            line["c4"] = {"workload": workload("c4"), "ms_per_iteration": c4["ms_per_iteration"],
+                          "time_to_gap": dict(c4["time_to_gap"], d_star_source=e4["source"])}
+    from paper_2310_08230_b200 import _native
+
+    line["native_so_loaded"] = _native._lib is not None
+    return line
 
 
 C5_INSTANCES = 64
@@ -542,8 +744,8 @@ def run_c5(args, rank, world, local_rank):
     seeds r, r+N, ...; no collective on the data path).  One step = the
     rank's share of the batch solved through qn.solve_batch (--streams
     concurrent solves) from the lowered HOST instances (device upload and every plan
-    build included), --batch-iters hybrid iterations per instance; warm-up =
-    W solves of the rank's first instance."""
+    build included), each to the reference's stopping rule with the --schedule
+    averaging schedule; warm-up = W solves of the rank's first instance."""
     import torch
 
     from paper_2310_08230_b200 import _native
@@ -553,8 +755,8 @@ def run_c5(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     seeds = c5_seeds(rank, world)
-    insts = [build_instance("c3", args.seed + s) for s in seeds]
-    cfg = SolveConfig(mode="hybrid", max_iterations=args.batch_iters, dual_tolerance=0.0)
+    insts = c5_instances([args.seed + s for s in seeds])
+    cfg = SolveConfig(mode="hybrid", mma_schedule=args.schedule)
     h2d = sum(sum(getattr(i.flat, k).nbytes for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd",
                                                       "zero_t", "one_t", "proc_ptr", "proc_layers"))
               + i.costs.nbytes for i in insts)
@@ -591,7 +793,7 @@ def run_c5(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "instances_per_s": n_inst / (max_ms / 1e3),
         "config": {"workload": f"c5: batch of {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}; "
-                               f"{args.batch_iters} hybrid iterations per instance from host arrays",
+                               f"each solved from host arrays to the stopping rule ({args.schedule} schedule)",
                    "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), {args.streams} streams per GPU",
                    "l2": "each solve uploads its instance (inputs not L2-resident across steps)"},
         "gpu_launches": _native.launch_count - l0,

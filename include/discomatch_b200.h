@@ -220,6 +220,10 @@ int dm_dfr_backward(const dm_flat *f, double omega, double *lam, const double *a
                     double *B_il, double *mbar, double *bounds, int record_decisions, void *stream);
 /* segmented reduction over the variable CSR (proc_ptr / proc_layers) */
 int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *stream);
+/* the flush: lam[l] += the average dm_dfr_average would write (one rounding,
+ * identical to a later pass adding avg_in); follow it by a plain
+ * dm_dfr_backward (mbar = avg_in = NULL) to rebuild B_il for the new duals */
+int dm_dfr_flush(const dm_flat *f, const double *mbar, double *lam, void *stream);
 /* interleaved table -> FlatBdds node order */
 int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream);
 
@@ -239,7 +243,8 @@ int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, in
  * float64): out[0] = 0.0 + pairwise(x[0:n]) — bit-identical to the
  * reference's bound sums.  dm_dot: the fixed inner-product order of the
  * L-BFGS path — numpy pairwise over each 4096-element chunk of a*b, then
- * over the chunk totals (n <= 4096^2); the reference's OpenBLAS ddot order
+ * over the chunk totals (any n: up to 4096 totals in one block, beyond that
+ * through the dm_sum tree); the reference's OpenBLAS ddot order
  * is host-dependent, so any fixed order is parity-equivalent.  Results land in device
  * memory.  Reduction trees and their scratch are planned once per (device,
  * length, stream) and cached for the process, so solves on different streams

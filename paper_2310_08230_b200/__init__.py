@@ -10,11 +10,11 @@ include/discomatch_b200.h.  Modules mirror the reference's names:
 
 from .config import MODE_HYBRID, MODE_MMA_ONLY, SolveConfig
 from .errors import (EmptyFeasibleSet, EmptyHistory, InfeasibleAfterFixing, NativeLibraryError,
-                     ProdmatchError, SplitAtTerminalLayer)
+                     ProdmatchError, SplitAtTerminalLayer, UnsupportedInstance)
 from .ilp import Bdd, IlpInstance, LinearRow, build_equality_bdd, make_row
 
 __version__ = "0.1.0"
 
 __all__ = ["Bdd", "IlpInstance", "LinearRow", "make_row", "build_equality_bdd", "SolveConfig",
            "MODE_HYBRID", "MODE_MMA_ONLY", "ProdmatchError", "EmptyFeasibleSet", "EmptyHistory",
-           "InfeasibleAfterFixing", "SplitAtTerminalLayer", "NativeLibraryError"]
+           "InfeasibleAfterFixing", "SplitAtTerminalLayer", "NativeLibraryError", "UnsupportedInstance"]

@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import EmptyFeasibleSet, NativeLibraryError, ProdmatchError
+from .errors import EmptyFeasibleSet, NativeLibraryError, ProdmatchError, UnsupportedInstance
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DM_LIB_PATH") or os.path.join(_HERE, "libdiscomatch_b200.so")
@@ -77,6 +77,7 @@ SIGNATURES = {
     "dm_dfr_forward": ([_P, _D, _P, _P, _P, _P, _P, _P, _P], _INT),
     "dm_dfr_backward": ([_P, _D, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
     "dm_dfr_average": ([_P, _P, _P, _P], _INT),
+    "dm_dfr_flush": ([_P, _P, _P, _P], _INT),
     "dm_dfr_to_nodes": ([_P, _P, _P, _P], _INT),
     "dm_init_duals": ([_P, _P, _P, _P], _INT),
     "dm_project_direction": ([_P, _P, _P, _P], _INT),
@@ -130,6 +131,8 @@ def check(rc: int, what: str = "") -> None:
         raise EmptyFeasibleSet(msg)
     if rc == DM_ERR_INVALID:
         raise ValueError(msg)
+    if rc == DM_ERR_UNSUPPORTED:
+        raise UnsupportedInstance(msg)
     raise ProdmatchError(msg)
 
 
@@ -140,7 +143,7 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
                   "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search",
-                  "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_average", "dm_dfr_to_nodes"}
+                  "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_average", "dm_dfr_flush", "dm_dfr_to_nodes"}
 launch_count = 0
 
 

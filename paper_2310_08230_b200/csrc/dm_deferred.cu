@@ -85,6 +85,13 @@ template <int W, bool kMM, bool kAvg, bool kDec>
 __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
     extern __shared__ double sm[];
     const dm::SweepDev &s = a.s;
+    double *__restrict__ lamp = a.lam;
+    const double *__restrict__ avgp = a.avg;
+    const double *__restrict__ inp = a.in;
+    double *__restrict__ outp = a.out;
+    double *__restrict__ mbarp = a.mbar;
+    double *__restrict__ boundsp = a.bounds;
+    uint64_t *__restrict__ decp = a.dec;
     const int lane = threadIdx.x & 31;
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
@@ -113,12 +120,12 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
                 const int64_t e = (slot_n + i) * 32 + lane;
                 za[i] = s.zl[e];
                 oa[i] = s.ol[e];
-                if (kMM) fa[i] = a.in[e];
+                if (kMM) fa[i] = inp[e];
             }
         if (k < nj) {
             const int32_t l = l0 + nj - 1 - k;
-            lam_n = a.lam[l];
-            if (kAvg) avg_n = a.avg[l];
+            lam_n = lamp[l];
+            if (kAvg) avg_n = avgp[l];
         }
     };
     if (K > 0) fetch(0);
@@ -149,11 +156,11 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
                         if (c0 < m0) m0 = c0;
                         if (c1 < m1) m1 = c1;
                     }
-                lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, a.mbar + l);
+                lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, mbarp + l);
             } else {
                 lam_l = __dadd_rn(lam_l, a_l);
             }
-            a.lam[l] = lam_l;
+            lamp[l] = lam_l;
         }
         uint64_t word = 0;
 #pragma unroll
@@ -166,17 +173,17 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
                 const bool zero_wins = c0 <= c1;
                 const double v = zero_wins ? c0 : c1;
                 cur[i * kThreads] = v;
-                a.out[(slot + i) * 32 + lane] = v;
+                outp[(slot + i) * 32 + lane] = v;
                 if (kDec && W <= 8) {
                     const int32_t t = zero_wins ? za_ : ob;
                     word |= (uint64_t)((((t >= 0) ? t : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * i);
                 }
             }
-        if (kDec && W <= 8 && act) a.dec[l] = word;
+        if (kDec && W <= 8 && act) decp[l] = word;
         double *t = nb;
         nb = cur;
         cur = t;
-        if (act && k == nj - 1) a.bounds[j] = nb[0];  // root layer: single node
+        if (act && k == nj - 1) boundsp[j] = nb[0];  // root layer: single node
     }
 }
 
@@ -186,6 +193,13 @@ template <int W, bool kMM, bool kAvg>
 __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     extern __shared__ double sm[];
     const dm::SweepDev &s = a.s;
+    double *__restrict__ lamp = a.lam;
+    const double *__restrict__ avgp = a.avg;
+    const double *__restrict__ inp = a.in;
+    double *__restrict__ outp = a.out;
+    double *__restrict__ mbarp = a.mbar;
+    double *__restrict__ boundsp = a.bounds;
+    uint64_t *__restrict__ decp = a.dec;
     const int lane = threadIdx.x & 31;
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
@@ -218,14 +232,14 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
                 oa[i] = s.ol[e];
             }
         const int32_t l = l0 + nj - 1 - k;
-        lam_n = a.lam[l];
-        if (kAvg) avg_n = a.avg[l];
+        lam_n = lamp[l];
+        if (kAvg) avg_n = avgp[l];
         if (kMM) {
             wb_n = k > 0 ? s.pos_width[p0 + k - 1] : 0;
             const int64_t sb = k > 0 ? s.pos_slot[p0 + k - 1] : 0;
 #pragma unroll
             for (int u = 0; u < W; ++u)
-                if (u < wb_n) ba[u] = a.in[(sb + u) * 32 + lane];
+                if (u < wb_n) ba[u] = inp[(sb + u) * 32 + lane];
         }
     };
     if (nj > 0) fetch(nj - 1);
@@ -256,7 +270,7 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         }
 #pragma unroll
         for (int i = 0; i < W; ++i)
-            if (i < w) a.out[(slot + i) * 32 + lane] = cur[i * kThreads];
+            if (i < w) outp[(slot + i) * 32 + lane] = cur[i * kThreads];
         if (kMM) {
             double m0 = DM_INF, m1 = DM_INF;
 #pragma unroll
@@ -268,11 +282,11 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
                     if (c0 < m0) m0 = c0;
                     if (c1 < m1) m1 = c1;
                 }
-            lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, a.mbar + l);
-            a.lam[l] = lam_l;
+            lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, mbarp + l);
+            lamp[l] = lam_l;
         } else if (kAvg) {
             lam_l = __dadd_rn(lam_l, a_l);
-            a.lam[l] = lam_l;
+            lamp[l] = lam_l;
         }
         // push this layer's distances into the next one (kernels.py:241-269)
 #pragma unroll
@@ -300,47 +314,51 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         cur = nxt;
         nxt = t;
     }
-    if (j >= 0) a.bounds[j] = tb;
+    if (j >= 0) boundsp[j] = tb;
 }
 
 // One pass's escrow -> the next pass's per-copy average: thread per
-// visitation position (variable), copies summed in copy order.
+// visitation position (variable), copies summed in copy order.  kApply (the
+// flush): the average goes straight into the duals, lam[l] += avg (the same
+// single rounding a pass applies), instead of into avg[].
+template <bool kApply>
 __global__ void dfr_average_kernel(int32_t P, const int32_t *__restrict__ proc_ptr,
                                    const int32_t *__restrict__ proc_layers, const double *__restrict__ mbar,
-                                   double *__restrict__ avg) {
+                                   double *__restrict__ out) {
     const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
     const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
     if (hi == lo) return;
     constexpr int kReg = 8;  // copies held in registers; the rest re-read
-    double v[kReg];
+    double v[kReg], lv[kReg];
     int32_t ls[kReg];
     double sum = 0.0;
     int32_t cnt = 0;
-    for (int32_t t = lo; t < hi; ++t) {
-        const int32_t l = proc_layers[t];
-        const double x = mbar[l];
-        if (t - lo < kReg) {
-            v[t - lo] = x;
-            ls[t - lo] = l;
+#pragma unroll
+    for (int i = 0; i < kReg; ++i)
+        if (lo + i < hi) {
+            ls[i] = proc_layers[lo + i];
+            v[i] = mbar[ls[i]];
+            if (kApply) lv[i] = out[ls[i]];
         }
+    for (int32_t t = lo; t < hi; ++t) {
+        const double x = t - lo < kReg ? v[t - lo] : mbar[proc_layers[t]];
         if (x != DM_INF) {
             sum = __dadd_rn(sum, x);
             ++cnt;
         }
     }
     const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
-    for (int32_t t = lo; t < hi; ++t) {
-        double x;
-        int32_t l;
-        if (t - lo < kReg) {
-            x = v[t - lo];
-            l = ls[t - lo];
-        } else {
-            l = proc_layers[t];
-            x = mbar[l];
+#pragma unroll
+    for (int i = 0; i < kReg; ++i)
+        if (lo + i < hi) {
+            const double a = v[i] != DM_INF ? mean : 0.0;
+            out[ls[i]] = kApply ? __dadd_rn(lv[i], a) : a;
         }
-        avg[l] = x != DM_INF ? mean : 0.0;
+    for (int32_t t = lo + kReg; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        const double a = mbar[l] != DM_INF ? mean : 0.0;
+        out[l] = kApply ? __dadd_rn(out[l], a) : a;
     }
 }
 
@@ -416,12 +434,15 @@ int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const d
     return backward_w<32>(a, st);
 }
 
-int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *avg,
-                void *stream) {
+int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *out,
+                bool apply, void *stream) {
     if (P == 0) return DM_OK;
     constexpr int kT = 256;
-    dfr_average_kernel<<<(int)((P + kT - 1) / kT), kT, 0, (cudaStream_t)stream>>>((int32_t)P, proc_ptr, proc_layers,
-                                                                                   mbar, avg);
+    const int blocks = (int)((P + kT - 1) / kT);
+    if (apply)
+        dfr_average_kernel<true><<<blocks, kT, 0, (cudaStream_t)stream>>>((int32_t)P, proc_ptr, proc_layers, mbar, out);
+    else
+        dfr_average_kernel<false><<<blocks, kT, 0, (cudaStream_t)stream>>>((int32_t)P, proc_ptr, proc_layers, mbar, out);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DM_OK : fail(e, "dfr_average");
 }

@@ -1735,7 +1735,8 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         }
     }
     if (max_width > 32) {
-        dm::set_error("layers wider than 32 nodes are not supported by the exact averaging kernels");
+        dm::set_error("instance outside the kernels' envelope: a layer has " + std::to_string(max_width) +
+                      " nodes (the sweep and averaging kernels support at most 32)");
         return DM_ERR_UNSUPPORTED;
     }
     const bool vb2v = env_int("DM_VERBOSE", 0) >= 2;
@@ -1773,7 +1774,8 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
                 return;
             }
             if (hi - lo > 32) {
-                vmsg[t] = "exact averaging pass supports at most 32 diagrams per variable";
+                vmsg[t] = "instance outside the kernels' envelope: a variable is shared by more than 32 diagrams "
+                          "(the exact averaging kernels support at most 32)";
                 return;
             }
             dm_ = std::max(dm_, hi - lo);
@@ -2035,11 +2037,34 @@ int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
     return DM_OK;
 }
 
+// Every entry point runs on the device its data lives on and restores the
+// caller's current device on return (a flat's device, or the stream's).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        int cur;
+        if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+            prev = cur;
+    }
+    ~DevGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+inline int stream_device(void *stream) {
+    int dev = -1;
+    if (stream && cudaStreamGetDevice((cudaStream_t)stream, &dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = -1;
+    }
+    return dev;
+}
 #define DM_CHECK_FLAT(f)                        \
     if (!(f)) {                                 \
         dm::set_error("null flat handle");      \
         return DM_ERR_INVALID;                  \
-    }
+    }                                           \
+    DevGuard dm_guard_((f)->device)
+#define DM_STREAM_GUARD(stream) DevGuard dm_guard_(stream_device(stream))
 
 int dm_flat_set_mma_config(dm_flat *f, int threads, int blocks_per_sm, int sleep_ns, int probe, int lookahead) {
     if (!f) {
@@ -2117,8 +2142,9 @@ int dm_flat_status(dm_flat *f, void *stream) {
 void dm_flat_destroy(dm_flat *f) {
     if (!f) return;
     // the flat may still be in use by work on any (possibly non-blocking)
-    // stream: wait for the device, then hand the blocks back to the pool
-    cudaSetDevice(f->device);
+    // stream: wait for its device, then hand the blocks back to the pool;
+    // the caller's current device is restored (this runs from GC)
+    DevGuard guard(f->device);
     cudaDeviceSynchronize();
     for (void *p : f->allocs) cudaFreeAsync(p, 0);
     cudaGetLastError();
@@ -2346,7 +2372,16 @@ int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *s
         dm::set_error("dm_dfr_average: null vector");
         return DM_ERR_INVALID;
     }
-    return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, avg_in, stream);
+    return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, avg_in, false, stream);
+}
+
+int dm_dfr_flush(const dm_flat *f, const double *mbar, double *lam, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!mbar || !lam) {
+        dm::set_error("dm_dfr_flush: null vector");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, lam, true, stream);
 }
 
 int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream) {
@@ -2408,6 +2443,7 @@ static int pairwise(const double *a, const double *b, int64_t n, double *out, cu
 }
 
 int dm_sum(const double *x, int64_t n, double *out, void *stream) {
+    DM_STREAM_GUARD(stream);
     return pairwise(x, nullptr, n, out, (cudaStream_t)stream);
 }
 
@@ -2438,6 +2474,7 @@ static int dot_scratch(int64_t n, void *stream, bool slots, DotScratch **out) {
 }
 
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream) {
+    DM_STREAM_GUARD(stream);
     if (!a || !b || !out || n < 0) {
         if (n == 0 && out) {
             cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream);  // empty dot = 0.0
@@ -2450,11 +2487,6 @@ int dm_dot(const double *a, const double *b, int64_t n, double *out, void *strea
         DM_CUDA(cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream));
         return DM_OK;
     }
-    const int64_t nch = (n + dm::kDotChunk - 1) / dm::kDotChunk;
-    if (nch > dm::kDotChunk) {
-        dm::set_error("dm_dot: length above 4096*4096 not supported");
-        return DM_ERR_UNSUPPORTED;
-    }
     DotScratch *sc;
     if (int rc = dot_scratch(n, stream, false, &sc)) return rc;
     return dm::chunk_dot(a, b, n, sc->partial, out, stream);
@@ -2462,13 +2494,10 @@ int dm_dot(const double *a, const double *b, int64_t n, double *out, void *strea
 
 int dm_lbfgs_direction(const double *g, const double *const *s, const double *const *y, const double *rho,
                        const double *sy, int m, int64_t n, double *d, void *stream) {
+    DM_STREAM_GUARD(stream);
     if (!g || !s || !y || !rho || !sy || !d || m < 1 || m > kMaxPairs || n < 1) {
         dm::set_error("dm_lbfgs_direction: needs g, d, 1 <= m <= 64 pairs and n >= 1");
         return DM_ERR_INVALID;
-    }
-    if ((n + dm::kDotChunk - 1) / dm::kDotChunk > dm::kDotChunk) {
-        dm::set_error("dm_lbfgs_direction: length above 4096*4096 not supported");
-        return DM_ERR_UNSUPPORTED;
     }
     for (int i = 0; i < m; ++i)
         if (!s[i] || !y[i]) {
@@ -2482,13 +2511,10 @@ int dm_lbfgs_direction(const double *g, const double *const *s, const double *co
 
 int dm_curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
                       double *y, int64_t n, double *sy, void *stream) {
+    DM_STREAM_GUARD(stream);
     if (!lam || !lam_prev || !g || !g_prev || !s || !y || !sy || n < 1) {
         dm::set_error("dm_curvature_pair: needs six vectors of length n >= 1 and an output");
         return DM_ERR_INVALID;
-    }
-    if ((n + dm::kDotChunk - 1) / dm::kDotChunk > dm::kDotChunk) {
-        dm::set_error("dm_curvature_pair: length above 4096*4096 not supported");
-        return DM_ERR_UNSUPPORTED;
     }
     DotScratch *sc;
     if (int rc = dot_scratch(n, stream, false, &sc)) return rc;
@@ -2497,29 +2523,41 @@ int dm_curvature_pair(const double *lam, double *lam_prev, const double *g, cons
 
 int dm_axpy_dev(double *x, const double *y, double alpha_host, const double *dot_dev, double *alpha_out, int64_t n,
                 void *stream) {
+    DM_STREAM_GUARD(stream);
     axpy_dev_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, y, alpha_host, dot_dev, alpha_out, n);
     return check_stream_error("axpy_dev");
 }
 
 int dm_scale_dev(double *x, double num_host, const double *den_dev, int64_t n, void *stream) {
+    DM_STREAM_GUARD(stream);
     scale_dev_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, num_host, den_dev, n);
     return check_stream_error("scale_dev");
 }
 
 int dm_lbfgs_up(double *x, const double *s, const double *alpha_dev, double rho_host, const double *dot_dev, int64_t n,
                 void *stream) {
+    DM_STREAM_GUARD(stream);
     lbfgs_up_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, s, alpha_dev, rho_host, dot_dev, n);
     return check_stream_error("lbfgs_up");
 }
 
 int dm_axpy_host(double *x, double gamma, const double *y, int64_t n, void *stream) {
+    DM_STREAM_GUARD(stream);
     axpy_host_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(x, gamma, y, n);
     return check_stream_error("axpy_host");
 }
 
 int dm_sub(double *out, const double *a, const double *b, int64_t n, void *stream) {
+    DM_STREAM_GUARD(stream);
     sub_kernel<<<grid_stride_blocks(n), 256, 0, (cudaStream_t)stream>>>(out, a, b, n);
     return check_stream_error("sub");
 }
 
 }  // extern "C"
+
+namespace dm {
+int pairwise_device(const double *x, int64_t n, double *out, void *stream) {
+    return pairwise(x, nullptr, n, out, (cudaStream_t)stream);
+}
+}  // namespace dm
+

@@ -155,8 +155,12 @@ int sweep_backward(const SweepDev &s, const double *lam, const double *d, double
                    double *bounds, void *stream, const double *ctl = nullptr);
 // kernels.py:123-159
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream);
-// Chunked inner product (dm_sweep.cu): partial[nchunks] scratch, counter a
-// zeroed device word; requires nchunks = ceil(n / 4096) <= 4096.
+// numpy-order pairwise sum of a device vector into out[0] (dm_device.cu's
+// planned pw_leaf / pw_combine kernels, the dm_sum path), stream-ordered.
+int pairwise_device(const double *x, int64_t n, double *out, void *stream);
+// Chunked inner product (dm_sweep.cu): partial[nchunks] scratch; the chunk
+// totals are reduced in the finishing block up to 4096 chunks and by
+// pairwise_device beyond (same numpy order: vectors of any length).
 int chunk_dot(const double *a, const double *b, int64_t n, double *partial, double *out, void *stream);
 constexpr int64_t kDotChunk = 4096;
 // L-BFGS two-loop direction (qn.py:95-115) in 2m+2 fused launches; s/y are
@@ -170,8 +174,9 @@ int curvature_pair(const double *lam, double *lam_prev, const double *g, const d
 // add; dec (backward, W <= 8): argmin decision words per layer.
 int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const double *avg, const double *in,
              double *out, double *mbar, double *bounds, uint64_t *dec, void *stream);
-int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *avg,
-                void *stream);
+// apply: lam[l] += average (the flush) instead of avg[l] = average
+int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *out,
+                bool apply, void *stream);
 int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream);
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);

@@ -475,10 +475,13 @@ __global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, 
 // Tail chunk (update + its total) and the reduction of all chunk totals.
 // `full` = 0 also covers unaligned vectors: every chunk is then done here,
 // one at a time.
+// totals == false (more than 4096 chunks): only the tail chunk; the chunk
+// totals are then reduced by dm::pairwise_device (numpy's order for any length).
 template <int kMode>
 __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep a, int64_t n, int64_t full,
                                                                       double *__restrict__ partial,
-                                                                      const __grid_constant__ FinishPlans plans) {
+                                                                      const __grid_constant__ FinishPlans plans,
+                                                                      bool totals) {
     __shared__ double buf[kChunk];
     pdl_launch_dependents();
     pdl_wait();
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kFinishThreads) chunk_finish_kernel(ChunkStep 
         if (threadIdx.x == 0) partial[ch] = t;
         __syncthreads();
     }
-    if (!dot) return;
+    if (!dot || !totals) return;
     double pv[kPer];
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
@@ -556,11 +559,17 @@ cudaError_t chunk_step(const ChunkStep &a, int64_t n, double *partial, cudaStrea
     if (full > 0 &&
         (e = launch_maybe_pdl(chunk_step_kernel<kMode>, (unsigned)full, kChunkThreads, st, pdl, a, partial)))
         return e;
+    const int64_t nch = (n + kChunk - 1) / kChunk;
+    const bool two_level = nch > kChunk;
     FinishPlans plans;
     plans.chunk = make_sum_plan(kChunk);
     plans.tail = make_sum_plan((int)(n % kChunk));
-    plans.totals = make_sum_plan((int)((n + kChunk - 1) / kChunk));
-    return launch_maybe_pdl(chunk_finish_kernel<kMode>, 1, kFinishThreads, st, true, a, n, full, partial, plans);
+    plans.totals = make_sum_plan(two_level ? 0 : (int)nch);
+    if ((e = launch_maybe_pdl(chunk_finish_kernel<kMode>, 1, kFinishThreads, st, true, a, n, full, partial, plans,
+                              !two_level)))
+        return e;
+    if (two_level && a.v && dm::pairwise_device(partial, nch, a.dot_out, st)) return cudaErrorUnknown;
+    return cudaSuccess;
 }
 
 // Curvature pair of one iteration (qn.py:85-92, 245-252) in one pass:
@@ -645,31 +654,32 @@ namespace dm {
 int curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,
                    double *y, int64_t n, double *partial, double *sy, void *stream) {
     const int64_t nch = (n + kChunk - 1) / kChunk;
-    if (n <= 0 || nch > kChunk) return DM_ERR_UNSUPPORTED;
+    if (n <= 0 || nch >= INT32_MAX) return DM_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     const bool vec = aligned16(lam) && aligned16(lam_prev) && aligned16(g) && aligned16(g_prev) && aligned16(s) &&
                      aligned16(y);
     FinishPlans plans;
     plans.chunk = make_sum_plan(kChunk);
     plans.tail = make_sum_plan((int)(n % kChunk));
-    plans.totals = make_sum_plan((int)nch);
+    plans.totals = make_sum_plan(nch > kChunk ? 0 : (int)nch);
     curvature_pair_kernel<<<(unsigned)nch, kChunkThreads, 0, st>>>(lam, lam_prev, g, g_prev, s, y, n, vec, partial,
                                                                    plans);
     cudaError_t e = cudaGetLastError();
     if (e) return fail(e, "curvature_pair");
     // totals only: every chunk is done (`full` = nch), so the finishing block just reduces them
+    if (nch > kChunk) return dm::pairwise_device(partial, nch, sy, st);
     ChunkStep a{};
     a.x = s;
     a.v = y;
     a.dot_out = sy;
-    e = launch_maybe_pdl(chunk_finish_kernel<kDot>, 1, kFinishThreads, st, true, a, n, nch, partial, plans);
+    e = launch_maybe_pdl(chunk_finish_kernel<kDot>, 1, kFinishThreads, st, true, a, n, nch, partial, plans, true);
     return e == cudaSuccess ? DM_OK : fail(e, "curvature_pair finish");
 }
 
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream) {
     const int64_t nch = (n + kChunk - 1) / kChunk;
-    if (n <= 0 || nch > kChunk || m < 1) return DM_ERR_UNSUPPORTED;
+    if (n <= 0 || nch >= INT32_MAX || m < 1) return DM_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     // slots: [0, m) first-loop dots, [m, 2m) alphas, 2m = y0.y0, [2m+1, 3m+1) second-loop dots
     double *dot1 = slots, *alpha = slots + m, *yy = slots + 2 * m, *dot2 = slots + 2 * m + 1;
@@ -720,7 +730,7 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
 
 int chunk_dot(const double *a, const double *b, int64_t n, double *partial, double *out, void *stream) {
     const int64_t nch = (n + kChunk - 1) / kChunk;
-    if (n <= 0 || nch > kChunk || !b) return DM_ERR_UNSUPPORTED;
+    if (n <= 0 || nch >= INT32_MAX || !b) return DM_ERR_UNSUPPORTED;
     ChunkStep st{};
     st.x = const_cast<double *>(a);  // read only in kDot mode
     st.v = b;

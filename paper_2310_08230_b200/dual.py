@@ -254,12 +254,14 @@ class DualState:
         self.dev.dfr_backward(omega, self.lam_d, self.avg, self.F_il, self.B_il, self.mbar, self._bounds)
         if ev:
             timer.end(ev)
-        ev = timer.begin("dfr_average") if timer else None
-        self.dev.dfr_average(self.mbar, self.avg)
+        # flush: the backward pass's escrow straight into the duals, then a
+        # plain sweep rebuilds B (and the argmin decisions) for them
+        ev = timer.begin("dfr_flush") if timer else None
+        self.dev.dfr_flush(self.mbar, self.lam_d)
         if ev:
             timer.end(ev)
-        ev = timer.begin("dfr_flush") if timer else None
-        self.dev.dfr_backward(0.0, self.lam_d, self.avg, None, self.B_il, None, self._bounds, record_decisions=True)
+        ev = timer.begin("dfr_sweep") if timer else None
+        self.dev.dfr_backward(0.0, self.lam_d, None, None, self.B_il, None, self._bounds, record_decisions=True)
         if ev:
             timer.end(ev)
         self._bgen += 1

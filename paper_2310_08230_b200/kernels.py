@@ -158,6 +158,9 @@ class DeviceFlat:
     def dfr_average(self, mbar, avg):
         _native.call("dm_dfr_average", self._h, _ptr(mbar), _ptr(avg), self._s())
 
+    def dfr_flush(self, mbar, lam):
+        _native.call("dm_dfr_flush", self._h, _ptr(mbar), _ptr(lam), self._s())
+
     def dfr_to_nodes(self, x_il, x):
         _native.call("dm_dfr_to_nodes", self._h, _ptr(x_il), _ptr(x), self._s())
 

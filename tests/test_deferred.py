@@ -142,14 +142,18 @@ def test_deferred_passes_match_oracle(case, omega):
     assert _nodes(st, st.B_il).tobytes() == ost.B.tobytes()
     assert st.mbar.cpu().numpy().tobytes() == mbar.tobytes()
     assert st._bounds.cpu().numpy().tobytes() == bounds.tobytes()
-    # flush sweep
+    # flush: average + a sweep adding it == dm_dfr_flush (average into lam) + a plain sweep
+    lam2, B2, b2 = st.lam_d.clone(), st.B_il.clone(), st._bounds.clone()
     st.dev.dfr_average(st.mbar, st.avg)
+    st.dev.dfr_backward(0.0, lam2, st.avg, None, B2, None, b2)
+    st.dev.dfr_flush(st.mbar, st.lam_d)
+    st.dev.dfr_backward(0.0, st.lam_d, None, None, st.B_il, None, st._bounds, record_decisions=True)
     lib.oracle_dfr_average(P, ptr(of.proc_ptr), ptr(of.proc_layers), ptr(mbar), ptr(avg))
-    st.dev.dfr_backward(0.0, st.lam_d, st.avg, None, st.B_il, None, st._bounds, record_decisions=True)
     lib.oracle_dfr_backward(*geo, 0.0, ptr(ost.lam), ptr(avg), None, ptr(ost.B), None, ptr(bounds))
-    assert st.lam.tobytes() == ost.lam.tobytes()
-    assert _nodes(st, st.B_il).tobytes() == ost.B.tobytes()
-    assert st._bounds.cpu().numpy().tobytes() == bounds.tobytes()
+    for lam_t, B_t, b_t in ((st.lam_d, st.B_il, st._bounds), (lam2, B2, b2)):
+        assert lam_t.cpu().numpy().tobytes() == ost.lam.tobytes()
+        assert _nodes(st, B_t).tobytes() == ost.B.tobytes()
+        assert b_t.cpu().numpy().tobytes() == bounds.tobytes()
 
 
 @pytest.mark.gpu

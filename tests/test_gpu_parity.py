@@ -154,7 +154,9 @@ def test_sweep_kernels_on_random_duals(name):
 # 3849..4095 (and totals counts in that range) are the lengths whose numpy
 # pairwise tree has 33 leaves
 @pytest.mark.parametrize("n", [0, 1, 5, 7, 8, 9, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 3849, 4095, 4096, 4097,
-                               2 * 4096 + 4000, 65537, 636_800, 2_000_003, 3849 * 4096 - 7])
+                               2 * 4096 + 4000, 65537, 636_800, 2_000_003, 3849 * 4096 - 7,
+                               # more than 4096 chunks: totals reduced through the dm_sum tree
+                               4096 * 4096, 4096 * 4096 + 1, 20_000_003, 40_000_000])
 def test_pairwise_sum_and_dot_match_numpy(n):
     rng = np.random.default_rng(n)
     a = rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)
@@ -481,3 +483,54 @@ def test_exact_pass_division_matches_ddiv(k):
     bad = ctypes.c_ulonglong(0)
     _native.check(_native.load().dm_debug_div_check(k, 1 << 26, 12345 + k, ctypes.byref(bad)))
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("n", [4096 * 4096 + 4096, 20_000_003])
+def test_two_loop_and_curvature_pair_beyond_4096_chunks(n):
+    """The fused L-BFGS two-loop and the curvature pair on vectors longer than
+    4096 chunks, bitwise against the oracle's two-loop in chunked-dot order."""
+    from paper_2310_08230_b200.kernels import dev_curvature_pair, dev_lbfgs_direction
+
+    rng = np.random.default_rng(5)
+    dev = torch.device("cuda")
+    pairs_h, pairs_d = [], []
+    for _ in range(3):
+        s_ = rng.standard_normal(n)
+        y_ = s_ + 0.1 * rng.standard_normal(n)
+        sy = solver._dot_chunked(s_, y_)
+        pairs_h.append((s_, y_, 1.0 / sy, sy))
+        pairs_d.append((torch.as_tensor(s_, device=dev), torch.as_tensor(y_, device=dev), 1.0 / sy, sy))
+    g = rng.standard_normal(n)
+    d = torch.empty(n, dtype=torch.float64, device=dev)
+    dev_lbfgs_direction(torch.as_tensor(g, device=dev), pairs_d, d)
+    want = solver.lbfgs(g, pairs_h, solver._dot_chunked)
+    assert d.cpu().numpy().tobytes() == want.tobytes()
+    lam, lam_prev = torch.as_tensor(rng.standard_normal(n), device=dev), torch.as_tensor(rng.standard_normal(n), device=dev)
+    gg, gp = torch.as_tensor(rng.standard_normal(n), device=dev), torch.as_tensor(rng.standard_normal(n), device=dev)
+    s_o, y_o = torch.empty_like(lam), torch.empty_like(lam)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    want_sy = solver._dot_chunked((lam - lam_prev).cpu().numpy(), (gp - gg).cpu().numpy())
+    dev_curvature_pair(lam, lam_prev, gg, gp, s_o, y_o, out)
+    assert float(out.item()) == want_sy
+
+
+def test_layers_wider_than_32_raise_unsupported_instance():
+    """dm_flat_create's envelope: a cardinality row whose
+    diagram has a 33-node layer raises the typed error, not a crash."""
+    from paper_2310_08230_b200.errors import UnsupportedInstance
+
+    n = 70
+    inst = IlpInstance.from_rows(np.arange(n, dtype=np.float64), [make_row(list(range(n)), [1] * n, 32)],
+                                 chunk_size=0)
+    assert inst.flat.max_width >= 33
+    with pytest.raises(UnsupportedInstance):
+        init_duals(inst)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_solve_on_a_non_current_device_restores_the_current_device():
+    inst = kinked()
+    torch.cuda.set_device(0)
+    res = qn.solve(inst, SolveConfig(max_iterations=3), device="cuda:1")
+    assert torch.cuda.current_device() == 0
+    assert res.state.device == torch.device("cuda", 1)
