@@ -382,10 +382,12 @@ def algorithmic_bytes(flat):
         # lam r/w 16 + escrow write 8 (+ average read 8, backward) per layer; bound 8 per diagram
         "dfr_forward": 24 * N + 24 * L + 8 * nb,
         "dfr_backward": 24 * N + 32 * L + 8 * nb,
-        # flush sweep: arcs 8 + table write 8 per node; lam r/w 16 + average read 8 + decision word 8 per layer
-        "dfr_flush": 16 * N + 32 * L + 8 * nb,
         # segmented average: escrow read 8 + copy index 4 + average write 8 per layer; CSR offset 4 per variable
         "dfr_average": 20 * L + 4 * P,
+        # flush (average applied to the duals): escrow read 8 + copy index 4 + lam r/w 16 per layer; 4 per variable
+        "dfr_flush": 28 * L + 4 * P,
+        # plain sweep after the flush: arcs 8 + table write 8 per node; lam 8 + decision word 8 per layer
+        "dfr_sweep": 16 * N + 16 * L + 8 * nb,
     }
 
 

@@ -224,6 +224,25 @@ int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *s
  * identical to a later pass adding avg_in); follow it by a plain
  * dm_dfr_backward (mbar = avg_in = NULL) to rebuild B_il for the new duals */
 int dm_dfr_flush(const dm_flat *f, const double *mbar, double *lam, void *stream);
+/* Partitioned instances (one instance's diagrams split over ranks; the
+ * north star's C4 split, paper_2310_08230_b200/partition.py).
+ * dm_dfr_average_csr: dm_dfr_average / dm_dfr_flush (apply != 0) over a
+ * caller-supplied visitation CSR (device int32: the rank's variables whose
+ * copies are all local).  A variable with copies on several ranks is
+ * averaged through an exchange buffer with one slot per copy in global copy
+ * order: dm_dfr_boundary_gather writes buf[slot[i]] = mbar[layer[i]] for the
+ * rank's boundary copies (buf zeroed before, every slot has one writer, so
+ * an allreduce-sum over ranks completes it exactly), and
+ * dm_dfr_boundary_average writes (apply: adds) the mean of the finite
+ * entries of buf[slot_lo[i], slot_hi[i]) to out[layer[i]] — the same
+ * arithmetic as dm_dfr_average, so a partitioned run is bit-identical to
+ * the one-GPU run. */
+int dm_dfr_average_csr(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar,
+                       double *out, int apply, void *stream);
+int dm_dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, const double *mbar, double *buf,
+                           void *stream);
+int dm_dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,
+                            const int32_t *slot_hi, const double *buf, double *out, int apply, void *stream);
 /* interleaved table -> FlatBdds node order */
 int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream);
 

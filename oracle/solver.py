@@ -295,7 +295,7 @@ def solve(inst: OracleInstance, mode="hybrid", max_iterations=2000, dual_toleran
                 hist.appendleft((s, y, 1.0 / sy, sy))
             lam_prev = st.lam.copy()
             g_prev = g_now
-        k = stall_window if stall_window is not None else (8 if schedule == "deferred" else 1)
+        k = stall_window if stall_window is not None else (32 if schedule == "deferred" else 1)
         if k == 1:
             if bound - records[-2][2] < dual_tolerance * max(1.0, abs(bound)):
                 reason = "dual_tolerance"

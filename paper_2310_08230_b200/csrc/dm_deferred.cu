@@ -379,6 +379,44 @@ __global__ void dfr_to_nodes_kernel(dm::SweepDev s, const double *__restrict__ x
     }
 }
 
+// --------------------------------------------------------------------------
+// Partitioned instances (partition.py): the diagrams are split over ranks,
+// and a variable whose copies span ranks ("boundary" variable) is averaged
+// from an exchange buffer that holds one slot per copy in global copy order
+// (each rank writes its copies' escrow, zeros elsewhere; one allreduce-sum
+// per pass makes it whole — exact, every slot has one contributor).
+__global__ void dfr_boundary_gather_kernel(int64_t n, const int32_t *__restrict__ layer,
+                                           const int32_t *__restrict__ slot, const double *__restrict__ mbar,
+                                           double *__restrict__ buf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) buf[slot[i]] = mbar[layer[i]];
+}
+
+// per local boundary copy i: the mean of the finite escrow in
+// buf[slot_lo[i], slot_hi[i]) (copy order, from 0.0 — dfr_average_kernel's
+// arithmetic), written to out[layer[i]] (apply: added to it)
+template <bool kApply>
+__global__ void dfr_boundary_average_kernel(int64_t n, const int32_t *__restrict__ layer,
+                                            const int32_t *__restrict__ slot, const int32_t *__restrict__ slot_lo,
+                                            const int32_t *__restrict__ slot_hi, const double *__restrict__ buf,
+                                            double *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double sum = 0.0;
+    int32_t cnt = 0;
+    for (int32_t t = slot_lo[i]; t < slot_hi[i]; ++t) {
+        const double x = buf[t];
+        if (x != DM_INF) {
+            sum = __dadd_rn(sum, x);
+            ++cnt;
+        }
+    }
+    const double mean = cnt ? __ddiv_rn(sum, (double)cnt) : 0.0;
+    const double a = buf[slot[i]] != DM_INF ? mean : 0.0;
+    const int32_t l = layer[i];
+    out[l] = kApply ? __dadd_rn(out[l], a) : a;
+}
+
 int fail(cudaError_t e, const char *what) {
     dm::set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return DM_ERR_CUDA;
@@ -455,4 +493,27 @@ int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream)
     return e == cudaSuccess ? DM_OK : fail(e, "dfr_to_nodes");
 }
 
+int dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, const double *mbar, double *buf,
+                        void *stream) {
+    if (n <= 0) return DM_OK;
+    dfr_boundary_gather_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, layer, slot, mbar, buf);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, "dfr_boundary_gather");
+}
+
+int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,
+                         const int32_t *slot_hi, const double *buf, double *out, bool apply, void *stream) {
+    if (n <= 0) return DM_OK;
+    const int blocks = (int)((n + 255) / 256);
+    if (apply)
+        dfr_boundary_average_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(n, layer, slot, slot_lo, slot_hi,
+                                                                                     buf, out);
+    else
+        dfr_boundary_average_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(n, layer, slot, slot_lo,
+                                                                                      slot_hi, buf, out);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, "dfr_boundary_average");
+}
+
 }  // namespace dm
+

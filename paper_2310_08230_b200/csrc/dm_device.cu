@@ -2384,6 +2384,36 @@ int dm_dfr_flush(const dm_flat *f, const double *mbar, double *lam, void *stream
     return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, lam, true, stream);
 }
 
+int dm_dfr_average_csr(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar,
+                       double *out, int apply, void *stream) {
+    DM_STREAM_GUARD(stream);
+    if (P < 0 || P >= INT32_MAX || (P > 0 && (!proc_ptr || !proc_layers || !mbar || !out))) {
+        dm::set_error("dm_dfr_average_csr: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_average(P, proc_ptr, proc_layers, mbar, out, apply != 0, stream);
+}
+
+int dm_dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, const double *mbar, double *buf,
+                           void *stream) {
+    DM_STREAM_GUARD(stream);
+    if (n < 0 || (n > 0 && (!layer || !slot || !mbar || !buf))) {
+        dm::set_error("dm_dfr_boundary_gather: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_boundary_gather(n, layer, slot, mbar, buf, stream);
+}
+
+int dm_dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,
+                            const int32_t *slot_hi, const double *buf, double *out, int apply, void *stream) {
+    DM_STREAM_GUARD(stream);
+    if (n < 0 || (n > 0 && (!layer || !slot || !slot_lo || !slot_hi || !buf || !out))) {
+        dm::set_error("dm_dfr_boundary_average: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    return dm::dfr_boundary_average(n, layer, slot, slot_lo, slot_hi, buf, out, apply != 0, stream);
+}
+
 int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream) {
     DM_CHECK_FLAT(f);
     if (!x_il || !x) {

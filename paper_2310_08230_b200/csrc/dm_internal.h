@@ -178,6 +178,10 @@ int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const d
 int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *out,
                 bool apply, void *stream);
 int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream);
+int dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, const double *mbar, double *buf,
+                        void *stream);
+int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,
+                         const int32_t *slot_hi, const double *buf, double *out, bool apply, void *stream);
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
 
