@@ -2,8 +2,9 @@
 across 1/2/4/8 B200 with NCCL marginal allreduce").
 
 No reference counterpart: the reference is single-process (SURVEY.md §2.2);
-the plan is SURVEY.md §5(b).  The diagrams are cut into k contiguous blocks
-(balanced by node count); each rank owns its block's diagrams, their nodes,
+the plan is SURVEY.md §5(b).  The diagrams are cut into k compact blocks
+(slabs of a breadth-first diagram order, balanced by node count); each rank
+owns its block's diagrams, their nodes,
 duals and distance tables, and runs the DEFERRED averaging schedule
 (dm_deferred.cu) on them — within a pass every diagram is independent, so
 the only data-plane exchange is, per pass, the escrow of the variables whose
@@ -52,10 +53,8 @@ class PartPlan:
     """What one rank owns and how its boundary copies map into the buffer."""
 
     rank: int
-    bdd_lo: int
-    bdd_hi: int
-    layer_lo: int
-    layer_hi: int
+    bdds: np.ndarray  # global ids of the diagrams this rank owns (ascending)
+    layers: np.ndarray  # global ids of their layers (local layer i = global layers[i])
     table: FlatTable  # local FlatBdds arrays (local diagram / layer / node ids, global variable ids)
     local_ptr: np.ndarray  # visitation CSR of the variables whose copies are all on this rank (int32)
     local_layers: np.ndarray
@@ -69,8 +68,8 @@ class PartPlan:
 @dataclass
 class PartitionPlan:
     k: int
-    cuts: list  # diagram ids: part r owns [cuts[r], cuts[r+1])
     parts: list
+    bdd_order: np.ndarray  # the parts' diagrams concatenated in rank order (global ids)
     slots: int  # boundary exchange buffer length (copies of boundary variables)
     boundary_variables: int
     variables_with_copies: int
@@ -81,32 +80,89 @@ class PartitionPlan:
         return self.boundary_variables / max(self.variables_with_copies, 1)
 
 
-def diagram_cuts(flat, k: int) -> list:
-    """k contiguous diagram blocks with (nearly) equal node counts."""
+def _diagram_graph(flat):
+    """CSR of diagram -> diagrams sharing a variable with it (through the
+    visitation CSR), as (ptr, nbr) int64 arrays; duplicates kept."""
+    ptr, pl = flat.proc_ptr, flat.proc_layers
+    cnt = np.diff(ptr)
+    pos = np.repeat(np.arange(len(cnt)), cnt)
+    bdd_of_copy = flat.layer_bdd[pl]
+    # every ordered pair of copies of one variable (degrees are small: <= 32)
+    src, dst = [], []
+    for d in range(1, int(cnt.max()) if len(cnt) else 1):
+        ok = np.flatnonzero((np.arange(len(pl)) - ptr[pos] + d) < cnt[pos])
+        src.append(bdd_of_copy[ok])
+        dst.append(bdd_of_copy[ok + d])
+    src = np.concatenate(src + [np.zeros(0, np.int64)])
+    dst = np.concatenate(dst + [np.zeros(0, np.int64)])
+    u = np.concatenate([src, dst])
+    v = np.concatenate([dst, src])
+    order = np.argsort(u, kind="stable")
+    nb = flat.num_bdds
+    gptr = np.zeros(nb + 1, np.int64)
+    np.add.at(gptr, u + 1, 1)
+    return np.cumsum(gptr), v[order]
+
+
+def diagram_order(flat) -> np.ndarray:
+    """Breadth-first order of the diagram graph (diagrams adjacent when they
+    share a variable) from a far corner: consecutive runs of it are compact
+    regions of the instance, so cutting it into k slabs leaves few variables
+    with copies on two sides (a bandwidth-reducing, Cuthill-McKee-like order;
+    every component is walked in turn)."""
+    nb = flat.num_bdds
+    gptr, nbr = _diagram_graph(flat)
+    seen = np.zeros(nb, bool)
+    out = []
+
+    def bfs(start):
+        lvl = np.array([start])
+        seen[start] = True
+        order = [lvl]
+        while len(lvl):
+            lo, hi = gptr[lvl], gptr[lvl + 1]
+            idx = np.repeat(lo - np.cumsum(np.concatenate([[0], (hi - lo)[:-1]])), hi - lo) + np.arange((hi - lo).sum())
+            cand = np.unique(nbr[idx]) if len(idx) else np.zeros(0, np.int64)
+            cand = cand[~seen[cand]]
+            seen[cand] = True
+            lvl = cand
+            if len(cand):
+                order.append(cand)
+        return np.concatenate(order)
+
+    for root in range(nb):
+        if seen[root]:
+            continue
+        first = bfs(root)  # pseudo-peripheral start: the last diagram reached from an arbitrary one
+        seen[first] = False
+        out.append(bfs(int(first[-1])))
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def plan_partition(instance: IlpInstance, k: int, order: np.ndarray | None = None) -> PartitionPlan:
+    """Cut the diagrams into k parts of (nearly) equal node counts along
+    ``order`` (default: diagram_order, compact slabs) and build each rank's
+    local table, averaging CSR and boundary slots."""
+    flat = instance.flat
     nb = flat.num_bdds
     if not 1 <= k <= max(nb, 1):
         raise ValueError(f"cannot split {nb} diagrams into {k} parts")
-    node_end = flat.layer_node_lo[flat.bdd_layer_lo[1:]]  # nodes up to the end of each diagram
-    total = flat.num_nodes
-    cuts = [0]
-    for r in range(1, k):
-        c = int(np.searchsorted(node_end, total * r / k, side="left")) + 1
-        cuts.append(min(max(c, cuts[-1] + 1), nb - (k - r)))
-    cuts.append(nb)
-    return cuts
-
-
-def plan_partition(instance: IlpInstance, k: int) -> PartitionPlan:
-    flat = instance.flat
-    cuts = diagram_cuts(flat, k)
     bl, lnl = flat.bdd_layer_lo, flat.layer_node_lo
-    layer_rank = np.repeat(np.arange(k), [int(bl[cuts[r + 1]] - bl[cuts[r]]) for r in range(k)])
+    order = diagram_order(flat) if order is None else np.asarray(order, np.int64)
+    sizes = lnl[bl[order + 1]] - lnl[bl[order]]
+    ends = np.cumsum(sizes)
+    cut = [0] + [int(np.searchsorted(ends, ends[-1] * r / k, side="left")) + 1 for r in range(1, k)] + [nb]
+    for r in range(1, k):  # every part non-empty
+        cut[r] = min(max(cut[r], cut[r - 1] + 1), nb - (k - r))
+    bdd_rank = np.empty(nb, np.int64)
+    for r in range(k):
+        bdd_rank[order[cut[r]:cut[r + 1]]] = r
+    layer_rank = bdd_rank[flat.layer_bdd]
     ptr, pl = flat.proc_ptr, flat.proc_layers
     P = len(ptr) - 1
     cnt = np.diff(ptr)
     pos_of_copy = np.repeat(np.arange(P), cnt)
     copy_rank = layer_rank[pl]
-    # a position is on the boundary when its copies are not all on one rank
     first_rank = np.full(P, -1, np.int64)
     first_rank[cnt > 0] = copy_rank[ptr[:-1][cnt > 0]]
     mixed = np.zeros(P, bool)
@@ -121,44 +177,58 @@ def plan_partition(instance: IlpInstance, k: int) -> PartitionPlan:
     lam_all = instance.costs[flat.layer_var] / counts[flat.layer_var]
     free = np.flatnonzero(counts == 0)
     free_contribution = float(np.minimum(instance.costs[free], 0.0).sum()) if len(free) else 0.0
+
+    def ranges(lo, hi):  # concatenation of [lo_i, hi_i)
+        n = hi - lo
+        return np.repeat(lo - np.concatenate([[0], np.cumsum(n)[:-1]]), n) + np.arange(n.sum())
+
     parts = []
     for r in range(k):
-        b0, b1 = cuts[r], cuts[r + 1]
-        L0, L1 = int(bl[b0]), int(bl[b1])
-        N0, N1 = int(lnl[L0]), int(lnl[L1])
+        sel = np.sort(order[cut[r]:cut[r + 1]])
+        nl = bl[sel + 1] - bl[sel]
+        g_layers = ranges(bl[sel], bl[sel + 1])
+        g_nodes = ranges(lnl[g_layers], lnl[g_layers + 1])
         t = FlatTable()
         t.costs = instance.costs
         t.variable_order = instance.variable_order
         t.constraint_counts = counts
-        t.bdd_layer_lo = bl[b0:b1 + 1] - L0
-        t.layer_node_lo = lnl[L0:L1 + 1] - N0
-        t.layer_var = flat.layer_var[L0:L1].copy()
-        t.layer_bdd = flat.layer_bdd[L0:L1] - b0
-        z, o = flat.zero_t[N0:N1], flat.one_t[N0:N1]
-        t.zero_t = np.where(z >= 0, z - N0, z)
-        t.one_t = np.where(o >= 0, o - N0, o)
+        t.bdd_layer_lo = np.concatenate([[0], np.cumsum(nl)]).astype(np.int64)
+        t.layer_node_lo = np.concatenate([[0], np.cumsum(lnl[g_layers + 1] - lnl[g_layers])]).astype(np.int64)
+        t.layer_var = flat.layer_var[g_layers]
+        t.layer_bdd = np.repeat(np.arange(len(sel), dtype=np.int64), nl)
+        z, o = flat.zero_t[g_nodes], flat.one_t[g_nodes]
+        t.zero_t = np.where(z >= 0, np.searchsorted(g_nodes, np.maximum(z, 0)), z).astype(np.int64)
+        t.one_t = np.where(o >= 0, np.searchsorted(g_nodes, np.maximum(o, 0)), o).astype(np.int64)
         mine = copy_rank == r
         # full local visitation CSR (every local layer visited, global copy order kept)
         lcnt = np.bincount(pos_of_copy[mine], minlength=P)
         t.proc_ptr = np.concatenate([[0], np.cumsum(lcnt)]).astype(np.int64)
-        t.proc_layers = (pl[mine] - L0).astype(np.int64)
+        t.proc_layers = np.searchsorted(g_layers, pl[mine]).astype(np.int64)
         widths = np.diff(t.layer_node_lo)
         t.max_width = int(widths.max()) if len(widths) else 0
         t.max_degree = int(lcnt.max()) if P else 0
-        t.max_layers = int(np.diff(t.bdd_layer_lo).max()) if b1 > b0 else 0
+        t.max_layers = int(nl.max()) if len(nl) else 0
         # averaging CSR over the variables whose copies are all here
         only = mine & ~mixed[pos_of_copy]
         ocnt = np.bincount(pos_of_copy[only], minlength=P)
-        keep = ocnt > 0
-        local_ptr = np.concatenate([[0], np.cumsum(ocnt[keep])]).astype(np.int32)
-        local_layers = (pl[only] - L0).astype(np.int32)
+        local_ptr = np.concatenate([[0], np.cumsum(ocnt[ocnt > 0])]).astype(np.int32)
+        local_layers = np.searchsorted(g_layers, pl[only]).astype(np.int32)
         bm = mine & mixed[pos_of_copy]
         bpos_idx = np.searchsorted(bpos, pos_of_copy[bm])
-        parts.append(PartPlan(r, b0, b1, L0, L1, t, local_ptr, local_layers,
-                              (pl[bm] - L0).astype(np.int32), copy_slot[bm].astype(np.int32),
+        parts.append(PartPlan(r, sel, g_layers, t, local_ptr, local_layers,
+                              np.searchsorted(g_layers, pl[bm]).astype(np.int32), copy_slot[bm].astype(np.int32),
                               bptr[bpos_idx].astype(np.int32), bptr[bpos_idx + 1].astype(np.int32),
-                              np.ascontiguousarray(lam_all[L0:L1])))
-    return PartitionPlan(k, cuts, parts, int(bptr[-1]), len(bpos), int((cnt > 0).sum()), free_contribution)
+                              np.ascontiguousarray(lam_all[g_layers])))
+    return PartitionPlan(k, parts, np.concatenate([p.bdds for p in parts]), int(bptr[-1]), len(bpos),
+                         int((cnt > 0).sum()), free_contribution)
+
+
+def scatter_duals(plan: PartitionPlan, lam_parts: list, num_layers: int) -> np.ndarray:
+    """The global dual vector (FlatBdds layer order) from the parts' duals."""
+    lam = np.empty(num_layers)
+    for p, x in zip(plan.parts, lam_parts):
+        lam[p.layers] = x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+    return lam
 
 
 # --------------------------------------------------------------------------- communicators
@@ -289,6 +359,7 @@ class PartitionedSolver:
         if self.cfg.mode != "mma-only":
             raise ValueError("partitioned solves run the averaging-only mode (mode='mma-only')")
         self.bufs = [e.new_buffer(plan.slots) for e in engines]
+        self._perm = torch.as_tensor(plan.bdd_order)
 
     def _exchange(self, apply: bool):
         for e in self.engines:
@@ -300,37 +371,52 @@ class PartitionedSolver:
             e.average_boundary(b, apply)
 
     def _bound(self) -> float:
-        alls = self.comm.allgather_cat([e.bounds for e in self.engines])
-        return self.engines[0].global_bound(alls[0]) + self.plan.free_contribution
+        alls = self.comm.allgather_cat([e.bounds for e in self.engines])[0]
+        ordered = torch.empty_like(alls)
+        ordered[self._perm.to(alls.device)] = alls  # back to global diagram order: numpy's summation order
+        return self.engines[0].global_bound(ordered) + self.plan.free_contribution
 
-    def solve(self, clock=time.perf_counter) -> PartitionedResult:
-        cfg, omega = self.cfg, self.cfg.mma_damping
-        t0 = clock()
+    def start(self, clock=time.perf_counter) -> "PartitionedSolver":
+        self.clock = clock
+        self.t0 = clock()
         for e in self.engines:
             e.sweep()
-        bounds, times = [self._bound()], [clock() - t0]
+        self.bounds, self.times = [self._bound()], [clock() - self.t0]
+        self.iterations = 0
+        return self
+
+    def step(self) -> str | None:
+        """One deferred averaging round over all parts; the stop reason or None."""
+        cfg, omega = self.cfg, self.cfg.mma_damping
+        for e in self.engines:
+            e.forward_pass(omega)
+        self._exchange(apply=False)
+        for e in self.engines:
+            e.backward_pass(omega)
+        self._exchange(apply=True)  # the flush: escrow straight into the duals
+        for e in self.engines:
+            e.sweep()
+        b = self._bound()
+        self.bounds.append(b)
+        self.times.append(self.clock() - self.t0)
+        self.iterations += 1
+        it, k, bounds = self.iterations, cfg.effective_stall_window, self.bounds
+        if k == 1:
+            if b - bounds[-2] < cfg.dual_tolerance * max(1.0, abs(b)):
+                return "dual_tolerance"
+        elif it >= k and max(bounds[-k:]) - max(bounds[:-k]) < cfg.dual_tolerance * max(1.0, abs(b)):
+            return "dual_tolerance"
+        if cfg.max_seconds is not None and self.times[-1] > cfg.max_seconds:
+            return "max_seconds"
+        return None
+
+    def solve(self, clock=time.perf_counter) -> PartitionedResult:
+        self.start(clock)
         reason = "max_iterations"
-        k = cfg.effective_stall_window
-        for it in range(1, cfg.max_iterations + 1):
-            for e in self.engines:
-                e.forward_pass(omega)
-            self._exchange(apply=False)
-            for e in self.engines:
-                e.backward_pass(omega)
-            self._exchange(apply=True)  # the flush: escrow straight into the duals
-            for e in self.engines:
-                e.sweep()
-            b = self._bound()
-            bounds.append(b)
-            times.append(clock() - t0)
-            if k == 1:
-                if b - bounds[-2] < cfg.dual_tolerance * max(1.0, abs(b)):
-                    reason = "dual_tolerance"
-                    break
-            elif it >= k and max(bounds[-k:]) - max(bounds[:-k]) < cfg.dual_tolerance * max(1.0, abs(b)):
-                reason = "dual_tolerance"
+        for _ in range(self.cfg.max_iterations):
+            r = self.step()
+            if r is not None:
+                reason = r
                 break
-            if cfg.max_seconds is not None and clock() - t0 > cfg.max_seconds:
-                reason = "max_seconds"
-                break
-        return PartitionedResult(bounds, max(bounds), len(bounds) - 1, reason, [e.lam for e in self.engines], times)
+        return PartitionedResult(self.bounds, max(self.bounds), self.iterations, reason,
+                                 [e.lam for e in self.engines], self.times)
