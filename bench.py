@@ -55,6 +55,7 @@ def parse():
                     help="averaging schedule of the headline line (the other one is reported as an extra key)")
     ap.add_argument("--no-extras", action="store_true", help="headline only: no other-schedule / C4 / C5 keys")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--split", action="store_true", help="one instance's diagrams partitioned over the ranks (C4)")
     ap.add_argument("--cpu-budget", type=float, default=300.0, help="wall budget (s) of a CPU time-to-gap run")
     ap.add_argument("--batch", type=int, default=0, help="also time K independent instances via qn.solve_batch")
     ap.add_argument("--batch-iters", type=int, default=30)
@@ -642,44 +643,129 @@ def c5_instances(seeds):
     return [build_instance("c3", s) for s in seeds]
 
 
-def c5_solve(insts, dev, schedule, streams):
-    """One C5 step: every instance solved from its lowered HOST arrays (device
-    upload and plans included) to the reference's stopping rule, ``streams``
-    solves in flight (qn.solve_batch).  Returns (seconds, results)."""
+def c5_solve(insts, dev, schedule):
+    """One C5 step: the batch merged into one block-diagonal instance
+    (batch.py) from the lowered HOST tables — merge, upload, plans, the hybrid
+    solve to the reference's stopping rule and the per-instance bounds read
+    back, all inside the clock.  Returns (seconds, BatchResult)."""
     import torch
 
-    from paper_2310_08230_b200.config import SolveConfig
-    from paper_2310_08230_b200.qn import solve_batch
+    from paper_2310_08230_b200.batch import solve_merged
 
     torch.cuda.synchronize()
     t = time.perf_counter()
-    res = solve_batch(insts, SolveConfig(mode="hybrid", mma_schedule=schedule), device=dev, concurrency=streams)
+    res = solve_merged(insts, SolveConfigC5(schedule), device=dev)
     torch.cuda.synchronize()
     return time.perf_counter() - t, res
 
 
-def c5_summary(args, dev, reps=3):
+def SolveConfigC5(schedule):  # noqa: N802 - a config factory
+    from paper_2310_08230_b200.config import SolveConfig
+
+    return SolveConfig(mode="hybrid", mma_schedule=schedule, max_iterations=3000)
+
+
+def c5_summary(args, dev, reps=5):
     """Config C5 on this GPU (the default line's extra key): 64 independent
-    ~500-triangle pairs, each solved to the stopping rule; median of ``reps``
-    repetitions after one warm-up, and their spread."""
+    ~500-triangle pairs solved as one merged instance; median of ``reps``
+    repetitions after one warm-up, their spread, and each instance's bound
+    against its own d* (the best bound of its separate converged solve)."""
     import numpy as np
 
+    from paper_2310_08230_b200.qn import solve
+
     insts = c5_instances(range(args.seed, args.seed + C5_INSTANCES))
-    out = {"workload": f"c5: {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}, solved from host arrays "
-                       "(upload + plans included) to the reference's stopping rule", "streams": args.streams}
+    out = {"workload": f"c5: {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}, solved as ONE merged "
+                       "block-diagonal instance (batch.py) from the lowered host tables: merge, upload, plans, "
+                       "hybrid solve to the stopping rule and per-instance bounds inside the clock"}
+    sep = [solve(i, SolveConfigC5("exact"), device=dev).best_bound for i in insts]
     for schedule in ("exact", "deferred"):
-        c5_solve(insts[:8], dev, schedule, args.streams)  # warm-up
-        times, iters = [], 0
+        c5_solve(insts, dev, schedule)  # warm-up
+        times = []
         for _ in range(reps):
-            sec, res = c5_solve(insts, dev, schedule, args.streams)
+            sec, res = c5_solve(insts, dev, schedule)
             times.append(sec)
-            iters = sum(r.iterations for r in res)
-            bounds = [r.best_bound for r in res]
         med = float(np.median(times))
+        rel = [abs(b - d) / abs(d) for b, d in zip(res.bounds, sep)]
         out[schedule] = {"instances_per_s": C5_INSTANCES / med, "seconds": med, "runs_s": times,
-                         "spread": (max(times) - min(times)) / med, "iterations_total": iters,
-                         "mean_best_bound": float(np.mean(bounds))}
+                         "spread": (max(times) - min(times)) / med, "iterations": res.iterations,
+                         "stop": res.merged.stop_reason, "max_rel_gap_to_separate_solves": max(rel),
+                         "instances_within_1e-3": int(sum(r <= 1e-3 for r in rel))}
     return out
+
+
+def run_split(args, rank, world, local_rank):
+    """Config C4 split: ONE instance's diagrams partitioned over the ranks
+    (partition.py: breadth-first slabs), deferred-schedule averaging rounds
+    (mode "mma-only") with one NCCL allreduce of the boundary variables'
+    escrow per pass and an all-gather of the per-diagram optima per round.
+    One step = one round on every rank; bit-identical to the one-GPU solve
+    (tests/test_partition.py).  "scaling": "strong" (total work fixed)."""
+    import torch
+
+    from paper_2310_08230_b200.config import SolveConfig
+    from paper_2310_08230_b200.partition import DeviceEngine, DistComm, LoopbackComm, PartitionedSolver, plan_partition
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    inst = build_instance(args.config, args.seed)
+    t = time.perf_counter()
+    plan = plan_partition(inst, world)
+    t_plan = time.perf_counter() - t
+    part = plan.parts[rank]
+    eng = DeviceEngine(part, dev)
+    comm = DistComm([p.table.num_bdds for p in plan.parts]) if world > 1 else LoopbackComm()
+    cfg = SolveConfig(mode="mma-only", mma_schedule="deferred", max_iterations=10**9, dual_tolerance=-float("inf"))
+    run = PartitionedSolver(plan, [eng], comm, cfg).start()
+    with ClockSampler(local_rank) as clk:
+        time.sleep(1.0)
+        for _ in range(args.warmup):
+            run.step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        clk.mark()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(args.steps):
+            run.step()
+        end.record()
+        torch.cuda.synchronize()
+        clk.mark()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(end)
+    arcs = args.steps * 5 * 2 * part.table.num_nodes  # fw + bw passes (2 sweeps each) + the sweep
+    total_arcs, max_ms = aggregate_work_time(arcs, ms, world, dev)
+    # time to the 1e-3 gap of the split solve from init (stopping rule on), same d* as the other lines
+    e = d_star_for(args.config, args.seed, inst._rows_hash)
+    ttg = None
+    if not args.no_ttg and e:
+        res = PartitionedSolver(plan, [eng_fresh(part, dev)], comm,
+                                SolveConfig(mode="mma-only", mma_schedule="deferred", max_iterations=3000)).solve()
+        hit = next((i for i, b in enumerate(res.bounds) if e["d_star"] - b <= 1e-3 * abs(e["d_star"])), None)
+        ttg = {"value": res.times[hit] if hit is not None else None, "iterations": hit, "unit": "s", "gap": 1e-3,
+               "d_star": e["d_star"], "best_bound": res.best_bound, "stop": res.stop_reason,
+               "solve_iterations": res.iterations}
+    if rank != 0:
+        return None
+    return {
+        "metric": METRIC, "value": total_arcs / (max_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "ms_per_iteration": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload(args.config) + f", diagrams split over {world} GPU(s) (partition.py), "
+                                                       "deferred-schedule averaging rounds (mode mma-only)",
+                   "boundary_fraction": round(plan.boundary_fraction, 4),
+                   "exchange_bytes_per_pass": 8 * plan.slots, "plan_s": round(t_plan, 2),
+                   "parallelism": f"diagram-partitioned x{world}"},
+        "time_to_gap": ttg, "clocks": clk.summary(),
+    }
+
+
+def eng_fresh(part, dev):
+    from paper_2310_08230_b200.partition import DeviceEngine
+
+    return DeviceEngine(part, dev)
 
 
 def _peaks():
@@ -744,28 +830,25 @@ def run_c5(args, rank, world, local_rank):
     """Config C5: a batch of 64 independent ~500-triangle pairs (the C3
     generator, seeds 0..63), instance-sharded over ranks (rank r solves
     seeds r, r+N, ...; no collective on the data path).  One step = the
-    rank's share of the batch solved through qn.solve_batch (--streams
-    concurrent solves) from the lowered HOST instances (device upload and every plan
-    build included), each to the reference's stopping rule with the --schedule
-    averaging schedule; warm-up = W solves of the rank's first instance."""
+    rank's share of the batch merged into one block-diagonal instance
+    (batch.py) and solved from the lowered HOST tables (merge, device upload
+    and every plan build included) to the reference's stopping rule with the
+    --schedule averaging schedule; warm-up = W such solves."""
     import torch
 
     from paper_2310_08230_b200 import _native
-    from paper_2310_08230_b200.config import SolveConfig
-    from paper_2310_08230_b200.qn import solve, solve_batch
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     seeds = c5_seeds(rank, world)
     insts = c5_instances([args.seed + s for s in seeds])
-    cfg = SolveConfig(mode="hybrid", mma_schedule=args.schedule)
     h2d = sum(sum(getattr(i.flat, k).nbytes for k in ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd",
                                                       "zero_t", "one_t", "proc_ptr", "proc_layers"))
               + i.costs.nbytes for i in insts)
     with ClockSampler(local_rank) as clk:
         time.sleep(1.0)
         for _ in range(args.warmup):
-            solve(insts[0], cfg, device=dev)
+            c5_solve(insts, dev, args.schedule)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -776,8 +859,8 @@ def run_c5(args, rank, world, local_rank):
         start.record()
         arcs = 0
         for _ in range(args.steps):
-            res = solve_batch(insts, cfg, device=dev, concurrency=args.streams)
-            arcs += sum(r.state.arc_updates for r in res)
+            _, res = c5_solve(insts, dev, args.schedule)
+            arcs += res.merged.state.arc_updates
         end.record()
         torch.cuda.synchronize()
         clk.mark()
@@ -795,8 +878,9 @@ def run_c5(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "instances_per_s": n_inst / (max_ms / 1e3),
         "config": {"workload": f"c5: batch of {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}; "
-                               f"each solved from host arrays to the stopping rule ({args.schedule} schedule)",
-                   "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), {args.streams} streams per GPU",
+                               f"merged per GPU and solved from host arrays to the stopping rule ({args.schedule} "
+                               "schedule)",
+                   "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), merged into one instance per GPU",
                    "l2": "each solve uploads its instance (inputs not L2-resident across steps)"},
         "gpu_launches": _native.launch_count - l0,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -821,7 +905,8 @@ def main():
 
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = (run_c5 if args.config == "c5" else run_b200)(args, rank, world, local_rank)
+    fn = run_split if args.split else (run_c5 if args.config == "c5" else run_b200)
+    out = fn(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -1,0 +1,125 @@
+"""Independent instances solved as ONE merged instance (BASELINE config C5:
+a batch of 64 independent ~500-triangle pairs).
+
+No reference counterpart (the reference solves one instance per call,
+qn.py:211-259).  The batch's flat tables are concatenated block-diagonally
+(variables, diagrams, layers and nodes offset; visitation orders appended),
+so one upload, one set of plans and one launch per kernel serve every
+instance: the exact passes' persistent grid walks the interleaved DAG levels
+of all instances at once (depth = the deepest instance, not the sum), the
+sweeps and vector kernels see one long vector.  Diagrams of different
+instances never share a variable, so every averaging pass acts on each
+instance exactly as on its own — in mode "mma-only" the per-instance duals
+after n iterations are bit-identical to n-iteration solves of the instances
+one by one (tests/test_batch.py).  In hybrid mode the L-BFGS direction and
+step size are those of the merged dual (a block-diagonal quasi-Newton step),
+so per-instance trajectories differ from separate solves while every
+instance's duals stay feasible and its bound valid; parity is then at
+convergence (tests/test_batch.py).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .config import SolveConfig
+from .ilp import FlatTable, IlpInstance
+
+_FIELDS = ("bdd_layer_lo", "layer_node_lo", "layer_var", "layer_bdd", "zero_t", "one_t", "proc_ptr", "proc_layers")
+
+
+@dataclass
+class BatchIndex:
+    """Offsets of each instance in the merged arrays (length n + 1 each)."""
+
+    var: np.ndarray
+    bdd: np.ndarray
+    layer: np.ndarray
+    node: np.ndarray
+
+    def __len__(self) -> int:
+        return len(self.var) - 1
+
+
+def merge_instances(instances) -> tuple[IlpInstance, BatchIndex]:
+    """Block-diagonal concatenation of lowered instances (their FlatTables)."""
+    flats = [i.flat for i in instances]
+    if not flats:
+        raise ValueError("empty batch")
+    off = lambda xs: np.concatenate([[0], np.cumsum(xs)]).astype(np.int64)  # noqa: E731
+    vo = off([len(i.costs) for i in instances])
+    bo = off([f.num_bdds for f in flats])
+    lo = off([f.num_layers for f in flats])
+    no = off([f.num_nodes for f in flats])
+    t = FlatTable()
+    t.costs = np.concatenate([i.costs for i in instances])
+    t.variable_order = np.concatenate([i.variable_order + vo[k] for k, i in enumerate(instances)])
+    t.constraint_counts = np.concatenate([f.constraint_counts for f in flats])
+    t.bdd_layer_lo = np.concatenate([f.bdd_layer_lo[:-1] + lo[k] for k, f in enumerate(flats)] + [[lo[-1]]])
+    t.layer_node_lo = np.concatenate([f.layer_node_lo[:-1] + no[k] for k, f in enumerate(flats)] + [[no[-1]]])
+    t.layer_var = np.concatenate([f.layer_var + vo[k] for k, f in enumerate(flats)])
+    t.layer_bdd = np.concatenate([f.layer_bdd + bo[k] for k, f in enumerate(flats)])
+    t.zero_t = np.concatenate([np.where(f.zero_t >= 0, f.zero_t + no[k], f.zero_t) for k, f in enumerate(flats)])
+    t.one_t = np.concatenate([np.where(f.one_t >= 0, f.one_t + no[k], f.one_t) for k, f in enumerate(flats)])
+    # visitation positions appended instance after instance (a position's copies stay in ascending layer order)
+    t.proc_ptr = np.concatenate([f.proc_ptr[:-1] + lo[k] for k, f in enumerate(flats)] + [[lo[-1]]])
+    t.proc_layers = np.concatenate([f.proc_layers + lo[k] for k, f in enumerate(flats)])
+    t.max_width = max(int(f.max_width) for f in flats)
+    t.max_degree = max(int(f.max_degree) for f in flats)
+    t.max_layers = max(int(f.max_layers) for f in flats)
+    for name in _FIELDS:
+        setattr(t, name, np.ascontiguousarray(getattr(t, name), dtype=np.int64))
+    return IlpInstance(t.costs, flat=t), BatchIndex(vo, bo, lo, no)
+
+
+@dataclass
+class BatchResult:
+    merged: object  # qn.SolveResult of the merged instance
+    index: BatchIndex
+    bounds: list  # per instance: bound of its final duals (its diagrams' optima, numpy order, + free part)
+    iterations: int
+    seconds: float
+
+    def lam(self, k: int) -> np.ndarray:
+        """Final duals of instance k (host copy)."""
+        i = self.index
+        return self.merged.state.lam[i.layer[k]:i.layer[k + 1]]
+
+
+def instance_bounds(state, index: BatchIndex, instances) -> list:
+    """Per-instance bound of the merged state's current duals: each
+    instance's diagram optima summed in numpy's order (dual.py:66-69) plus
+    its unconstrained variables' part."""
+    F, B = state.node_tables(need_f=False)
+    del F
+    opt = torch.empty(state.flat.num_bdds, dtype=torch.float64, device=state.device)
+    # per-diagram optimum = B at its root (kernels.py:359-361 / 104-120)
+    roots = torch.as_tensor(state.flat.layer_node_lo[state.flat.bdd_layer_lo[:-1]], device=state.device)
+    opt.copy_(B[roots])
+    host = opt.cpu().numpy()
+    out = []
+    for k, inst in enumerate(instances):
+        free = inst.unconstrained_variables()
+        fc = float(np.minimum(inst.costs[free], 0.0).sum()) if len(free) else 0.0
+        out.append(float(np.sum(host[index.bdd[k]:index.bdd[k + 1]])) + fc)
+    return out
+
+
+def solve_merged(instances, cfg: SolveConfig | None = None, device=None, clock=time.perf_counter) -> BatchResult:
+    """Solve a batch of independent instances as one merged instance (from
+    their lowered host tables: merge, upload, plans and solve all timed)."""
+    from .dual import init_duals
+    from .qn import solve
+
+    instances = list(instances)
+    cfg = cfg or SolveConfig()
+    t0 = clock()
+    merged, index = merge_instances(instances)
+    state = init_duals(merged, device=device, schedule=cfg.mma_schedule)
+    res = solve(merged, cfg, device=device, state=state, clock=clock)
+    bounds = instance_bounds(res.state, index, instances)
+    return BatchResult(res, index, bounds, res.iterations, clock() - t0)
