@@ -12,6 +12,7 @@ from .config import MODE_HYBRID, MODE_MMA_ONLY, SolveConfig
 from .errors import (EmptyFeasibleSet, EmptyHistory, InfeasibleAfterFixing, NativeLibraryError,
                      ProdmatchError, SplitAtTerminalLayer, UnsupportedInstance)
 from .ilp import Bdd, IlpInstance, LinearRow, build_equality_bdd, make_row
+from . import bdd  # noqa: E402  (attaches the reference's per-diagram Bdd methods)
 
 __version__ = "0.1.0"
 

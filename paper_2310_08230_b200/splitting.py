@@ -8,13 +8,76 @@ entry points.
 from __future__ import annotations
 
 import ctypes
+from dataclasses import dataclass
+from typing import Iterator
 
 import numpy as np
 
 from . import _native
-from .ilp import FlatTable, IlpInstance
+from .errors import SplitAtTerminalLayer
+from .ilp import Bdd, FlatTable, IlpInstance
 
 DEFAULT_CHUNK_SIZE = 128
+_F, _T = -1, -2  # FALSE / TRUE terminals (bdd.py:24-25)
+
+
+@dataclass(frozen=True)
+class SplitResult:
+    """The two coupled halves of a cut diagram and the coupling variables
+    (splitting.py:28-32)."""
+
+    left: Bdd
+    right: Bdd
+    aux_ids: list
+
+
+def split_bdd(bdd: Bdd, split_after_layer: int, fresh_ids: Iterator[int]) -> SplitResult:
+    """Cut one diagram after its first ``split_after_layer`` layers into two
+    coupled by k fresh one-hot variables, k = width of the crossing layer
+    (splitting.py:35-96; the same construction the native lowering applies,
+    csrc/dm_host.cpp).  The left half reads the prefix and then y = e_t for
+    the crossing node t it reached; the right half decodes y and resumes the
+    suffix at node t.  Per-diagram API; instances are split natively by
+    split_instance."""
+    n = bdd.num_variables
+    cut = int(split_after_layer)
+    if not 1 <= cut < n:
+        raise SplitAtTerminalLayer(f"split index {cut} outside [1, {n - 1}]")
+    k = len(bdd.zeros[cut])
+    aux = [next(fresh_ids) for _ in range(k)]
+
+    def layer(width):
+        return np.full(width, _F, np.int32), np.full(width, _F, np.int32)
+
+    # left tail, layer q over y_q: slots 0..k-q-1 = crossing nodes q.. still
+    # waiting for their bit, slot k-q (q > 0) = "bit already placed"
+    lz, lo = [z.copy() for z in bdd.zeros[:cut]], [o.copy() for o in bdd.ones[:cut]]
+    for q in range(k):
+        waiting, final = k - q, q == k - 1
+        z, o = layer(waiting + (q > 0))
+        o[0] = _T if final else waiting - 1  # node q places its bit here -> "placed"
+        z[1:waiting] = np.arange(waiting - 1)  # the others wait one more layer
+        if q > 0:
+            z[waiting] = _T if final else waiting - 1  # "placed" passes zeros
+        lz.append(z)
+        lo.append(o)
+    # right head, layer q over y_q: slot 0 = nothing placed yet, slot t+1 =
+    # placed at t; the last layer hands over to crossing node t of the suffix
+    rz, ro = [], []
+    for q in range(k):
+        final = q == k - 1
+        z, o = layer(q + 1)
+        o[0] = q if final else q + 1
+        if not final:
+            z[0] = 0
+        z[1:] = np.arange(q) + (0 if final else 1)
+        rz.append(z)
+        ro.append(o)
+    rz += [z.copy() for z in bdd.zeros[cut:]]
+    ro += [o.copy() for o in bdd.ones[cut:]]
+    left = Bdd(list(bdd.variables[:cut]) + aux, lz, lo)
+    right = Bdd(aux + list(bdd.variables[cut:]), rz, ro)
+    return SplitResult(left, right, aux)
 
 
 def plan_chunks(instance: IlpInstance, chunk_size: int) -> list[tuple[int, list[int]]]:
