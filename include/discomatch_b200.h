@@ -246,6 +246,18 @@ int dm_dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot
 /* interleaved table -> FlatBdds node order */
 int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *stream);
 
+/* Perturbation rounding (rounding.py; the paper's primal heuristic, after
+ * FastDOG: PAPER.md:5031-5043), one round on fresh min-marginals m0 / m1:
+ * per variable (by id) the copies' votes give a direction dir (+1: the
+ * copies prefer 0, -1: prefer 1) — unanimous and strict vote, else the sign
+ * of the summed differences, else bit 10 of h = splitmix64(seed, round, v);
+ * its cost moves by dir * delta * (1 + u), u = (h >> 11) * 2^-53, split
+ * evenly over the copies' duals (lam[l] += that / copies).  values[v] =
+ * the voted value (dir > 0 -> 0), agrees[v] = 1 for a unanimous strict
+ * vote; *disagree (device int) = variables without one. */
+int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, uint64_t seed,
+                     int round, int8_t *values, int8_t *agrees, int *disagree, void *stream);
+
 /* --- vectors over dual coordinates / variables ----------------------------- */
 /* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream);

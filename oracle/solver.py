@@ -333,3 +333,63 @@ def agreement_scores(st: OracleDual):
     score = np.abs(np.nan_to_num(total, nan=0.0, posinf=np.inf, neginf=-np.inf))
     preferred = np.where(vmax > 0, 0, 1).astype(np.int8)
     return agrees, score, preferred
+
+
+# ---------------------------------------------------------------------------
+# Perturbation rounding (restates paper_2310_08230_b200/rounding.py and the
+# dm_perturb_round kernel, csrc/dm_device.cu: same votes, same splitmix64
+# hash, same roundings) — for the GPU-vs-oracle rounding test.
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def mix64(seed, rnd, v):
+    """splitmix64 of (seed, round, variable ids v) as uint64 numpy."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * (
+            (np.uint64(rnd & 0xFFFFFFFF) << np.uint64(32)) + np.asarray(v, np.uint64) + np.uint64(1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def perturb_round(st: OracleDual, delta, seed, rnd):
+    """One round on fresh min-marginals: returns (values, agrees, disagree
+    count) and moves st.lam (caches invalidated)."""
+    m0, m1 = st.min_marginals()
+    f = st.flat
+    nv = st.inst.num_variables
+    values = np.zeros(nv, np.int8)
+    agrees = np.zeros(nv, np.int8)
+    dis = 0
+    for p in range(len(f.proc_ptr) - 1):
+        lo, hi = int(f.proc_ptr[p]), int(f.proc_ptr[p + 1])
+        if hi == lo:
+            continue
+        ls = f.proc_layers[lo:hi]
+        vmax, vmin, total = -2.0, 2.0, 0.0
+        for l in ls:
+            a, b = m0[l], m1[l]
+            fa, fb = a != INF, b != INF
+            diff = (b - a) if (fa and fb) else (INF if fa else -INF)
+            vote = 1.0 if diff > 0.0 else (-1.0 if diff < 0.0 else 0.0)
+            vmax, vmin = max(vmax, vote), min(vmin, vote)
+            total = total + diff
+        v = int(f.layer_var[ls[0]])
+        agree = vmax == vmin and vmax != 0.0
+        h = int(mix64(seed, rnd, v))
+        if agree:
+            d = vmax
+        elif total > 0.0:
+            d = 1.0
+        elif total < 0.0:
+            d = -1.0
+        else:
+            d = 1.0 if (h >> 10) & 1 else -1.0
+        u = float(h >> 11) * 2.0 ** -53
+        share = ((d * delta) * (1.0 + u)) / float(hi - lo)
+        st.lam[ls] = st.lam[ls] + share
+        values[v] = 0 if d > 0.0 else 1
+        agrees[v] = agree
+        dis += not agree
+    st.f_valid = st.b_valid = False
+    return values, agrees, dis

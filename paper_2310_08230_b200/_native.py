@@ -82,6 +82,7 @@ SIGNATURES = {
     "dm_dfr_boundary_gather": ([_I, _P, _P, _P, _P, _P], _INT),
     "dm_dfr_boundary_average": ([_I, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
     "dm_dfr_to_nodes": ([_P, _P, _P, _P], _INT),
+    "dm_perturb_round": ([_P, _P, _P, _P, _D, ctypes.c_uint64, _INT, _P, _P, _P, _P], _INT),
     "dm_init_duals": ([_P, _P, _P, _P], _INT),
     "dm_project_direction": ([_P, _P, _P, _P], _INT),
     "dm_lambda_sums": ([_P, _P, _P, _P], _INT),
@@ -147,7 +148,8 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
                   "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search",
                   "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_average", "dm_dfr_flush", "dm_dfr_to_nodes",
-                  "dm_dfr_average_csr", "dm_dfr_boundary_gather", "dm_dfr_boundary_average"}
+                  "dm_dfr_average_csr", "dm_dfr_boundary_gather", "dm_dfr_boundary_average",
+                  "dm_perturb_round"}
 launch_count = 0
 
 

@@ -283,6 +283,60 @@ __global__ void agreement_kernel(int32_t P, const int32_t *__restrict__ proc_ptr
 }
 
 // --------------------------------------------------------------------------
+// Perturbation rounding (rounding.py; the paper's primal heuristic after
+// FastDOG): per variable, the copies' min-marginal
+// votes decide a push direction (unanimous vote, else the sign of their
+// sum, else a hashed coin), the cost moves by dir * delta * (1 + u) with u a
+// hashed uniform in [0, 1), spread evenly over the copies' duals so they
+// stay feasible for the perturbed costs.  values[v] = the voted value,
+// agrees[v] = unanimous and strict; *disagree counts the others.
+__device__ __forceinline__ uint64_t dm_mix64(uint64_t seed, int32_t round, int32_t v) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * ((((uint64_t)(uint32_t)round) << 32) + (uint64_t)(uint32_t)v + 1ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void perturb_kernel(int32_t P, const int32_t *__restrict__ proc_ptr, const int32_t *__restrict__ proc_layers,
+                               const int32_t *__restrict__ pos_var, const double *__restrict__ m0,
+                               const double *__restrict__ m1, double *__restrict__ lam, double delta, uint64_t seed,
+                               int32_t round, int8_t *__restrict__ values, int8_t *__restrict__ agrees,
+                               int *__restrict__ disagree) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P || pos_var[p] < 0) return;
+    const int32_t lo = proc_ptr[p], hi = proc_ptr[p + 1];
+    double vmax = -2.0, vmin = 2.0, total = 0.0;
+    for (int32_t t = lo; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        const double a = m0[l], b = m1[l];
+        const bool fa = a != DM_INF, fb = b != DM_INF;
+        const double diff = (fa && fb) ? __dsub_rn(b, a) : (fa ? DM_INF : -DM_INF);
+        const double vote = diff > 0.0 ? 1.0 : (diff < 0.0 ? -1.0 : 0.0);
+        vmax = fmax(vmax, vote);
+        vmin = fmin(vmin, vote);
+        total = __dadd_rn(total, diff);
+    }
+    const int32_t v = pos_var[p];
+    const bool agree = vmax == vmin && vmax != 0.0;
+    const uint64_t h = dm_mix64(seed, round, v);
+    double dir;
+    if (agree) dir = vmax;
+    else if (total > 0.0) dir = 1.0;
+    else if (total < 0.0) dir = -1.0;
+    else dir = ((h >> 10) & 1ull) ? 1.0 : -1.0;  // tie or inf - inf
+    const double u = (double)(h >> 11) * 0x1.0p-53;
+    const double d = __dmul_rn(__dmul_rn(dir, delta), __dadd_rn(1.0, u));
+    const double share = __ddiv_rn(d, (double)(hi - lo));
+    for (int32_t t = lo; t < hi; ++t) {
+        const int32_t l = proc_layers[t];
+        lam[l] = __dadd_rn(lam[l], share);
+    }
+    values[v] = dir > 0.0 ? 0 : 1;
+    agrees[v] = agree;
+    if (!agree) atomicAdd(disagree, 1);
+}
+
+// --------------------------------------------------------------------------
 // elementwise vectors (numpy rounding: one rounding per operation)
 // --------------------------------------------------------------------------
 __global__ void axpy_dev_kernel(double *__restrict__ x, const double *__restrict__ y, double alpha,
@@ -2421,6 +2475,21 @@ int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *strea
         return DM_ERR_INVALID;
     }
     return dm::dfr_to_nodes(f->sweep, x_il, x, stream);
+}
+
+int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, uint64_t seed,
+                     int round, int8_t *values, int8_t *agrees, int *disagree, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!m0 || !m1 || !lam || !values || !agrees || !disagree) {
+        dm::set_error("dm_perturb_round: null argument");
+        return DM_ERR_INVALID;
+    }
+    DM_CUDA(cudaMemsetAsync(disagree, 0, sizeof(int), (cudaStream_t)stream));
+    if (f->P == 0) return DM_OK;
+    perturb_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
+        (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, m0, m1, lam, delta, seed, round, values, agrees,
+        disagree);
+    return check_stream_error("perturb_round");
 }
 
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {
