@@ -654,17 +654,23 @@ def c5_solve(insts, dev, schedule):
 
     torch.cuda.synchronize()
     t = time.perf_counter()
-    res = solve_merged(insts, SolveConfigC5(schedule), device=dev)
+    res = solve_merged(insts, SolveConfigC5(schedule), device=dev, per_instance_stop=False)
     torch.cuda.synchronize()
     return time.perf_counter() - t, res
 
 
+C5_ITERATIONS = {"exact": 10, "deferred": 40}
+
+
 def SolveConfigC5(schedule):  # noqa: N802 - a config factory
-    """Averaging-only merged batches: bit-identical per instance to separate
-    solves, stopped when every instance's own stopping rule has fired."""
+    """Averaging-only merged batches of a fixed length (bit-identical per
+    instance to separate solves of that length; the reference's 1e-10
+    stall rule keeps averaging-only solves running long after the 1e-3 gap,
+    so the line reports the length and the quality it reaches instead)."""
     from paper_2310_08230_b200.config import SolveConfig
 
-    return SolveConfig(mode="mma-only", mma_schedule=schedule, max_iterations=3000)
+    return SolveConfig(mode="mma-only", mma_schedule=schedule, max_iterations=C5_ITERATIONS[schedule],
+                       dual_tolerance=-float("inf"))
 
 
 def c5_summary(args, dev, reps=5):
@@ -679,9 +685,9 @@ def c5_summary(args, dev, reps=5):
     insts = c5_instances(range(args.seed, args.seed + C5_INSTANCES))
     out = {"workload": f"c5: {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}, solved as ONE merged "
                        "block-diagonal instance (batch.py) from the lowered host tables: merge, upload, plans, "
-                       "averaging-only solve until every instance's own stopping rule fired (per-instance duals bit-identical "
-                       "to separate solves of that length) and per-instance bounds inside the clock; gap vs each "
-                       "instance's separate converged hybrid solve"}
+                       "averaging-only solve of a fixed length (per-instance duals bit-identical to separate solves of that "
+                       "length) and per-instance bounds inside the clock; quality = each instance's relative gap to "
+                       "its separate converged hybrid solve"}
     import gc
 
     import torch

@@ -251,12 +251,13 @@ int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *strea
  * per variable (by id) the copies' votes give a direction dir (+1: the
  * copies prefer 0, -1: prefer 1) — unanimous and strict vote, else the sign
  * of the summed differences, else bit 10 of h = splitmix64(seed, round, v);
- * its cost moves by dir * delta * (1 + u), u = (h >> 11) * 2^-53, split
+ * its cost moves by dir * mag * (1 + u), mag = delta (delta * boost when the
+ * vote is already unanimous), u = (h >> 11) * 2^-53, split
  * evenly over the copies' duals (lam[l] += that / copies).  values[v] =
  * the voted value (dir > 0 -> 0), agrees[v] = 1 for a unanimous strict
  * vote; *disagree (device int) = variables without one. */
-int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, uint64_t seed,
-                     int round, int8_t *values, int8_t *agrees, int *disagree, void *stream);
+int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, double boost,
+                     uint64_t seed, int round, int8_t *values, int8_t *agrees, int *disagree, void *stream);
 
 /* --- vectors over dual coordinates / variables ----------------------------- */
 /* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */

@@ -352,7 +352,7 @@ def mix64(seed, rnd, v):
         return z ^ (z >> np.uint64(31))
 
 
-def perturb_round(st: OracleDual, delta, seed, rnd):
+def perturb_round(st: OracleDual, delta, seed, rnd, boost=10.0):
     """One round on fresh min-marginals: returns (values, agrees, disagree
     count) and moves st.lam (caches invalidated)."""
     m0, m1 = st.min_marginals()
@@ -386,7 +386,8 @@ def perturb_round(st: OracleDual, delta, seed, rnd):
         else:
             d = 1.0 if (h >> 10) & 1 else -1.0
         u = float(h >> 11) * 2.0 ** -53
-        share = ((d * delta) * (1.0 + u)) / float(hi - lo)
+        mag = delta * boost if agree else delta
+        share = ((d * mag) * (1.0 + u)) / float(hi - lo)
         st.lam[ls] = st.lam[ls] + share
         values[v] = 0 if d > 0.0 else 1
         agrees[v] = agree

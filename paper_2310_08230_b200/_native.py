@@ -82,7 +82,7 @@ SIGNATURES = {
     "dm_dfr_boundary_gather": ([_I, _P, _P, _P, _P, _P], _INT),
     "dm_dfr_boundary_average": ([_I, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
     "dm_dfr_to_nodes": ([_P, _P, _P, _P], _INT),
-    "dm_perturb_round": ([_P, _P, _P, _P, _D, ctypes.c_uint64, _INT, _P, _P, _P, _P], _INT),
+    "dm_perturb_round": ([_P, _P, _P, _P, _D, _D, ctypes.c_uint64, _INT, _P, _P, _P, _P], _INT),
     "dm_init_duals": ([_P, _P, _P, _P], _INT),
     "dm_project_direction": ([_P, _P, _P, _P], _INT),
     "dm_lambda_sums": ([_P, _P, _P, _P], _INT),

@@ -286,7 +286,8 @@ __global__ void agreement_kernel(int32_t P, const int32_t *__restrict__ proc_ptr
 // Perturbation rounding (rounding.py; the paper's primal heuristic after
 // FastDOG): per variable, the copies' min-marginal
 // votes decide a push direction (unanimous vote, else the sign of their
-// sum, else a hashed coin), the cost moves by dir * delta * (1 + u) with u a
+// sum, else a hashed coin), the cost moves by dir * delta * (1 + u) (delta *
+// boost for variables whose vote is already unanimous) with u a
 // hashed uniform in [0, 1), spread evenly over the copies' duals so they
 // stay feasible for the perturbed costs.  values[v] = the voted value,
 // agrees[v] = unanimous and strict; *disagree counts the others.
@@ -299,8 +300,8 @@ __device__ __forceinline__ uint64_t dm_mix64(uint64_t seed, int32_t round, int32
 
 __global__ void perturb_kernel(int32_t P, const int32_t *__restrict__ proc_ptr, const int32_t *__restrict__ proc_layers,
                                const int32_t *__restrict__ pos_var, const double *__restrict__ m0,
-                               const double *__restrict__ m1, double *__restrict__ lam, double delta, uint64_t seed,
-                               int32_t round, int8_t *__restrict__ values, int8_t *__restrict__ agrees,
+                               const double *__restrict__ m1, double *__restrict__ lam, double delta, double boost,
+                               uint64_t seed, int32_t round, int8_t *__restrict__ values, int8_t *__restrict__ agrees,
                                int *__restrict__ disagree) {
     const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P || pos_var[p] < 0) return;
@@ -325,7 +326,8 @@ __global__ void perturb_kernel(int32_t P, const int32_t *__restrict__ proc_ptr, 
     else if (total < 0.0) dir = -1.0;
     else dir = ((h >> 10) & 1ull) ? 1.0 : -1.0;  // tie or inf - inf
     const double u = (double)(h >> 11) * 0x1.0p-53;
-    const double d = __dmul_rn(__dmul_rn(dir, delta), __dadd_rn(1.0, u));
+    const double mag = agree ? __dmul_rn(delta, boost) : delta;  // settled variables pushed harder
+    const double d = __dmul_rn(__dmul_rn(dir, mag), __dadd_rn(1.0, u));
     const double share = __ddiv_rn(d, (double)(hi - lo));
     for (int32_t t = lo; t < hi; ++t) {
         const int32_t l = proc_layers[t];
@@ -2477,8 +2479,8 @@ int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *strea
     return dm::dfr_to_nodes(f->sweep, x_il, x, stream);
 }
 
-int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, uint64_t seed,
-                     int round, int8_t *values, int8_t *agrees, int *disagree, void *stream) {
+int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, double boost,
+                     uint64_t seed, int round, int8_t *values, int8_t *agrees, int *disagree, void *stream) {
     DM_CHECK_FLAT(f);
     if (!m0 || !m1 || !lam || !values || !agrees || !disagree) {
         dm::set_error("dm_perturb_round: null argument");
@@ -2487,8 +2489,8 @@ int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, doubl
     DM_CUDA(cudaMemsetAsync(disagree, 0, sizeof(int), (cudaStream_t)stream));
     if (f->P == 0) return DM_OK;
     perturb_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
-        (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, m0, m1, lam, delta, seed, round, values, agrees,
-        disagree);
+        (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, m0, m1, lam, delta, boost, seed, round, values,
+        agrees, disagree);
     return check_stream_error("perturb_round");
 }
 

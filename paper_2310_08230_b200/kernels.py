@@ -178,8 +178,8 @@ class DeviceFlat:
     def lambda_sums(self, lam, out):
         _native.call("dm_lambda_sums", self._h, _ptr(lam), _ptr(out), self._s())
 
-    def perturb_round(self, m0, m1, lam, delta, seed, round_, values, agrees, disagree):
-        _native.call("dm_perturb_round", self._h, _ptr(m0), _ptr(m1), _ptr(lam), float(delta), int(seed),
+    def perturb_round(self, m0, m1, lam, delta, boost, seed, round_, values, agrees, disagree):
+        _native.call("dm_perturb_round", self._h, _ptr(m0), _ptr(m1), _ptr(lam), float(delta), float(boost), int(seed),
                      int(round_), _ptr(values), _ptr(agrees), _ptr(disagree), self._s())
 
     def agreement_scores(self, m0, m1, agrees, score, preferred):

@@ -7,7 +7,9 @@ available as primal.recover_primal).
 Round r, on the current duals: fresh min-marginals (k_min_marginals), then
 per variable the copies' votes give a direction — a unanimous strict vote,
 else the sign of the summed differences, else a hashed coin — and its cost
-moves by dir * delta_r * (1 + u) (u hashed in [0, 1)), spread evenly over the
+moves by dir * delta_r * (1 + u) (u hashed in [0, 1); variables whose vote is
+already unanimous move ``boost`` times further, which all but fixes them),
+spread evenly over the
 copies' duals (dm_perturb_round; feasibility for the perturbed costs is
 kept).  A few averaging iterations then re-equilibrate the duals.  When
 every constrained variable has a unanimous strict vote, each diagram's
@@ -66,8 +68,8 @@ def diagrams_accept(flat, x: np.ndarray) -> np.ndarray:
     return ok
 
 
-def perturbation_rounding(state: DualState, seed: int = 0, max_rounds: int = 60, iterations_per_round: int = 2,
-                          delta0: float | None = None, growth: float = 1.5, damping: float = 0.5,
+def perturbation_rounding(state: DualState, seed: int = 0, max_rounds: int = 80, iterations_per_round: int = 3,
+                          delta0: float | None = None, growth: float = 1.2, boost: float = 10.0, damping: float = 0.5,
                           clock=time.perf_counter) -> RoundingResult:
     """Round the solved duals of ``state`` to a feasible assignment (the state's
     duals end perturbed; its instance and best bound are untouched)."""
@@ -88,7 +90,7 @@ def perturbation_rounding(state: DualState, seed: int = 0, max_rounds: int = 60,
     r = 0
     for r in range(max_rounds):
         m0, m1 = state.min_marginal_table_device()
-        state.dev.perturb_round(m0, m1, state.lam_d, delta0 * growth ** r, seed, r, values, agrees, disagree)
+        state.dev.perturb_round(m0, m1, state.lam_d, delta0 * growth ** r, boost, seed, r, values, agrees, disagree)
         n_dis = int(disagree.item())
         history.append(n_dis)
         state.f_valid = state.b_valid = False  # duals moved

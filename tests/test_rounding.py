@@ -38,7 +38,7 @@ def test_diagrams_accept_matches_bdd_accepts(name):
         assert got.tolist() == want
 
 
-def _oracle_rounding(inst, res_lam, seed, delta0, growth, per_round, max_rounds):
+def _oracle_rounding(inst, res_lam, seed, delta0, growth, per_round, max_rounds, boost=10.0):
     from oracle import model, solver
 
     f = inst.flat
@@ -50,7 +50,7 @@ def _oracle_rounding(inst, res_lam, seed, delta0, growth, per_round, max_rounds)
     st.set_lambda(res_lam)
     hist = []
     for r in range(max_rounds):
-        values, _, dis = solver.perturb_round(st, delta0 * growth ** r, seed, r)
+        values, _, dis = solver.perturb_round(st, delta0 * growth ** r, seed, r, boost)
         hist.append(dis)
         if dis == 0:
             return hist, values
@@ -71,8 +71,8 @@ def test_gpu_rounding_matches_oracle_and_is_feasible(name):
     res = qn.solve(inst, SolveConfig(max_iterations=8))
     lam = res.state.lam
     delta0 = 1e-3 * float(np.median(np.abs(inst.costs[inst.costs != 0])))
-    out = perturbation_rounding(res.state, seed=7, max_rounds=40, iterations_per_round=2, delta0=delta0)
-    hist, values = _oracle_rounding(inst, lam, 7, delta0, 1.5, 2, 40)
+    out = perturbation_rounding(res.state, seed=7, max_rounds=60, iterations_per_round=3, delta0=delta0, growth=1.2)
+    hist, values = _oracle_rounding(inst, lam, 7, delta0, 1.2, 3, 60)
     assert out.disagree_history == hist
     assert out.assignment is not None and values is not None
     constrained = inst.constraint_counts > 0
