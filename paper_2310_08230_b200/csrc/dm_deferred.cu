@@ -80,6 +80,54 @@ __device__ __forceinline__ double dfr_update(double lam_l, double a_l, double m0
     return lam_l;
 }
 
+// Group metadata (width and first slot of every position) staged per warp
+// in shared memory, a window of kMetaWin positions at a time: the slot
+// addresses of the next positions then need no dependent global load, and
+// the passes can warm L2 with the rows kAhead positions ahead of the
+// register double buffer (a lane per 128-byte row: arcs, opposite table,
+// plus each lane's own dual entries).
+constexpr int kMetaWin = 128;
+constexpr int kAhead = 3;
+constexpr int kWarps = kThreads / 32;
+
+struct Meta {
+    int32_t *w;
+    int64_t *slot;
+    int32_t lo;  // first position held
+};
+
+__device__ __forceinline__ void meta_window(Meta &m, const dm::SweepDev &s, int64_t p0, int32_t K, int32_t lo,
+                                            int lane) {
+    __syncwarp();
+    for (int i = lane; i < kMetaWin; i += 32) {
+        const int32_t k = lo + i;
+        if (k < K) {
+            m.w[i] = s.pos_width[p0 + k];
+            m.slot[i] = s.pos_slot[p0 + k];
+        }
+    }
+    __syncwarp();
+    m.lo = lo;
+}
+
+__device__ __forceinline__ void l2_prefetch(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// warm L2 with position k's arc rows (lanes 0-7: zero arcs, 8-15: one arcs)
+// and, when tab != null, the table rows of position kt (lanes 16-31, two
+// lines per row)
+template <int W>
+__device__ __forceinline__ void warm_rows(const dm::SweepDev &s, int lane, int32_t w, int64_t slot, const double *tab,
+                                          int32_t wt, int64_t slot_t) {
+    if (lane < 8) {
+        if (lane < w) l2_prefetch(s.zl + (slot + lane) * 32);
+    } else if (lane < 16) {
+        if (lane - 8 < w) l2_prefetch(s.ol + (slot + lane - 8) * 32);
+    } else if (tab) {
+        const int q = lane - 16;  // row q / 2, half q % 2
+        if ((q >> 1) < wt) l2_prefetch(tab + (slot_t + (q >> 1)) * 32 + (q & 1) * 16);
+    }
+}
+
 // Backward direction: positions k = 0 (every lane's last layer) .. K-1.
 template <int W, bool kMM, bool kAvg, bool kDec>
 __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
@@ -111,9 +159,13 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
     double lam_n = 0.0, avg_n = 0.0;
     int32_t w_n = 0;
     int64_t slot_n = 0;
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    Meta meta{meta_w[threadIdx.x >> 5], meta_s[threadIdx.x >> 5], 0};
+    meta_window(meta, s, p0, K, 0, lane);
     auto fetch = [&](int32_t k) {
-        w_n = s.pos_width[p0 + k];
-        slot_n = s.pos_slot[p0 + k];
+        w_n = meta.w[k - meta.lo];
+        slot_n = meta.slot[k - meta.lo];
 #pragma unroll
         for (int i = 0; i < W; ++i)
             if (i < w_n) {
@@ -130,6 +182,20 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
     };
     if (K > 0) fetch(0);
     for (int32_t k = 0; k < K; ++k) {
+        // positions k .. k + 1 + kAhead must be in the metadata window (uniform in the warp)
+        if (k + 1 + kAhead >= meta.lo + kMetaWin && meta.lo + kMetaWin < K) meta_window(meta, s, p0, K, k, lane);
+        {
+            const int32_t kp = k + 1 + kAhead;
+            if (kp < K) {
+                const int32_t wp = meta.w[kp - meta.lo];
+                const int64_t sp = meta.slot[kp - meta.lo];
+                warm_rows<W>(s, lane, wp, sp, kMM ? inp : nullptr, wp, sp);
+                if (kp < nj) {
+                    l2_prefetch(lamp + (l0 + nj - 1 - kp));
+                    if (kAvg) l2_prefetch(avgp + (l0 + nj - 1 - kp));
+                }
+            }
+        }
         const int32_t w = w_n;
         const int64_t slot = slot_n;
         int32_t z[W], o[W];
@@ -221,9 +287,13 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     double lam_n = 0.0, avg_n = 0.0;
     int32_t w_n = 0, wb_n = 0;
     int64_t slot_n = 0;
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    Meta meta{meta_w[threadIdx.x >> 5], meta_s[threadIdx.x >> 5], 0};
+    meta_window(meta, s, p0, K, K > kMetaWin ? K - kMetaWin : 0, lane);
     auto fetch = [&](int32_t k) {  // k < nj
-        w_n = s.pos_width[p0 + k];
-        slot_n = s.pos_slot[p0 + k];
+        w_n = meta.w[k - meta.lo];
+        slot_n = meta.slot[k - meta.lo];
 #pragma unroll
         for (int i = 0; i < W; ++i)
             if (i < w_n) {
@@ -235,19 +305,40 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         lam_n = lamp[l];
         if (kAvg) avg_n = avgp[l];
         if (kMM) {
-            wb_n = k > 0 ? s.pos_width[p0 + k - 1] : 0;
-            const int64_t sb = k > 0 ? s.pos_slot[p0 + k - 1] : 0;
+            wb_n = k > 0 ? meta.w[k - 1 - meta.lo] : 0;
+            const int64_t sb = k > 0 ? meta.slot[k - 1 - meta.lo] : 0;
 #pragma unroll
             for (int u = 0; u < W; ++u)
                 if (u < wb_n) ba[u] = inp[(sb + u) * 32 + lane];
         }
     };
+    // positions k - 2 - kAhead .. k must be in the window (uniform in the warp)
+    auto window_for = [&](int32_t k) {
+        if (k - 2 - kAhead < meta.lo && meta.lo > 0) {
+            const int32_t lo = k + 1 > kMetaWin ? k + 1 - kMetaWin : 0;
+            meta_window(meta, s, p0, K, lo, lane);
+        }
+    };
+    if (K > 0) window_for(K - 1);
     if (nj > 0) fetch(nj - 1);
     for (int32_t k = K - 1; k >= 0; --k) {
+        window_for(k);
+        {
+            const int32_t kp = k - 1 - kAhead;  // warm L2 for position kp (and the table rows of kp - 1)
+            if (kp >= 0 && kp < nj) {
+                const int32_t wp = meta.w[kp - meta.lo];
+                const int64_t sp = meta.slot[kp - meta.lo];
+                const int32_t wt = kp > 0 ? meta.w[kp - 1 - meta.lo] : 0;
+                const int64_t st = kp > 0 ? meta.slot[kp - 1 - meta.lo] : 0;
+                warm_rows<W>(s, lane, wp, sp, kMM ? inp : nullptr, wt, st);
+                l2_prefetch(lamp + (l0 + nj - 1 - kp));
+                if (kAvg) l2_prefetch(avgp + (l0 + nj - 1 - kp));
+            }
+        }
         if (k >= nj) continue;
         const int32_t w = w_n;
         const int64_t slot = slot_n;
-        const int32_t wn = k > 0 ? s.pos_width[p0 + k - 1] : 0;
+        const int32_t wn = k > 0 ? meta.w[k - 1 - meta.lo] : 0;
         int32_t z[W], o[W];
 #pragma unroll
         for (int i = 0; i < W; ++i) {
