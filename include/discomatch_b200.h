@@ -125,6 +125,11 @@ typedef struct {
 } dm_flat_info;
 
 int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out);
+/* flags: DM_FLAT_NO_EXACT_PLANS skips the exact passes' level schedules and
+ * copy records (the deferred schedule, sweeps and vector kernels do not use
+ * them; dm_k_mma_* then return DM_ERR_INVALID). */
+#define DM_FLAT_NO_EXACT_PLANS 1
+int dm_flat_create_ex(const dm_flat_desc *desc, int device, void *stream, int flags, dm_flat **out);
 int dm_flat_get_info(const dm_flat *flat, dm_flat_info *info);
 /* Synchronises the stream and reports whether an exact pass since the last
  * call was aborted by its watchdog (DM_ERR_CUDA) — resets the word. */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "dm_instance_export": ([_P] + [_P] * 11, _INT),
     "dm_instance_free": ([_P], None),
     "dm_flat_create": ([ctypes.POINTER(FlatDesc), _INT, _P, ctypes.POINTER(_P)], _INT),
+    "dm_flat_create_ex": ([ctypes.POINTER(FlatDesc), _INT, _P, _INT, ctypes.POINTER(_P)], _INT),
     "dm_flat_get_info": ([_P, ctypes.POINTER(FlatInfo)], _INT),
     "dm_flat_status": ([_P, _P], _INT),
     "dm_flat_set_mma_config": ([_P, _INT, _INT, _INT, _INT, _INT], _INT),

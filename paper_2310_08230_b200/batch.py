@@ -47,8 +47,12 @@ class BatchIndex:
         return len(self.var) - 1
 
 
-def merge_instances(instances) -> tuple[IlpInstance, BatchIndex]:
-    """Block-diagonal concatenation of lowered instances (their FlatTables)."""
+def merge_instances(instances, threads: int = 8) -> tuple[IlpInstance, BatchIndex]:
+    """Block-diagonal concatenation of lowered instances (their FlatTables):
+    outputs preallocated, each instance's slices filled by a worker thread
+    (numpy releases the GIL on these copies)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     flats = [i.flat for i in instances]
     if not flats:
         raise ValueError("empty batch")
@@ -57,24 +61,53 @@ def merge_instances(instances) -> tuple[IlpInstance, BatchIndex]:
     bo = off([f.num_bdds for f in flats])
     lo = off([f.num_layers for f in flats])
     no = off([f.num_nodes for f in flats])
+    V, nb, L, N = int(vo[-1]), int(bo[-1]), int(lo[-1]), int(no[-1])
     t = FlatTable()
-    t.costs = np.concatenate([i.costs for i in instances])
-    t.variable_order = np.concatenate([i.variable_order + vo[k] for k, i in enumerate(instances)])
-    t.constraint_counts = np.concatenate([f.constraint_counts for f in flats])
-    t.bdd_layer_lo = np.concatenate([f.bdd_layer_lo[:-1] + lo[k] for k, f in enumerate(flats)] + [[lo[-1]]])
-    t.layer_node_lo = np.concatenate([f.layer_node_lo[:-1] + no[k] for k, f in enumerate(flats)] + [[no[-1]]])
-    t.layer_var = np.concatenate([f.layer_var + vo[k] for k, f in enumerate(flats)])
-    t.layer_bdd = np.concatenate([f.layer_bdd + bo[k] for k, f in enumerate(flats)])
-    t.zero_t = np.concatenate([np.where(f.zero_t >= 0, f.zero_t + no[k], f.zero_t) for k, f in enumerate(flats)])
-    t.one_t = np.concatenate([np.where(f.one_t >= 0, f.one_t + no[k], f.one_t) for k, f in enumerate(flats)])
-    # visitation positions appended instance after instance (a position's copies stay in ascending layer order)
-    t.proc_ptr = np.concatenate([f.proc_ptr[:-1] + lo[k] for k, f in enumerate(flats)] + [[lo[-1]]])
-    t.proc_layers = np.concatenate([f.proc_layers + lo[k] for k, f in enumerate(flats)])
+    t.costs = np.empty(V)
+    t.variable_order = np.empty(V, np.int64)
+    t.constraint_counts = np.empty(V, np.int64)
+    t.bdd_layer_lo = np.empty(nb + 1, np.int64)
+    t.layer_node_lo = np.empty(L + 1, np.int64)
+    t.layer_var = np.empty(L, np.int64)
+    t.layer_bdd = np.empty(L, np.int64)
+    t.zero_t = np.empty(N, np.int64)
+    t.one_t = np.empty(N, np.int64)
+    t.proc_ptr = np.empty(V + 1, np.int64)
+    t.proc_layers = np.empty(L, np.int64)
+    t.bdd_layer_lo[nb] = L
+    t.layer_node_lo[L] = N
+    t.proc_ptr[V] = L
+
+    def shifted(dst, src, by, nodes=False):
+        np.copyto(dst, src)
+        if by:
+            if nodes:  # node targets move, the terminal sentinels (-1, -2) stay
+                np.add(dst, by, out=dst, where=src >= 0)
+            else:
+                dst += by
+
+    def fill(k):
+        i, f = instances[k], flats[k]
+        v0, v1, b0, b1 = vo[k], vo[k + 1], bo[k], bo[k + 1]
+        l0, l1, n0, n1 = lo[k], lo[k + 1], no[k], no[k + 1]
+        t.costs[v0:v1] = i.costs
+        shifted(t.variable_order[v0:v1], i.variable_order, v0)
+        t.constraint_counts[v0:v1] = f.constraint_counts
+        shifted(t.bdd_layer_lo[b0:b1], f.bdd_layer_lo[:-1], l0)
+        shifted(t.layer_node_lo[l0:l1], f.layer_node_lo[:-1], n0)
+        shifted(t.layer_var[l0:l1], f.layer_var, v0)
+        shifted(t.layer_bdd[l0:l1], f.layer_bdd, b0)
+        shifted(t.zero_t[n0:n1], f.zero_t, n0, nodes=True)
+        shifted(t.one_t[n0:n1], f.one_t, n0, nodes=True)
+        # visitation positions appended instance after instance (copies stay in ascending layer order)
+        shifted(t.proc_ptr[v0:v1], f.proc_ptr[:-1], l0)
+        shifted(t.proc_layers[l0:l1], f.proc_layers, l0)
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(fill, range(len(instances))))
     t.max_width = max(int(f.max_width) for f in flats)
     t.max_degree = max(int(f.max_degree) for f in flats)
     t.max_layers = max(int(f.max_layers) for f in flats)
-    for name in _FIELDS:
-        setattr(t, name, np.ascontiguousarray(getattr(t, name), dtype=np.int64))
     return IlpInstance(t.costs, flat=t), BatchIndex(vo, bo, lo, no)
 
 

@@ -88,6 +88,10 @@ __device__ __forceinline__ double dfr_update(double lam_l, double a_l, double m0
 // plus each lane's own dual entries).
 constexpr int kMetaWin = 128;
 constexpr int kAhead = 3;
+#ifndef DM_DFR_WARM
+#define DM_DFR_WARM 0
+#endif
+constexpr bool kWarm = DM_DFR_WARM != 0;  // L2 warm-up of later positions (A/B: slower in the MM passes)
 constexpr int kWarps = kThreads / 32;
 
 struct Meta {
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
         if (k + 1 + kAhead >= meta.lo + kMetaWin && meta.lo + kMetaWin < K) meta_window(meta, s, p0, K, k, lane);
         {
             const int32_t kp = k + 1 + kAhead;
-            if (kp < K) {
+            if (kWarm && kp < K) {
                 const int32_t wp = meta.w[kp - meta.lo];
                 const int64_t sp = meta.slot[kp - meta.lo];
                 warm_rows<W>(s, lane, wp, sp, kMM ? inp : nullptr, wp, sp);
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         window_for(k);
         {
             const int32_t kp = k - 1 - kAhead;  // warm L2 for position kp (and the table rows of kp - 1)
-            if (kp >= 0 && kp < nj) {
+            if (kWarm && kp >= 0 && kp < nj) {
                 const int32_t wp = meta.w[kp - meta.lo];
                 const int64_t sp = meta.slot[kp - meta.lo];
                 const int32_t wt = kp > 0 ? meta.w[kp - 1 - meta.lo] : 0;

@@ -1400,6 +1400,7 @@ struct dm_flat {
     bool classic_uploaded = false;
     int mma_grid_fw = 0, mma_grid_bw = 0;
     int64_t bytes = 0;
+    bool exact_plans = true;  // false: created with DM_FLAT_NO_EXACT_PLANS (no exact averaging passes)
     dm::SweepDev sweep;  // interleaved layout for the full-table sweeps
     std::vector<void *> allocs;
 };
@@ -1727,6 +1728,11 @@ const char *dm_version(void) {
 }
 
 int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out) {
+    return dm_flat_create_ex(desc, device, stream, 0, out);
+}
+
+int dm_flat_create_ex(const dm_flat_desc *desc, int device, void *stream, int flags, dm_flat **out) {
+    const bool exact_plans = !(flags & DM_FLAT_NO_EXACT_PLANS);
     if (!desc || !out) {
         dm::set_error("invalid arguments");
         return DM_ERR_INVALID;
@@ -1966,11 +1972,12 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         for (auto &e : walk_ev) cudaEventCreate(&e);
         cudaEventRecord(walk_ev[0], ps.s);
     }
-    if (dm::device_level_orders(f->proc_ptr, f->proc_layers, f->layer_bdd, f->bdd_layer_lo, P, L, nvalid, f->fw_pos,
-                                f->fw_lev, f->bw_pos, f->bw_lev, plan_words, ps.s))
+    if (exact_plans && dm::device_level_orders(f->proc_ptr, f->proc_layers, f->layer_bdd, f->bdd_layer_lo, P, L,
+                                               nvalid, f->fw_pos, f->fw_lev, f->bw_pos, f->bw_lev, plan_words, ps.s))
         return DM_ERR_CUDA;
+    if (!exact_plans) DM_CUDA(cudaMemsetAsync(plan_words, 0, 8 * sizeof(int), ps.s));
     if (vb2) cudaEventRecord(walk_ev[1], ps.s);
-    if (want_np && (dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, f->fw_pos, nvalid,
+    if (exact_plans && want_np && (dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, f->fw_pos, nvalid,
                                           f->np_rec_fw, ps.s) ||
                     dm::device_np_records(f->proc_ptr, f->proc_layers, f->lnl, f->layer_flags, f->bw_pos, nvalid,
                                           f->np_rec_bw, ps.s)))
@@ -2063,9 +2070,10 @@ int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat *
         dm::set_error("device schedule: level walk stalled (watchdog)");
         return DM_ERR_CUDA;
     }
-    f->fw_depth = nvalid ? words[4] + 1 : 0;
-    f->bw_depth = nvalid ? words[5] + 1 : 0;
-    if (!f->mma_np && (rc = ensure_per_copy_schedules(f.get(), s))) return rc;
+    f->fw_depth = nvalid && exact_plans ? words[4] + 1 : 0;
+    f->bw_depth = nvalid && exact_plans ? words[5] + 1 : 0;
+    f->exact_plans = exact_plans;
+    if (exact_plans && !f->mma_np && (rc = ensure_per_copy_schedules(f.get(), s))) return rc;
     if (env_int("DM_VERBOSE", 0))
         std::fprintf(stderr,
                      "[dm_flat_create] validate %.3fs, topology staging + device plans %.3fs, plan tail %.3fs "
@@ -2277,6 +2285,10 @@ int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds,
 static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, double *B, double *bounds,
                     cudaStream_t s) {
     if (f->nb == 0) return DM_OK;
+    if (!f->exact_plans) {
+        dm::set_error("exact averaging pass on a flat created without its plans (DM_FLAT_NO_EXACT_PLANS)");
+        return DM_ERR_INVALID;
+    }
     double sent;
     std::memcpy(&sent, &kSentinel, sizeof(sent));
     if (forward) {

@@ -81,7 +81,7 @@ class DualState:
         self.schedule = schedule
         self.instance = instance
         self.flat = flat if flat is not None else FlatBdds(instance)
-        self.dev: DeviceFlat = self.flat.device(device)
+        self.dev: DeviceFlat = self.flat.device(device, exact_plans=schedule == SCHEDULE_EXACT)
         d = self.dev.device
         self.device = d
         f = self.flat

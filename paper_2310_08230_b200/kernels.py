@@ -41,7 +41,7 @@ def _stream(device: torch.device) -> int:
 class DeviceFlat:
     """dm_flat handle: topology + schedules resident in HBM."""
 
-    def __init__(self, table: FlatTable, device: torch.device):
+    def __init__(self, table: FlatTable, device: torch.device, exact_plans: bool = True):
         if not torch.cuda.is_available():
             raise NativeLibraryError("a CUDA device is required (there is no CPU path)")
         self.device = torch.device(device)
@@ -59,9 +59,10 @@ class DeviceFlat:
             setattr(desc, name, a.ctypes.data)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            _native.check(lib.dm_flat_create(ctypes.byref(desc), self.device.index or 0,
-                                             _stream(self.device), ctypes.byref(h)), "dm_flat_create")
+            _native.check(lib.dm_flat_create_ex(ctypes.byref(desc), self.device.index or 0, _stream(self.device),
+                                                0 if exact_plans else 1, ctypes.byref(h)), "dm_flat_create")
         self._h = h
+        self.exact_plans = exact_plans
         info = _native.FlatInfo()
         _native.check(lib.dm_flat_get_info(h, ctypes.byref(info)), "dm_flat_get_info")
         self.info = {k: getattr(info, k) for k, _ in _native.FlatInfo._fields_}
@@ -267,11 +268,14 @@ class FlatBdds:
         self.constraint_counts = table.constraint_counts
         self._dev: dict = {}
 
-    def device(self, device=None) -> DeviceFlat:
+    def device(self, device=None, exact_plans: bool = True) -> DeviceFlat:
+        """The device copy (cached per device); ``exact_plans=False`` skips the
+        exact passes' schedules (a deferred-schedule state never uses them)."""
         dev = torch.device(device if device is not None else "cuda")
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         key = str(dev)
-        if key not in self._dev:
-            self._dev[key] = DeviceFlat(self.table, dev)
+        have = self._dev.get(key)
+        if have is None or (exact_plans and not have.exact_plans):
+            self._dev[key] = DeviceFlat(self.table, dev, exact_plans)
         return self._dev[key]

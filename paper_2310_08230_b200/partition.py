@@ -280,7 +280,7 @@ class DeviceEngine:
 
         self.part = part
         self.device = torch.device(device)
-        self.dev = DeviceFlat(part.table, self.device)
+        self.dev = DeviceFlat(part.table, self.device, exact_plans=False)
         t = part.table
         n = self.dev.dfr_table_size()
         z = lambda m: torch.zeros(m, dtype=_F64, device=self.device)  # noqa: E731
