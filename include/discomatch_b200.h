@@ -194,7 +194,9 @@ int dm_k_argmin(const dm_flat *f, const double *lam, const double *B, double *bi
  * backward pass recorded when it ran the node-parallel kernels — valid only
  * while lam and B are exactly what that pass left (the caller tracks this;
  * DualState does via its distance-table generation).  B must be the table that
- * pass wrote; DM_ERR_INVALID otherwise.  Bit-identical to dm_k_argmin there. */
+ * pass wrote; DM_ERR_INVALID otherwise (also after dm_init_duals,
+ * dm_k_mma_forward or a sweep rewrote that table; duals moved by the
+ * flat-less vector kernels, e.g. dm_axpy_host, are the caller's to track).  Bit-identical to dm_k_argmin there. */
 int dm_k_argmin_from_pass(const dm_flat *flat, const double *B, double *bits, void *stream);
 
 /* --- deferred (throughput) averaging schedule ------------------------------

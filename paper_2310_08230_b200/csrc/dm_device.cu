@@ -2222,6 +2222,7 @@ int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds
         dm::set_error("k_backward needs B");
         return DM_ERR_INVALID;
     }
+    if (f->dec_B == B) const_cast<dm_flat *>(f)->dec_B = nullptr;  // recorded decisions no longer match B
     return dm::sweep_backward(f->sweep, lam, nullptr, 0.0, B, bounds, stream);
 }
 
@@ -2278,6 +2279,7 @@ int dm_step_search(const dm_flat *f, const double *lam, const double *d, double 
 
 int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
+    if (f->dec_B == F) const_cast<dm_flat *>(f)->dec_B = nullptr;
     if (f->nb == 0) return DM_OK;
     return dm::sweep_forward(f->sweep, lam, F, bounds, stream);
 }
@@ -2353,6 +2355,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
 
 int dm_k_mma_forward(const dm_flat *f, double *lam, double *F, const double *B, double *bounds, void *stream) {
     DM_CHECK_FLAT(f);
+    const_cast<dm_flat *>(f)->dec_B = nullptr;  // the duals move: recorded decisions are stale
     return mma_pass(f, true, lam, F, const_cast<double *>(B), bounds, (cudaStream_t)stream);
 }
 
@@ -2449,6 +2452,7 @@ int dm_dfr_flush(const dm_flat *f, const double *mbar, double *lam, void *stream
         dm::set_error("dm_dfr_flush: null vector");
         return DM_ERR_INVALID;
     }
+    const_cast<dm_flat *>(f)->dec_B = nullptr;  // the duals move
     return dm::dfr_average(f->P, f->proc_ptr, f->proc_layers, mbar, lam, true, stream);
 }
 
@@ -2499,6 +2503,7 @@ int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, doubl
         return DM_ERR_INVALID;
     }
     DM_CUDA(cudaMemsetAsync(disagree, 0, sizeof(int), (cudaStream_t)stream));
+    const_cast<dm_flat *>(f)->dec_B = nullptr;  // the duals move
     if (f->P == 0) return DM_OK;
     perturb_kernel<<<blocks_for(f->P, 256), 256, 0, (cudaStream_t)stream>>>(
         (int32_t)f->P, f->proc_ptr, f->proc_layers, f->pos_var, m0, m1, lam, delta, boost, seed, round, values,
@@ -2508,6 +2513,7 @@ int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, doubl
 
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {
     DM_CHECK_FLAT(f);
+    const_cast<dm_flat *>(f)->dec_B = nullptr;  // new duals: recorded decisions are stale
     if (f->L == 0) return DM_OK;
     init_duals_kernel<<<blocks_for(f->L, 256), 256, 0, (cudaStream_t)stream>>>(
         (int32_t)f->L, f->layer_var, f->var_count, costs_by_var, lam);
