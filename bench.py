@@ -82,19 +82,22 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def build_instance(config: str, seed: int):
+def build_instance(config: str, seed: int, chunk: int = 128):
+    """The config's product space lowered with ``chunk``-layer splitting (the
+    reference's default 128; 0 = unsplit)."""
     from paper_2310_08230_b200 import product_space as ps
     from paper_2310_08230_b200.ilp import IlpInstance
 
     t = time.perf_counter()
     p = ps.synthetic_product_space(config, seed)
     t1 = time.perf_counter()
-    inst = IlpInstance.from_csr(p.costs, p.row_ptr, p.row_var, p.row_coef, p.row_rhs, 128)
+    inst = IlpInstance.from_csr(p.costs, p.row_ptr, p.row_var, p.row_coef, p.row_rhs, chunk)
     t2 = time.perf_counter()
     log(f"[bench] {config} seed {seed}: product space {t1 - t:.1f}s, lowering {t2 - t1:.1f}s, "
         f"{inst.num_variables} vars, {inst.flat.num_bdds} bdds, {inst.flat.num_layers} layers, "
         f"{inst.flat.num_nodes} nodes")
     inst._rows_hash = rows_hash(p)
+    inst._chunk = chunk
     return inst
 
 
@@ -110,7 +113,7 @@ def rows_hash(p) -> str:
     return m.hexdigest()[:32]
 
 
-def oracle_instance(config: str, seed: int):
+def oracle_instance(config: str, seed: int, chunk: int = 128):
     """The CPU arm's instance, lowered by the ORACLE's restatement of the
     reference pipeline (rows -> equality diagrams -> 128-chunk split -> flat
     table, oracle/model.py), so the reference arm never maps the product
@@ -121,7 +124,9 @@ def oracle_instance(config: str, seed: int):
 
     t = time.perf_counter()
     p = ps.synthetic_product_space(config, seed)
-    oi = model.split_instance(model.instance_from_rows(p.costs, p.rows()), 128)
+    oi = model.instance_from_rows(p.costs, p.rows())
+    if chunk:
+        oi = model.split_instance(oi, chunk)
     of = model.flatten(oi)
     log(f"[bench] oracle lowering of {config} seed {seed}: {time.perf_counter() - t:.1f}s, {of.num_nodes} nodes")
     return oi, of, rows_hash(p)
@@ -224,16 +229,17 @@ def cpu_reference_run(oi, of, warmup: int, steps: int, d_star=None, gap=1e-3, bu
 DSTAR_PATH = os.path.join(ROOT, "profiles", "dstar.json")
 
 
-def d_star_for(config: str, seed: int, rhash: str):
+def d_star_for(config: str, seed: int, rhash: str, chunk: int = 128):
     """Best known dual bound of the instance (profiles/dstar.json: long runs of
     both schedules on a B200, plus a certified primal where one exists), or
-    None when the file has no entry for this exact instance (rows hash)."""
+    None when the file has no entry for this exact instance (rows hash,
+    split length)."""
     try:
         with open(DSTAR_PATH) as fh:
             table = json.load(fh)
     except (OSError, ValueError):
         return None
-    e = table.get(f"{config}:{seed}")
+    e = table.get(f"{config}:{seed}" + ("" if chunk == 128 else f":chunk{chunk}"))
     if not e or e.get("rows_hash") != rhash:
         return None
     return e
@@ -529,6 +535,12 @@ def run_b200(args, rank, world, local_rank):
             result["c4"] = {"workload": workload("c4"), "nodes": c4.flat.num_nodes,
                             "time_to_gap": time_to_gap_both(c4, dev, "c4", args.seed)}
             del c4
+            # the same C2 ILP lowered WITHOUT splitting (chunk_size 0): splitting is the
+            # reference's default, but its chained pieces slow both schedules down here
+            un = build_instance(args.config, args.seed, chunk=0)
+            result["time_to_gap_unsplit"] = dict(time_to_gap_both(un, dev, args.config, args.seed),
+                                                 nodes=un.flat.num_nodes, max_layers=int(un.flat.max_layers))
+            del un
     if args.config == "c2" and not args.no_extras and not args.no_c5:
         result["c5"] = c5_summary(args, dev)
     if not args.no_e2e:
@@ -551,7 +563,7 @@ def time_to_gap_both(inst, dev, config, seed):
     """Measured time to a 1e-3 relative gap for both schedules, against the
     best known dual bound d* (profiles/dstar.json) or, without an entry for
     this instance, the best bound either solve reached."""
-    e = d_star_for(config, seed, getattr(inst, "_rows_hash", ""))
+    e = d_star_for(config, seed, getattr(inst, "_rows_hash", ""), getattr(inst, "_chunk", 128))
     d_star = e["d_star"] if e else None
     out = {}
     runs = {}
@@ -654,7 +666,7 @@ def c5_solve(insts, dev, schedule):
 
     torch.cuda.synchronize()
     t = time.perf_counter()
-    res = solve_merged(insts, SolveConfigC5(schedule), device=dev, per_instance_stop=False)
+    res = solve_merged(insts, SolveConfigC5(schedule), device=dev, per_instance_stop=False, reuse_buffers=True)
     torch.cuda.synchronize()
     return time.perf_counter() - t, res
 
@@ -830,6 +842,12 @@ def run_reference(args, rank):
             c4 = cpu_reference_run(oi4, of4, 0, 1, d_star=e4["d_star"], budget_s=args.cpu_budget)
             line["c4"] = {"workload": workload("c4"), "ms_per_iteration": c4["ms_per_iteration"],
                           "time_to_gap": dict(c4["time_to_gap"], d_star_source=e4["source"])}
+        oiu, ofu, rhu = oracle_instance(config, args.seed, chunk=0)
+        eu = d_star_for(config, args.seed, rhu, chunk=0)
+        if eu:
+            cu = cpu_reference_run(oiu, ofu, 0, 1, d_star=eu["d_star"], budget_s=args.cpu_budget)
+            line["time_to_gap_unsplit"] = dict(cu["time_to_gap"], d_star_source=eu["source"],
+                                               ms_per_iteration=cu["ms_per_iteration"])
     from paper_2310_08230_b200 import _native
 
     line["native_so_loaded"] = _native._lib is not None

@@ -47,10 +47,16 @@ class BatchIndex:
         return len(self.var) - 1
 
 
-def merge_instances(instances, threads: int = 8) -> tuple[IlpInstance, BatchIndex]:
+_REUSE: dict = {}  # (V, nb, L, N) -> the FlatTable last merged with reuse_buffers
+
+
+def merge_instances(instances, threads: int = 8, reuse_buffers: bool = False) -> tuple[IlpInstance, BatchIndex]:
     """Block-diagonal concatenation of lowered instances (their FlatTables):
     outputs preallocated, each instance's slices filled by a worker thread
-    (numpy releases the GIL on these copies)."""
+    (numpy releases the GIL on these copies).  ``reuse_buffers`` refills the
+    host arrays of the previous merge of the same sizes instead of faulting
+    in gigabytes of fresh pages (the previous merged instance is then
+    overwritten: a serving loop's staging arena)."""
     from concurrent.futures import ThreadPoolExecutor
 
     flats = [i.flat for i in instances]
@@ -62,18 +68,13 @@ def merge_instances(instances, threads: int = 8) -> tuple[IlpInstance, BatchInde
     lo = off([f.num_layers for f in flats])
     no = off([f.num_nodes for f in flats])
     V, nb, L, N = int(vo[-1]), int(bo[-1]), int(lo[-1]), int(no[-1])
-    t = FlatTable()
-    t.costs = np.empty(V)
-    t.variable_order = np.empty(V, np.int64)
-    t.constraint_counts = np.empty(V, np.int64)
-    t.bdd_layer_lo = np.empty(nb + 1, np.int64)
-    t.layer_node_lo = np.empty(L + 1, np.int64)
-    t.layer_var = np.empty(L, np.int64)
-    t.layer_bdd = np.empty(L, np.int64)
-    t.zero_t = np.empty(N, np.int64)
-    t.one_t = np.empty(N, np.int64)
-    t.proc_ptr = np.empty(V + 1, np.int64)
-    t.proc_layers = np.empty(L, np.int64)
+    if reuse_buffers and (V, nb, L, N) in _REUSE:
+        t = _REUSE[(V, nb, L, N)]
+    else:
+        t = _new_table(V, nb, L, N)
+        if reuse_buffers:
+            _REUSE.clear()
+            _REUSE[(V, nb, L, N)] = t
     t.bdd_layer_lo[nb] = L
     t.layer_node_lo[L] = N
     t.proc_ptr[V] = L
@@ -111,6 +112,22 @@ def merge_instances(instances, threads: int = 8) -> tuple[IlpInstance, BatchInde
     return IlpInstance(t.costs, flat=t), BatchIndex(vo, bo, lo, no)
 
 
+def _new_table(V, nb, L, N) -> FlatTable:
+    t = FlatTable()
+    t.costs = np.empty(V)
+    t.variable_order = np.empty(V, np.int64)
+    t.constraint_counts = np.empty(V, np.int64)
+    t.bdd_layer_lo = np.empty(nb + 1, np.int64)
+    t.layer_node_lo = np.empty(L + 1, np.int64)
+    t.layer_var = np.empty(L, np.int64)
+    t.layer_bdd = np.empty(L, np.int64)
+    t.zero_t = np.empty(N, np.int64)
+    t.one_t = np.empty(N, np.int64)
+    t.proc_ptr = np.empty(V + 1, np.int64)
+    t.proc_layers = np.empty(L, np.int64)
+    return t
+
+
 @dataclass
 class BatchResult:
     merged: object  # qn.SolveResult of the merged instance
@@ -145,7 +162,7 @@ def instance_bounds(state, index: BatchIndex, instances) -> list:
 
 
 def solve_merged(instances, cfg: SolveConfig | None = None, device=None, clock=time.perf_counter,
-                 per_instance_stop: bool = True) -> BatchResult:
+                 per_instance_stop: bool = True, reuse_buffers: bool = False) -> BatchResult:
     """Solve a batch of independent instances as one merged instance (from
     their lowered host tables: merge, upload, plans and solve all timed).
 
@@ -162,7 +179,7 @@ def solve_merged(instances, cfg: SolveConfig | None = None, device=None, clock=t
     instances = list(instances)
     cfg = cfg or SolveConfig()
     t0 = clock()
-    merged, index = merge_instances(instances)
+    merged, index = merge_instances(instances, reuse_buffers=reuse_buffers)
     state = init_duals(merged, device=device, schedule=cfg.mma_schedule)
     if not per_instance_stop or cfg.mode != "mma-only":
         from .qn import solve

@@ -35,6 +35,7 @@
 // (consecutive layers of one diagram, so a lane walks its own cache lines).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "dm_internal.h"
@@ -412,6 +413,290 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     if (j >= 0) boundsp[j] = tb;
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined passes (W = 8, the product-space instances): every position's
+// inputs go through a per-warp ring of kStages shared-memory stages filled
+// by cp.async — the arc rows, the opposite table's rows (coalesced 16-byte
+// copies spread over the warp's lanes) and each lane's own dual / average
+// entry — so a lane walking a long diagram waits on memory once per
+// kStages - 1 positions instead of once per position.  Arithmetic and
+// operand order are those of the register kernels above (bit-identical).
+constexpr int kStages = 4;
+constexpr int kPW = 8;  // node slots per position
+
+struct PipeStage {
+    int32_t z[kPW][32], o[kPW][32];
+    double t[kPW][32];  // opposite-direction table rows (MM passes)
+    double lam[32], avg[32];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Stage fill: arc rows of position `ka` (w rows), table rows `kt` (wt rows),
+// this lane's dual and average at layer `l` (l < 0: none).  A row of int32 is
+// 128 bytes = 8 chunks, a row of doubles 256 bytes = 16 chunks; chunk c of
+// the stage goes to lane c % 32.
+template <bool kTab, bool kAvg>
+__device__ __forceinline__ void fill_stage(PipeStage &st, const dm::SweepDev &s, int lane, int32_t w, int64_t slot,
+                                           const double *tab, int32_t wt, int64_t slot_t, const double *lam,
+                                           const double *avg, int32_t l) {
+#pragma unroll
+    for (int c = lane; c < 2 * kPW * 8; c += 32) {  // zero / one arc rows
+        const int arr = c / (kPW * 8), row = (c / 8) % kPW, q = c % 8;
+        if (row < w) {
+            const int32_t *src = (arr ? s.ol : s.zl) + (slot + row) * 32 + q * 4;
+            cp16((arr ? &st.o[row][0] : &st.z[row][0]) + q * 4, src);
+        }
+    }
+    if (kTab) {
+#pragma unroll
+        for (int c = lane; c < kPW * 16; c += 32) {
+            const int row = c / 16, q = c % 16;
+            if (row < wt) cp16(&st.t[row][q * 2], tab + (slot_t + row) * 32 + q * 2);
+        }
+    }
+    if (l >= 0) {
+        cp8(&st.lam[lane], lam + l);
+        if (kAvg) cp8(&st.avg[lane], avg + l);
+    }
+}
+
+template <bool kMM, bool kAvg, bool kDec>
+__global__ void __launch_bounds__(kThreads) dfr_backward_pipe_kernel(DfrArgs a) {
+    constexpr int W = kPW;
+    extern __shared__ double sm[];
+    const dm::SweepDev &s = a.s;
+    double *__restrict__ lamp = a.lam;
+    const double *__restrict__ avgp = a.avg;
+    const double *__restrict__ inp = a.in;
+    double *__restrict__ outp = a.out;
+    double *__restrict__ mbarp = a.mbar;
+    double *__restrict__ boundsp = a.bounds;
+    uint64_t *__restrict__ decp = a.dec;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = s.bdd_layer_lo[j];
+        nj = s.bdd_layer_lo[j + 1] - l0;
+    }
+    const int32_t K = s.grp_npos[g];
+    const int64_t p0 = s.grp_pos_lo[g];
+    double *nb = sm + threadIdx.x;                  // distances of position k-1 (next layer)
+    double *cur = sm + W * kThreads + threadIdx.x;  // position k
+    PipeStage *ring = reinterpret_cast<PipeStage *>(sm + 2 * W * kThreads) + wid * kStages;
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    Meta meta{meta_w[wid], meta_s[wid], 0};
+    meta_window(meta, s, p0, K, 0, lane);
+    auto issue = [&](int32_t kk) {  // fill the stage of position kk (a commit group per position, maybe empty)
+        if (kk < K) {
+            const int32_t w = meta.w[kk - meta.lo];
+            const int64_t slot = meta.slot[kk - meta.lo];
+            fill_stage<kMM, kAvg>(ring[kk % kStages], s, lane, w, slot, inp, w, slot, lamp, avgp,
+                                  kk < nj ? l0 + nj - 1 - kk : -1);
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int kk = 0; kk < kStages - 1; ++kk) issue(kk);
+    for (int32_t k = 0; k < K; ++k) {
+        // positions k .. k + kStages - 1 must be in the metadata window (uniform in the warp)
+        if (k + kStages - 1 >= meta.lo + kMetaWin && meta.lo + kMetaWin < K) meta_window(meta, s, p0, K, k, lane);
+        cp_wait<kStages - 2>();  // position k's stage has landed (this lane's copies) ...
+        __syncwarp();            // ... and every lane's
+        const PipeStage &st = ring[k % kStages];
+        const int32_t w = meta.w[k - meta.lo];
+        const int64_t slot = meta.slot[k - meta.lo];
+        const bool act = k < nj;
+        const int32_t l = l0 + nj - 1 - k;
+        double lam_l = act ? st.lam[lane] : 0.0;
+        if (act && (kMM || kAvg)) {
+            const double a_l = kAvg ? st.avg[lane] : 0.0;
+            if (kMM) {
+                double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+                for (int i = 0; i < W; ++i)
+                    if (i < w) {
+                        const double fv = st.t[i][lane];
+                        const double c0 = c_zero(st.z[i][lane], fv, nb);
+                        const double c1 = c_one(st.o[i][lane], __dadd_rn(fv, lam_l), nb);
+                        if (c0 < m0) m0 = c0;
+                        if (c1 < m1) m1 = c1;
+                    }
+                lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, mbarp + l);
+            } else {
+                lam_l = __dadd_rn(lam_l, a_l);
+            }
+            lamp[l] = lam_l;
+        }
+        uint64_t word = 0;
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < w) {
+                const int32_t za_ = st.z[i][lane], ob = st.o[i][lane];
+                const double c0 = za_ == dm::kTrue ? 0.0 : (za_ == dm::kFalse ? DM_INF : nb[za_ * kThreads]);
+                const double c1 =
+                    ob == dm::kTrue ? lam_l : (ob == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[ob * kThreads]));
+                const bool zero_wins = c0 <= c1;
+                const double v = zero_wins ? c0 : c1;
+                cur[i * kThreads] = v;
+                outp[(slot + i) * 32 + lane] = v;
+                if (kDec) {
+                    const int32_t t = zero_wins ? za_ : ob;
+                    word |= (uint64_t)((((t >= 0) ? t : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * i);
+                }
+            }
+        if (kDec && act) decp[l] = word;
+        __syncwarp();  // every lane is done with this stage before it is refilled
+        issue(k + kStages - 1);
+        double *t = nb;
+        nb = cur;
+        cur = t;
+        if (act && k == nj - 1) boundsp[j] = nb[0];  // root layer: single node
+    }
+    cp_wait<0>();
+}
+
+template <bool kMM, bool kAvg>
+__global__ void __launch_bounds__(kThreads) dfr_forward_pipe_kernel(DfrArgs a) {
+    constexpr int W = kPW;
+    extern __shared__ double sm[];
+    const dm::SweepDev &s = a.s;
+    double *__restrict__ lamp = a.lam;
+    const double *__restrict__ avgp = a.avg;
+    const double *__restrict__ inp = a.in;
+    double *__restrict__ outp = a.out;
+    double *__restrict__ mbarp = a.mbar;
+    double *__restrict__ boundsp = a.bounds;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = s.bdd_layer_lo[j];
+        nj = s.bdd_layer_lo[j + 1] - l0;
+    }
+    const int32_t K = s.grp_npos[g];
+    const int64_t p0 = s.grp_pos_lo[g];
+    double *cur = sm + threadIdx.x;                 // distances from the root, position k
+    double *nxt = sm + W * kThreads + threadIdx.x;  // position k-1
+    PipeStage *ring = reinterpret_cast<PipeStage *>(sm + 2 * W * kThreads) + wid * kStages;
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    Meta meta{meta_w[wid], meta_s[wid], 0};
+    meta_window(meta, s, p0, K, K > kMetaWin ? K - kMetaWin : 0, lane);
+    double tb = DM_INF;
+    // step n handles position k = K - 1 - n (the walk runs from the roots down)
+    auto issue = [&](int32_t n) {
+        const int32_t kk = K - 1 - n;
+        if (kk >= 0) {
+            const int32_t w = meta.w[kk - meta.lo];
+            const int64_t slot = meta.slot[kk - meta.lo];
+            const int32_t wt = kk > 0 ? meta.w[kk - 1 - meta.lo] : 0;
+            const int64_t st = kk > 0 ? meta.slot[kk - 1 - meta.lo] : 0;
+            fill_stage<kMM, kAvg>(ring[n % kStages], s, lane, w, slot, inp, wt, st, lamp, avgp,
+                                  kk < nj ? l0 + nj - 1 - kk : -1);
+        }
+        cp_commit();
+    };
+    // positions k - kStages .. k must be in the window (uniform in the warp)
+    auto window_for = [&](int32_t k) {
+        if (k - kStages < meta.lo && meta.lo > 0) {
+            const int32_t lo = k + 1 > kMetaWin ? k + 1 - kMetaWin : 0;
+            meta_window(meta, s, p0, K, lo, lane);
+        }
+    };
+    window_for(K - 1);
+#pragma unroll
+    for (int n = 0; n < kStages - 1; ++n) issue(n);
+    for (int32_t n = 0; n < K; ++n) {
+        const int32_t k = K - 1 - n;
+        window_for(k);
+        cp_wait<kStages - 2>();
+        __syncwarp();
+        const PipeStage &st = ring[n % kStages];
+        if (k < nj) {
+            const int32_t w = meta.w[k - meta.lo];
+            const int64_t slot = meta.slot[k - meta.lo];
+            const int32_t wn = k > 0 ? meta.w[k - 1 - meta.lo] : 0;
+            double lam_l = st.lam[lane];
+            const int32_t l = l0 + nj - 1 - k;
+            if (k == nj - 1) {  // root layer: F[root] = 0 (kernels.py:187-193)
+                cur[0] = 0.0;
+#pragma unroll
+                for (int i = 1; i < W; ++i) cur[i * kThreads] = DM_INF;
+            }
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < w) outp[(slot + i) * 32 + lane] = cur[i * kThreads];
+            if (kMM) {
+                const double a_l = kAvg ? st.avg[lane] : 0.0;
+                double m0 = DM_INF, m1 = DM_INF;
+#pragma unroll
+                for (int i = 0; i < W; ++i)
+                    if (i < w) {
+                        const double fv = cur[i * kThreads];
+                        const int32_t za_ = st.z[i][lane], ob = st.o[i][lane];
+                        const double c0 = za_ == dm::kTrue ? fv : (za_ == dm::kFalse ? DM_INF : __dadd_rn(fv, st.t[za_][lane]));
+                        const double fl = __dadd_rn(fv, lam_l);
+                        const double c1 = ob == dm::kTrue ? fl : (ob == dm::kFalse ? DM_INF : __dadd_rn(fl, st.t[ob][lane]));
+                        if (c0 < m0) m0 = c0;
+                        if (c1 < m1) m1 = c1;
+                    }
+                lam_l = dfr_update<kAvg>(lam_l, a_l, m0, m1, a.omega, mbarp + l);
+                lamp[l] = lam_l;
+            } else if (kAvg) {
+                lam_l = __dadd_rn(lam_l, st.avg[lane]);
+                lamp[l] = lam_l;
+            }
+            // push this layer's distances into the next one (kernels.py:241-269)
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                if (u < wn) nxt[u * kThreads] = DM_INF;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < w) {
+                    const double fv = cur[i * kThreads];
+                    if (fv == DM_INF) continue;
+                    const int32_t za_ = st.z[i][lane], ob = st.o[i][lane];
+                    if (za_ >= 0) {
+                        if (fv < nxt[za_ * kThreads]) nxt[za_ * kThreads] = fv;
+                    } else if (za_ == dm::kTrue) {
+                        if (fv < tb) tb = fv;
+                    }
+                    const double c = __dadd_rn(fv, lam_l);
+                    if (ob >= 0) {
+                        if (c < nxt[ob * kThreads]) nxt[ob * kThreads] = c;
+                    } else if (ob == dm::kTrue) {
+                        if (c < tb) tb = c;
+                    }
+                }
+            double *t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        __syncwarp();
+        issue(n + kStages - 1);
+    }
+    cp_wait<0>();
+    if (j >= 0) boundsp[j] = tb;
+}
+
 // One pass's escrow -> the next pass's per-copy average: thread per
 // visitation position (variable), copies summed in copy order.  kApply (the
 // flush): the average goes straight into the duals, lam[l] += avg (the same
@@ -526,6 +811,34 @@ int launch(Kern kern, const DfrArgs &a, size_t smem, cudaStream_t st, const char
     return e == cudaSuccess ? DM_OK : fail(e, what);
 }
 
+bool use_pipe() {
+    static const int v = [] {
+        const char *e = std::getenv("DM_DFR_PIPE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+int backward_pipe(const DfrArgs &a, cudaStream_t st) {
+    const size_t smem = 2 * kPW * kThreads * sizeof(double) + kWarps * kStages * sizeof(PipeStage);
+    const bool mm = a.mbar != nullptr, avg = a.avg != nullptr, dec = a.dec != nullptr;
+    if (mm && avg) return launch(dfr_backward_pipe_kernel<true, true, false>, a, smem, st, "dfr_backward");
+    if (mm) return launch(dfr_backward_pipe_kernel<true, false, false>, a, smem, st, "dfr_backward");
+    if (avg && dec) return launch(dfr_backward_pipe_kernel<false, true, true>, a, smem, st, "dfr_backward");
+    if (avg) return launch(dfr_backward_pipe_kernel<false, true, false>, a, smem, st, "dfr_backward");
+    if (dec) return launch(dfr_backward_pipe_kernel<false, false, true>, a, smem, st, "dfr_backward");
+    return launch(dfr_backward_pipe_kernel<false, false, false>, a, smem, st, "dfr_backward");
+}
+
+int forward_pipe(const DfrArgs &a, cudaStream_t st) {
+    const size_t smem = 2 * kPW * kThreads * sizeof(double) + kWarps * kStages * sizeof(PipeStage);
+    const bool mm = a.mbar != nullptr, avg = a.avg != nullptr;
+    if (mm && avg) return launch(dfr_forward_pipe_kernel<true, true>, a, smem, st, "dfr_forward");
+    if (mm) return launch(dfr_forward_pipe_kernel<true, false>, a, smem, st, "dfr_forward");
+    if (avg) return launch(dfr_forward_pipe_kernel<false, true>, a, smem, st, "dfr_forward");
+    return launch(dfr_forward_pipe_kernel<false, false>, a, smem, st, "dfr_forward");
+}
+
 template <int W>
 int backward_w(const DfrArgs &a, cudaStream_t st) {
     const size_t smem = 2 * W * kThreads * sizeof(double);
@@ -558,10 +871,12 @@ int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const d
     DfrArgs a{s, omega, lam, avg, in, out, mbar, bounds, forward ? nullptr : dec};
     cudaStream_t st = (cudaStream_t)stream;
     if (forward) {
+        if (s.max_width <= 8 && use_pipe()) return forward_pipe(a, st);
         if (s.max_width <= 8) return forward_w<8>(a, st);
         if (s.max_width <= 16) return forward_w<16>(a, st);
         return forward_w<32>(a, st);
     }
+    if (s.max_width <= 8 && use_pipe()) return backward_pipe(a, st);
     if (s.max_width <= 8) return backward_w<8>(a, st);
     if (s.max_width <= 16) return backward_w<16>(a, st);
     return backward_w<32>(a, st);

@@ -24,13 +24,14 @@ ap.add_argument("configs", nargs="+")
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--iters-exact", type=int, default=1500)
 ap.add_argument("--iters-deferred", type=int, default=4000)
+ap.add_argument("--chunk", type=int, default=128, help="split length of the lowering (0: unsplit)")
 a = ap.parse_args()
 table = {}
 if os.path.exists(DSTAR_PATH):
     with open(DSTAR_PATH) as fh:
         table = json.load(fh)
 for cfg in a.configs:
-    inst = build_instance(cfg, a.seed)
+    inst = build_instance(cfg, a.seed, a.chunk)
     runs = {}
     for sched, iters in (("exact", a.iters_exact), ("deferred", a.iters_deferred)):
         t = time.perf_counter()
@@ -43,7 +44,8 @@ for cfg in a.configs:
                        "gain_last_10pct": res.best_bound - max(b[:-k])}
         print(cfg, sched, runs[sched], file=sys.stderr, flush=True)
     best = max(r["best_bound"] for r in runs.values())
-    table[f"{cfg}:{a.seed}"] = {"d_star": best, "rows_hash": inst._rows_hash, "runs": runs,
+    table[f"{cfg}:{a.seed}" + ("" if a.chunk == 128 else f":chunk{a.chunk}")] = {"d_star": best, "rows_hash": inst._rows_hash, "runs": runs,
+                                "chunk": a.chunk,
                                 "source": "best dual bound of long hybrid runs of both schedules on a B200 "
                                           f"(exact {a.iters_exact}, deferred {a.iters_deferred} iterations, no "
                                           "stopping rule; tools/dstar.py)"}
