@@ -814,7 +814,7 @@ int launch(Kern kern, const DfrArgs &a, size_t smem, cudaStream_t st, const char
 bool use_pipe() {
     static const int v = [] {
         const char *e = std::getenv("DM_DFR_PIPE");
-        return e ? std::atoi(e) : 1;
+        return e ? std::atoi(e) : 0;  // A/B: the ring costs occupancy; slower than the register kernels
     }();
     return v != 0;
 }
