@@ -289,6 +289,10 @@ int dm_agreement_scores(const dm_flat *f, const double *m0, const double *m1, in
  * length, stream) and cached for the process, so solves on different streams
  * may run concurrently; calls on one stream are ordered by that stream. */
 int dm_sum(const double *x, int64_t n, double *out, void *stream);
+/* Free every cached reduction plan / dot scratch (all devices; synchronises
+ * them first).  For long-running processes between batches, with no work in
+ * flight on any stream that used them. */
+int dm_release_caches(void);
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream);
 
 /* L-BFGS two-loop recursion (reference qn.py:95-115, lbfgs_direction):

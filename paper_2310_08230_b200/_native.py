@@ -89,6 +89,7 @@ SIGNATURES = {
     "dm_lambda_sums": ([_P, _P, _P, _P], _INT),
     "dm_agreement_scores": ([_P, _P, _P, _P, _P, _P, _P], _INT),
     "dm_sum": ([_P, _I, _P, _P], _INT),
+    "dm_release_caches": ([], _INT),
     "dm_dot": ([_P, _P, _I, _P, _P], _INT),
     "dm_axpy_dev": ([_P, _P, _D, _P, _P, _I, _P], _INT),
     "dm_scale_dev": ([_P, _D, _P, _I, _P], _INT),

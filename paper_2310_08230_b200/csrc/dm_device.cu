@@ -2592,6 +2592,33 @@ static int dot_scratch(int64_t n, void *stream, bool slots, DotScratch **out) {
     return DM_OK;
 }
 
+// Frees every cached reduction plan and dot scratch (all devices): the
+// caches are keyed by (device, length, stream) and otherwise live for the
+// process — a long-running service calls this between batches, with no
+// work in flight.
+int dm_release_caches(void) {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    auto release = [&](int dev, std::initializer_list<void *> ptrs) {
+        cudaSetDevice(dev);
+        cudaDeviceSynchronize();
+        for (void *p : ptrs)
+            if (p) cudaFree(p);
+    };
+    for (auto &kv : g_plans) {
+        const DevPlan &p = kv.second;
+        release(std::get<0>(kv.first), {p.leaf_off, p.leaf_len, p.left, p.right, p.height_lo, p.vals});
+    }
+    g_plans.clear();
+    for (auto &kv : g_dot) release(std::get<0>(kv.first), {kv.second.partial, kv.second.slots});
+    g_dot.clear();
+    cudaSetDevice(cur);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "release caches");
+    return DM_OK;
+}
+
 int dm_dot(const double *a, const double *b, int64_t n, double *out, void *stream) {
     DM_STREAM_GUARD(stream);
     if (!a || !b || !out || n < 0) {

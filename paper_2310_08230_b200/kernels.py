@@ -189,6 +189,13 @@ class DeviceFlat:
 
 
 # --- reductions and elementwise vectors (no handle needed) ---------------------
+def release_caches() -> None:
+    """Free the library's cached reduction plans and dot scratch (keyed by
+    device, length and stream; they otherwise live for the process).  Call
+    with no solve in flight."""
+    _native.check(_native.load().dm_release_caches(), "dm_release_caches")
+
+
 def dev_sum(x: torch.Tensor, out: torch.Tensor) -> None:
     """out[0] = np.sum(x) in numpy's pairwise order."""
     _native.call("dm_sum", _ptr(x), x.numel(), _ptr(out), _stream(x.device))

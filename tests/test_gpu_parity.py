@@ -534,3 +534,22 @@ def test_solve_on_a_non_current_device_restores_the_current_device():
     res = qn.solve(inst, SolveConfig(max_iterations=3), device="cuda:1")
     assert torch.cuda.current_device() == 0
     assert res.state.device == torch.device("cuda", 1)
+
+
+def test_release_caches_then_reductions_still_match():
+    """dm_release_caches frees the cached plans / scratch; later reductions
+    rebuild them and still give numpy's bits."""
+    from paper_2310_08230_b200.kernels import release_caches
+
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal(100_003)
+    ta = torch.as_tensor(a, device="cuda")
+    out = torch.empty(2, dtype=torch.float64, device="cuda")
+    dev_sum(ta, out[0:1])
+    dev_dot(ta, ta, out[1:2])
+    release_caches()
+    dev_sum(ta, out[0:1])
+    dev_dot(ta, ta, out[1:2])
+    got = out.cpu().numpy()
+    assert got[0].tobytes() == np.sum(a).tobytes()
+    assert got[1].tobytes() == np.float64(solver._dot_chunked(a, a)).tobytes()
