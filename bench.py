@@ -671,7 +671,7 @@ def c5_solve(insts, dev, schedule):
     return time.perf_counter() - t, res
 
 
-C5_ITERATIONS = {"exact": 10, "deferred": 40}
+C5_ITERATIONS = {"exact": 25, "deferred": 100}
 
 
 def SolveConfigC5(schedule):  # noqa: N802 - a config factory
