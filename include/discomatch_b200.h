@@ -122,6 +122,7 @@ typedef struct {
     int64_t device_bytes;
     int64_t lanes_per_task;     /* trace / task_levels records per task: 32 (one per BDD copy lane),
                                    8 (node-parallel kernels: one per copy slot) */
+    int64_t dfr_node_parallel;  /* 1: dm_dfr_np_* available (layers <= 8 nodes, single-source publish) */
 } dm_flat_info;
 
 int dm_flat_create(const dm_flat_desc *desc, int device, void *stream, dm_flat **out);
@@ -225,6 +226,14 @@ int dm_dfr_forward(const dm_flat *f, double omega, double *lam, const double *av
  * dm_k_argmin_from_pass(f, B_il, ...) walks */
 int dm_dfr_backward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *F_il,
                     double *B_il, double *mbar, double *bounds, int record_decisions, void *stream);
+/* The same two passes node-parallel (8 lanes per diagram) on tables in the
+ * reference NODE order (FlatBdds F / B, as dm_k_forward / dm_k_backward
+ * write them); bit-identical to the interleaved ones.  DM_ERR_UNSUPPORTED
+ * unless dm_flat_info.dfr_node_parallel. */
+int dm_dfr_np_forward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *B,
+                      double *F, double *mbar, double *bounds, void *stream);
+int dm_dfr_np_backward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *F, double *B,
+                       double *mbar, double *bounds, int record_decisions, void *stream);
 /* segmented reduction over the variable CSR (proc_ptr / proc_layers) */
 int dm_dfr_average(const dm_flat *f, const double *mbar, double *avg_in, void *stream);
 /* the flush: lam[l] += the average dm_dfr_average would write (one rounding,

@@ -42,7 +42,7 @@ class FlatDesc(ctypes.Structure):
 class FlatInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "fw_depth", "bw_depth", "fw_tasks", "bw_tasks", "mma_grid", "mma_block", "max_width",
-        "max_degree", "device_bytes", "lanes_per_task")]
+        "max_degree", "device_bytes", "lanes_per_task", "dfr_node_parallel")]
 
 
 # name -> (argtypes, restype); kept in sync with include/discomatch_b200.h
@@ -77,6 +77,8 @@ SIGNATURES = {
     "dm_dfr_table_size": ([_P, ctypes.POINTER(_I)], _INT),
     "dm_dfr_forward": ([_P, _D, _P, _P, _P, _P, _P, _P, _P], _INT),
     "dm_dfr_backward": ([_P, _D, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
+    "dm_dfr_np_forward": ([_P, _D, _P, _P, _P, _P, _P, _P, _P], _INT),
+    "dm_dfr_np_backward": ([_P, _D, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
     "dm_dfr_average": ([_P, _P, _P, _P], _INT),
     "dm_dfr_flush": ([_P, _P, _P, _P], _INT),
     "dm_dfr_average_csr": ([_I, _P, _P, _P, _P, _INT, _P], _INT),
@@ -149,7 +151,7 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",
                   "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search",
-                  "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_average", "dm_dfr_flush", "dm_dfr_to_nodes",
+                  "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_np_forward", "dm_dfr_np_backward", "dm_dfr_average", "dm_dfr_flush", "dm_dfr_to_nodes",
                   "dm_dfr_average_csr", "dm_dfr_boundary_gather", "dm_dfr_boundary_average",
                   "dm_perturb_round"}
 launch_count = 0

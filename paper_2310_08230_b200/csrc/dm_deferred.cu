@@ -133,6 +133,13 @@ __device__ __forceinline__ void warm_rows(const dm::SweepDev &s, int lane, int32
     }
 }
 
+// dfr_update with the escrow returned instead of stored
+template <bool kAvg>
+__device__ __forceinline__ double dfr_update_v(double lam_l, double a_l, double m0, double m1, double omega,
+                                               double &mbar_out) {
+    return dfr_update<kAvg>(lam_l, a_l, m0, m1, omega, &mbar_out);
+}
+
 // Backward direction: positions k = 0 (every lane's last layer) .. K-1.
 template <int W, bool kMM, bool kAvg, bool kDec>
 __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
@@ -411,6 +418,259 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         nxt = t;
     }
     if (j >= 0) boundsp[j] = tb;
+}
+
+// ---------------------------------------------------------------------------
+// Node-parallel passes (layers of <= 8 nodes with single-source publish
+// descriptors — every product-space instance): 8 lanes per diagram, lane q
+// holds node q of the diagram's current layer, 4 diagrams per warp (taken in
+// the sweep layout's longest-first order).  A position's work is spread over
+// the layer's nodes: next-layer distances reach the arcs by shuffles, m0/m1
+// are leftmost-minimum trees over the 8 lanes (the same value a sequential
+// strict-< scan keeps, ties included), the forward publish reads the
+// per-layer source descriptors (dm_plan.cu relax_kernel) and takes, per
+// target, the leftmost minimum of its candidates in the reference's scan
+// order.  Tables in the reference node order (FlatBdds F / B).  Bit-identical
+// to the lane-per-diagram kernels and the oracle.
+struct NpArgs {
+    const int32_t *order;  // diagrams, longest first (sweep layout lanes; -1 = padding)
+    int64_t entries;
+    const int32_t *bdd_layer_lo, *lnl, *zero_t, *one_t;
+    const uint64_t *relax;
+    double omega;
+    double *lam;
+    const double *avg;
+    const double *in;  // opposite-direction table (node order)
+    double *out;       // this direction's table (node order)
+    double *mbar, *bounds;
+    uint64_t *dec;
+};
+
+constexpr int kNpThreads = 256;
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// leftmost minimum over the 8 lanes of a group (combine(left, right) keeps
+// left unless right < left): equals a sequential strict-< scan from +inf
+__device__ __forceinline__ double lmin8(double v, int q) {
+#pragma unroll
+    for (int s = 1; s < 8; s <<= 1) {
+        const double o = __shfl_xor_sync(kFullMask, v, s);
+        v = (q & s) ? ((v < o) ? v : o) : ((o < v) ? o : v);
+    }
+    return v;
+}
+
+template <bool kMM, bool kAvg, bool kDec>
+__global__ void __launch_bounds__(kNpThreads) dfr_np_backward_kernel(NpArgs a) {
+    const int lane = threadIdx.x & 31, q = lane & 7, gb = lane & ~7;
+    const int64_t e = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4 + (lane >> 3);
+    const int32_t j = e < a.entries ? a.order[e] : -1;
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = a.bdd_layer_lo[j];
+        nj = a.bdd_layer_lo[j + 1] - l0;
+    }
+    int32_t K = nj;
+    K = max(K, __shfl_xor_sync(kFullMask, K, 8));
+    K = max(K, __shfl_xor_sync(kFullMask, K, 16));
+    if (K == 0) return;
+    // prefetch: node range of position k+1, and the rows of position k
+    int32_t base_n = 0, end_n = 0;  // [lnl[l], lnl[l+1]) of the next position
+    auto range = [&](int32_t k, int32_t &b, int32_t &en) {
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            b = a.lnl[l];
+            en = a.lnl[l + 1];
+        } else {
+            b = en = 0;
+        }
+    };
+    int32_t z_n = dm::kFalse, o_n = dm::kFalse;
+    double f_n = 0.0, lam_n = 0.0, avg_n = 0.0;
+    int32_t base_c = 0, end_c = 0;
+    auto rows = [&](int32_t k, int32_t b, int32_t en) {
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            if (q < en - b) {
+                z_n = a.zero_t[b + q];
+                o_n = a.one_t[b + q];
+                if (kMM) f_n = a.in[b + q];
+            }
+            lam_n = a.lam[l];
+            if (kAvg) avg_n = a.avg[l];
+        }
+    };
+    range(0, base_c, end_c);
+    range(1, base_n, end_n);
+    rows(0, base_c, end_c);
+    double bnext = DM_INF;  // B of node q of the next layer (position k-1)
+    int32_t nbase = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        const bool act = k < nj;
+        const int32_t l = l0 + nj - 1 - k;
+        const int32_t base = base_c, w = end_c - base_c;
+        const int32_t z = z_n, o = o_n;
+        const double fv = f_n;
+        double lam_l = lam_n;
+        const double a_l = avg_n;
+        const bool valid = act && q < w;
+        // issue the next position's loads
+        base_c = base_n;
+        end_c = end_n;
+        z_n = o_n = dm::kFalse;
+        if (k + 1 < K) rows(k + 1, base_c, end_c);
+        if (k + 2 < K) range(k + 2, base_n, end_n);
+        // next-layer distances of this node's arcs (terminals: lane unused)
+        const double bz = __shfl_sync(kFullMask, bnext, gb + (z >= 0 ? z - nbase : 0));
+        const double bo = __shfl_sync(kFullMask, bnext, gb + (o >= 0 ? o - nbase : 0));
+        if (kMM) {
+            double c0 = DM_INF, c1 = DM_INF;
+            if (valid) {
+                c0 = z == dm::kTrue ? fv : (z == dm::kFalse ? DM_INF : __dadd_rn(fv, bz));
+                const double fl = __dadd_rn(fv, lam_l);
+                c1 = o == dm::kTrue ? fl : (o == dm::kFalse ? DM_INF : __dadd_rn(fl, bo));
+            }
+            const double m0 = lmin8(c0, q), m1 = lmin8(c1, q);
+            if (act) {
+                double mb;
+                lam_l = dfr_update_v<kAvg>(lam_l, a_l, m0, m1, a.omega, mb);
+                if (q == 0) a.mbar[l] = mb;
+            }
+        } else if (kAvg && act) {
+            lam_l = __dadd_rn(lam_l, a_l);
+        }
+        if ((kMM || kAvg) && act && q == 0) a.lam[l] = lam_l;
+        const double c0 = z == dm::kTrue ? 0.0 : (z == dm::kFalse ? DM_INF : bz);
+        const double c1 = o == dm::kTrue ? lam_l : (o == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo));
+        const bool zero_wins = c0 <= c1;
+        const double bq = zero_wins ? c0 : c1;
+        if (valid) a.out[base + q] = bq;
+        if (kDec) {
+            const int32_t t = zero_wins ? z : o;
+            uint64_t word = valid ? (uint64_t)((((t >= 0) ? t - nbase : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * q) : 0ull;
+            word |= __shfl_xor_sync(kFullMask, word, 1);
+            word |= __shfl_xor_sync(kFullMask, word, 2);
+            word |= __shfl_xor_sync(kFullMask, word, 4);
+            if (act && q == 0) a.dec[l] = word;
+        }
+        bnext = valid ? bq : DM_INF;
+        nbase = base;
+        if (act && k == nj - 1 && q == 0) a.bounds[j] = bq;  // root layer: single node
+    }
+}
+
+template <bool kMM, bool kAvg>
+__global__ void __launch_bounds__(kNpThreads) dfr_np_forward_kernel(NpArgs a) {
+    const int lane = threadIdx.x & 31, q = lane & 7, gb = lane & ~7;
+    const int64_t e = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4 + (lane >> 3);
+    const int32_t j = e < a.entries ? a.order[e] : -1;
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = a.bdd_layer_lo[j];
+        nj = a.bdd_layer_lo[j + 1] - l0;
+    }
+    int32_t K = nj;
+    K = max(K, __shfl_xor_sync(kFullMask, K, 8));
+    K = max(K, __shfl_xor_sync(kFullMask, K, 16));
+    if (K == 0) return;
+    // position p = layer l0 + p; prefetch node ranges two ahead, rows one ahead
+    int32_t b_n = 0, e_n = 0, e2_n = 0;  // lnl[l], lnl[l+1], lnl[l+2] of position p+1
+    auto range = [&](int32_t p, int32_t &b, int32_t &en, int32_t &en2) {
+        if (p < nj) {
+            const int32_t l = l0 + p;
+            b = a.lnl[l];
+            en = a.lnl[l + 1];
+            en2 = p + 1 < nj ? a.lnl[l + 2] : en;
+        } else {
+            b = en = en2 = 0;
+        }
+    };
+    int32_t z_n = dm::kFalse, o_n = dm::kFalse;
+    double bn_n = DM_INF, lam_n = 0.0, avg_n = 0.0;
+    uint64_t desc_n = ~0ull;
+    int32_t b_c = 0, e_c = 0, e2_c = 0;
+    auto rows = [&](int32_t p, int32_t b, int32_t en, int32_t en2) {
+        if (p < nj) {
+            const int32_t l = l0 + p;
+            if (q < en - b) {
+                z_n = a.zero_t[b + q];
+                o_n = a.one_t[b + q];
+            }
+            if (kMM && q < en2 - en) bn_n = a.in[en + q];
+            lam_n = a.lam[l];
+            if (kAvg) avg_n = a.avg[l];
+            desc_n = a.relax[l];
+        }
+    };
+    range(0, b_c, e_c, e2_c);
+    range(1, b_n, e_n, e2_n);
+    rows(0, b_c, e_c, e2_c);
+    double fq = q == 0 ? 0.0 : DM_INF;  // F of node q of the current layer (root: F[root] = 0)
+    double tb = DM_INF;
+    for (int32_t p = 0; p < K; ++p) {
+        const bool act = p < nj;
+        const int32_t l = l0 + p;
+        const int32_t base = b_c, w = e_c - b_c, nbase = e_c, wn = e2_c - e_c;
+        const int32_t z = z_n, o = o_n;
+        const double bnq = bn_n;
+        double lam_l = lam_n;
+        const double a_l = avg_n;
+        const uint64_t desc = desc_n;
+        const bool valid = act && q < w;
+        b_c = b_n;
+        e_c = e_n;
+        e2_c = e2_n;
+        z_n = o_n = dm::kFalse;
+        bn_n = DM_INF;
+        if (p + 1 < K) rows(p + 1, b_c, e_c, e2_c);
+        if (p + 2 < K) range(p + 2, b_n, e_n, e2_n);
+        if (valid) a.out[base + q] = fq;
+        if (kMM) {
+            const double bz = __shfl_sync(kFullMask, bnq, gb + (z >= 0 ? z - nbase : 0));
+            const double bo = __shfl_sync(kFullMask, bnq, gb + (o >= 0 ? o - nbase : 0));
+            double c0 = DM_INF, c1 = DM_INF;
+            if (valid) {
+                c0 = z == dm::kTrue ? fq : (z == dm::kFalse ? DM_INF : __dadd_rn(fq, bz));
+                const double fl = __dadd_rn(fq, lam_l);
+                c1 = o == dm::kTrue ? fl : (o == dm::kFalse ? DM_INF : __dadd_rn(fl, bo));
+            }
+            const double m0 = lmin8(c0, q), m1 = lmin8(c1, q);
+            if (act) {
+                double mb;
+                lam_l = dfr_update_v<kAvg>(lam_l, a_l, m0, m1, a.omega, mb);
+                if (q == 0) {
+                    a.mbar[l] = mb;
+                    a.lam[l] = lam_l;
+                }
+            }
+        } else if (kAvg && act) {
+            lam_l = __dadd_rn(lam_l, a_l);
+            if (q == 0) a.lam[l] = lam_l;
+        }
+        // TRUE arcs of this layer: leftmost minimum in (node, zero-before-one) order
+        double t_loc = DM_INF;
+        if (valid && fq != DM_INF) {
+            if (z == dm::kTrue) t_loc = fq;
+            const double c = __dadd_rn(fq, lam_l);
+            if (o == dm::kTrue && c < t_loc) t_loc = c;
+        }
+        t_loc = lmin8(t_loc, q);
+        if (act && t_loc < tb) tb = t_loc;
+        // publish into the next layer: target u = q, its (at most one) zero and one source
+        const int zs = (int)((desc >> (8 * q)) & 15), os = (int)((desc >> (8 * q + 4)) & 15);
+        const double fz = __shfl_sync(kFullMask, fq, gb + (zs < 8 ? zs : 0));
+        const double fo = __shfl_sync(kFullMask, fq, gb + (os < 8 ? os : 0));
+        double fnew = DM_INF;
+        if (act && q < wn) {
+            const double cz = zs < 8 ? fz : DM_INF;  // INF sources never win a strict <
+            const double co = os < 8 ? __dadd_rn(fo, lam_l) : DM_INF;
+            const double first = (os < zs) ? co : cz, second = (os < zs) ? cz : co;  // same node: zero first
+            if (first < fnew) fnew = first;
+            if (second < fnew) fnew = second;
+        }
+        fq = fnew;
+    }
+    if (j >= 0 && q == 0) a.bounds[j] = tb;
 }
 
 // ---------------------------------------------------------------------------
@@ -925,5 +1185,33 @@ int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, c
     return e == cudaSuccess ? DM_OK : fail(e, "dfr_boundary_average");
 }
 
+int dfr_np_pass(const SweepDev &s, const int32_t *zero_t, const int32_t *one_t, const uint64_t *relax, bool forward,
+                double omega, double *lam, const double *avg, const double *in, double *out, double *mbar,
+                double *bounds, uint64_t *dec, void *stream) {
+    if (s.groups == 0) return DM_OK;
+    NpArgs a{s.grp_bdd, s.groups * 32, s.bdd_layer_lo, s.lnl, zero_t, one_t, relax, omega, lam, avg, in, out, mbar,
+             bounds, forward ? nullptr : dec};
+    const int64_t warps = (a.entries + 3) / 4;
+    const int blocks = (int)((warps * 32 + kNpThreads - 1) / kNpThreads);
+    const cudaStream_t st = (cudaStream_t)stream;
+    const bool mm = mbar != nullptr, av = avg != nullptr, dc = a.dec != nullptr;
+    if (forward) {
+        if (mm && av) dfr_np_forward_kernel<true, true><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (mm) dfr_np_forward_kernel<true, false><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (av) dfr_np_forward_kernel<false, true><<<blocks, kNpThreads, 0, st>>>(a);
+        else dfr_np_forward_kernel<false, false><<<blocks, kNpThreads, 0, st>>>(a);
+    } else {
+        if (mm && av) dfr_np_backward_kernel<true, true, false><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (mm) dfr_np_backward_kernel<true, false, false><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (av && dc) dfr_np_backward_kernel<false, true, true><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (av) dfr_np_backward_kernel<false, true, false><<<blocks, kNpThreads, 0, st>>>(a);
+        else if (dc) dfr_np_backward_kernel<false, false, true><<<blocks, kNpThreads, 0, st>>>(a);
+        else dfr_np_backward_kernel<false, false, false><<<blocks, kNpThreads, 0, st>>>(a);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DM_OK : fail(e, forward ? "dfr_np_forward" : "dfr_np_backward");
+}
+
 }  // namespace dm
+
 

@@ -2092,6 +2092,7 @@ int dm_flat_get_info(const dm_flat *f, dm_flat_info *info) {
     info->bw_depth = f->bw_depth;
     info->fw_tasks = f->mma_np ? f->np_fw_tasks : f->fw_tasks;
     info->bw_tasks = f->mma_np ? f->np_bw_tasks : f->bw_tasks;
+    info->dfr_node_parallel = f->relax_ok ? 1 : 0;
     info->lanes_per_task = f->mma_np ? 8 : 32;
     info->mma_grid = f->mma_grid_fw;
     info->mma_block = f->mma_threads;
@@ -2434,6 +2435,49 @@ int dm_dfr_backward(const dm_flat *f, double omega, double *lam, const double *a
     }
     const int rc = dm::dfr_pass(f->sweep, false, omega, lam, avg_in, F_il, B_il, mbar, bounds, dec, stream);
     m->dec_B = (rc == DM_OK && dec) ? B_il : (m->dec_B == B_il ? nullptr : m->dec_B);
+    return rc;
+}
+
+int dm_dfr_np_forward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *B,
+                      double *F, double *mbar, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!f->relax_ok) {
+        dm::set_error("dm_dfr_np_forward: needs layers of <= 8 nodes with single-source publish descriptors");
+        return DM_ERR_UNSUPPORTED;
+    }
+    if (!lam || !F || !bounds || (mbar && !B)) {
+        dm::set_error("dm_dfr_np_forward: lam, F, bounds (and B with mbar) are required");
+        return DM_ERR_INVALID;
+    }
+    if (f->dec_B == F) const_cast<dm_flat *>(f)->dec_B = nullptr;
+    return dm::dfr_np_pass(f->sweep, f->zero_t, f->one_t, f->relax_layer, true, omega, lam, avg_in, B, F, mbar, bounds,
+                           nullptr, stream);
+}
+
+int dm_dfr_np_backward(const dm_flat *f, double omega, double *lam, const double *avg_in, const double *F, double *B,
+                       double *mbar, double *bounds, int record_decisions, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!f->relax_ok) {
+        dm::set_error("dm_dfr_np_backward: needs layers of <= 8 nodes with single-source publish descriptors");
+        return DM_ERR_UNSUPPORTED;
+    }
+    if (!lam || !B || !bounds || (mbar && !F)) {
+        dm::set_error("dm_dfr_np_backward: lam, B, bounds (and F with mbar) are required");
+        return DM_ERR_INVALID;
+    }
+    dm_flat *m = const_cast<dm_flat *>(f);
+    uint64_t *dec = nullptr;
+    if (record_decisions && f->L > 0) {
+        if (!m->dec) {
+            DM_CUDA(cudaMallocAsync((void **)&m->dec, (size_t)f->L * 8, (cudaStream_t)stream));
+            m->allocs.push_back(m->dec);
+            m->bytes += (size_t)f->L * 8;
+        }
+        dec = m->dec;
+    }
+    const int rc = dm::dfr_np_pass(f->sweep, f->zero_t, f->one_t, f->relax_layer, false, omega, lam, avg_in, F, B,
+                                   mbar, bounds, dec, stream);
+    m->dec_B = (rc == DM_OK && dec) ? B : (m->dec_B == B ? nullptr : m->dec_B);
     return rc;
 }
 

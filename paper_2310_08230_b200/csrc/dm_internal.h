@@ -178,6 +178,11 @@ int dfr_pass(const SweepDev &s, bool forward, double omega, double *lam, const d
 int dfr_average(int64_t P, const int32_t *proc_ptr, const int32_t *proc_layers, const double *mbar, double *out,
                 bool apply, void *stream);
 int dfr_to_nodes(const SweepDev &s, const double *x_il, double *x, void *stream);
+// the same passes node-parallel (8 lanes per diagram; W <= 8 with single-source
+// publish descriptors `relax`), tables in the reference node order
+int dfr_np_pass(const SweepDev &s, const int32_t *zero_t, const int32_t *one_t, const uint64_t *relax, bool forward,
+                double omega, double *lam, const double *avg, const double *in, double *out, double *mbar,
+                double *bounds, uint64_t *dec, void *stream);
 int dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, const double *mbar, double *buf,
                         void *stream);
 int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,

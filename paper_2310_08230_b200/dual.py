@@ -10,6 +10,8 @@ unconstrained variables.  All vectors live in HBM (``lam_d``, ``F``, ``B``);
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -107,13 +109,18 @@ class DualState:
         self._bgen = 0  # generation of the distance-to-TRUE table B
         self._argmin_cache = None
         self._dec_gen = -1  # B generation whose argmin decisions the last backward pass recorded
+        self._np = False
         if schedule == SCHEDULE_DEFERRED:
-            # the deferred schedule keeps its distance tables in the sweep
-            # layout (dm_dfr_*): f_valid / b_valid then refer to F_il / B_il,
-            # and the node-order F / B are filled from them on demand
-            n = self.dev.dfr_table_size()
-            self.F_il = torch.zeros(n, dtype=_F64, device=d)
-            self.B_il = torch.zeros(n, dtype=_F64, device=d)
+            # node-parallel passes on the node-order F / B when the instance
+            # allows them (dm_dfr_np_*); otherwise lane-per-diagram passes on
+            # tables in the sweep layout (dm_dfr_*): f_valid / b_valid then
+            # refer to F_il / B_il, and the node-order F / B are filled from
+            # them on demand
+            self._np = self.dev.dfr_node_parallel and os.environ.get("DM_DFR_NP", "1") != "0"
+            if not self._np:
+                n = self.dev.dfr_table_size()
+                self.F_il = torch.zeros(n, dtype=_F64, device=d)
+                self.B_il = torch.zeros(n, dtype=_F64, device=d)
             self.mbar = torch.zeros(f.num_layers, dtype=_F64, device=d)  # escrow of the last pass
             self.avg = torch.zeros(f.num_layers, dtype=_F64, device=d)  # its per-copy average
         free = instance.unconstrained_variables()
@@ -195,9 +202,27 @@ class DualState:
     def deferred(self) -> bool:
         return self.schedule == SCHEDULE_DEFERRED
 
+    # the deferred schedule's two passes, on whichever tables it keeps
+    def _dfr_fw(self, omega, avg, mbar) -> None:
+        if self._np:
+            self.dev.dfr_np_forward(omega, self.lam_d, avg, self.B, self.F, mbar, self._bounds)
+        else:
+            self.dev.dfr_forward(omega, self.lam_d, avg, self.B_il, self.F_il, mbar, self._bounds)
+
+    def _dfr_bw(self, omega, avg, mbar, record_decisions=False) -> None:
+        if self._np:
+            self.dev.dfr_np_backward(omega, self.lam_d, avg, self.F, self.B, mbar, self._bounds, record_decisions)
+        else:
+            self.dev.dfr_backward(omega, self.lam_d, avg, self.F_il, self.B_il, mbar, self._bounds, record_decisions)
+
+    @property
+    def _dec_table(self) -> torch.Tensor:
+        """The distance table the recorded argmin decisions belong to."""
+        return self.B_il if self.deferred and not self._np else self.B
+
     def refresh_backward(self) -> None:
         if self.deferred:
-            self.dev.dfr_backward(0.0, self.lam_d, None, None, self.B_il, None, self._bounds, record_decisions=True)
+            self._dfr_bw(0.0, None, None, record_decisions=True)
             self._bgen += 1
             if self.dev.dfr_records_decisions:
                 self._dec_gen = self._bgen
@@ -210,7 +235,7 @@ class DualState:
 
     def refresh_forward(self) -> None:
         if self.deferred:
-            self.dev.dfr_forward(0.0, self.lam_d, None, None, self.F_il, None, self._bounds)
+            self._dfr_fw(0.0, None, None)
         else:
             self.dev.k_forward(self.lam_d, self.F, self._bounds)
         self.sweeps += 1
@@ -224,7 +249,7 @@ class DualState:
             self.refresh_forward()
         if need_b and not self.b_valid:
             self.refresh_backward()
-        if self.deferred:
+        if self.deferred and not self._np:
             if need_f:
                 self.dev.dfr_to_nodes(self.F_il, self.F)
             if need_b:
@@ -243,7 +268,7 @@ class DualState:
         if not self.b_valid:
             self.refresh_backward()
         ev = timer.begin("dfr_forward") if timer else None
-        self.dev.dfr_forward(omega, self.lam_d, None, self.B_il, self.F_il, self.mbar, self._bounds)
+        self._dfr_fw(omega, None, self.mbar)
         if ev:
             timer.end(ev)
         ev = timer.begin("dfr_average") if timer else None
@@ -251,7 +276,7 @@ class DualState:
         if ev:
             timer.end(ev)
         ev = timer.begin("dfr_backward") if timer else None
-        self.dev.dfr_backward(omega, self.lam_d, self.avg, self.F_il, self.B_il, self.mbar, self._bounds)
+        self._dfr_bw(omega, self.avg, self.mbar)
         if ev:
             timer.end(ev)
         # flush: the backward pass's escrow straight into the duals, then a
@@ -261,7 +286,7 @@ class DualState:
         if ev:
             timer.end(ev)
         ev = timer.begin("dfr_sweep") if timer else None
-        self.dev.dfr_backward(0.0, self.lam_d, None, None, self.B_il, None, self._bounds, record_decisions=True)
+        self._dfr_bw(0.0, None, None, record_decisions=True)
         if ev:
             timer.end(ev)
         self._bgen += 1
@@ -425,7 +450,7 @@ def subgradient_device(state: DualState) -> torch.Tensor:
     bits = torch.empty(state.flat.num_layers, dtype=_F64, device=state.device)
     if state._dec_gen == state._bgen:
         # decisions of the pass that wrote B
-        state.dev.k_argmin_from_pass(state.B_il if state.deferred else state.B, bits)
+        state.dev.k_argmin_from_pass(state._dec_table, bits)
     else:
         _, B = state.node_tables(need_f=False)
         state.dev.k_argmin(state.lam_d, B, bits)

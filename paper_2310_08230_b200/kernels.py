@@ -156,6 +156,18 @@ class DeviceFlat:
         _native.call("dm_dfr_backward", self._h, float(omega), _ptr(lam), _ptr(avg), _ptr(F_il), _ptr(B_il),
                      _ptr(mbar), _ptr(bounds), int(bool(record_decisions)), self._s())
 
+    def dfr_np_forward(self, omega, lam, avg, B, F, mbar, bounds):
+        _native.call("dm_dfr_np_forward", self._h, float(omega), _ptr(lam), _ptr(avg), _ptr(B), _ptr(F), _ptr(mbar),
+                     _ptr(bounds), self._s())
+
+    def dfr_np_backward(self, omega, lam, avg, F, B, mbar, bounds, record_decisions=False):
+        _native.call("dm_dfr_np_backward", self._h, float(omega), _ptr(lam), _ptr(avg), _ptr(F), _ptr(B), _ptr(mbar),
+                     _ptr(bounds), int(bool(record_decisions)), self._s())
+
+    @property
+    def dfr_node_parallel(self) -> bool:
+        return bool(self.info.get("dfr_node_parallel", 0))
+
     def dfr_average(self, mbar, avg):
         _native.call("dm_dfr_average", self._h, _ptr(mbar), _ptr(avg), self._s())
 

@@ -19,6 +19,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import model, solver
 from tests.golden_util import FLAT_FIELDS, case_inputs, load_cases
@@ -103,32 +104,45 @@ def _nodes(st, x_il):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("layout", ["node_parallel", "interleaved"])
 @pytest.mark.parametrize("omega", [0.5, 0.3])
 @pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
-def test_deferred_passes_match_oracle(case, omega):
-    """Each pass of a round, from arbitrary duals, bit for bit."""
+def test_deferred_passes_match_oracle(case, omega, layout, monkeypatch):
+    """Each pass of a round, from arbitrary duals, bit for bit — both kernel
+    families: node-parallel on node-order tables (dm_dfr_np_*) and lane per
+    diagram on the interleaved sweep layout (dm_dfr_*)."""
     from oracle.clib import lib, ptr
     from paper_2310_08230_b200.dual import init_duals
 
+    if layout == "interleaved":
+        monkeypatch.setenv("DM_DFR_NP", "0")
     inst = gpu_instance(case)
     oi, of = oracle_twin(inst)
     rng = np.random.default_rng(7)
     lam = rng.standard_normal(of.num_layers) * 3.0
     st = init_duals(inst, schedule="deferred")
-    st.set_lambda(lam)  # refresh_backward: the interleaved B and its decisions
+    if layout == "node_parallel" and not st._np:
+        pytest.skip("instance outside the node-parallel passes' envelope")
+    if st._np:
+        F_t, B_t, fw, bw = st.F, st.B, st.dev.dfr_np_forward, st.dev.dfr_np_backward
+        nodes = lambda x: x.cpu().numpy()  # noqa: E731
+    else:
+        F_t, B_t, fw, bw = st.F_il, st.B_il, st.dev.dfr_forward, st.dev.dfr_backward
+        nodes = lambda x: _nodes(st, x)  # noqa: E731
+    st.set_lambda(lam)  # refresh_backward: B and its decisions
     ost = solver.OracleDual(oi, of)
     ost.lam[:] = lam
     ost.refresh_backward()
-    assert _nodes(st, st.B_il).tobytes() == ost.B.tobytes()
+    assert nodes(B_t).tobytes() == ost.B.tobytes()
     assert st.bound == ost.bound
     geo = (of.num_bdds, ptr(of.bdd_layer_lo), ptr(of.layer_node_lo), ptr(of.zero_t), ptr(of.one_t))
     P = len(of.proc_ptr) - 1
     mbar, avg, bounds = np.zeros(of.num_layers), np.zeros(of.num_layers), np.zeros(of.num_bdds)
     # forward pass
-    st.dev.dfr_forward(omega, st.lam_d, None, st.B_il, st.F_il, st.mbar, st._bounds)
+    fw(omega, st.lam_d, None, B_t, F_t, st.mbar, st._bounds)
     lib.oracle_dfr_forward(*geo, omega, ptr(ost.lam), None, ptr(ost.B), ptr(ost.F), ptr(mbar), ptr(bounds))
     assert st.lam.tobytes() == ost.lam.tobytes()
-    assert _nodes(st, st.F_il).tobytes() == ost.F.tobytes()
+    assert nodes(F_t).tobytes() == ost.F.tobytes()
     assert st.mbar.cpu().numpy().tobytes() == mbar.tobytes()
     assert st._bounds.cpu().numpy().tobytes() == bounds.tobytes()
     # average
@@ -136,35 +150,42 @@ def test_deferred_passes_match_oracle(case, omega):
     lib.oracle_dfr_average(P, ptr(of.proc_ptr), ptr(of.proc_layers), ptr(mbar), ptr(avg))
     assert st.avg.cpu().numpy().tobytes() == avg.tobytes()
     # backward pass (adds the forward escrow)
-    st.dev.dfr_backward(omega, st.lam_d, st.avg, st.F_il, st.B_il, st.mbar, st._bounds)
+    bw(omega, st.lam_d, st.avg, F_t, B_t, st.mbar, st._bounds)
     lib.oracle_dfr_backward(*geo, omega, ptr(ost.lam), ptr(avg), ptr(ost.F), ptr(ost.B), ptr(mbar), ptr(bounds))
     assert st.lam.tobytes() == ost.lam.tobytes()
-    assert _nodes(st, st.B_il).tobytes() == ost.B.tobytes()
+    assert nodes(B_t).tobytes() == ost.B.tobytes()
     assert st.mbar.cpu().numpy().tobytes() == mbar.tobytes()
     assert st._bounds.cpu().numpy().tobytes() == bounds.tobytes()
     # flush: average + a sweep adding it == dm_dfr_flush (average into lam) + a plain sweep
-    lam2, B2, b2 = st.lam_d.clone(), st.B_il.clone(), st._bounds.clone()
+    lam2, B2, b2 = st.lam_d.clone(), B_t.clone(), st._bounds.clone()
     st.dev.dfr_average(st.mbar, st.avg)
-    st.dev.dfr_backward(0.0, lam2, st.avg, None, B2, None, b2)
+    bw(0.0, lam2, st.avg, None, B2, None, b2)
     st.dev.dfr_flush(st.mbar, st.lam_d)
-    st.dev.dfr_backward(0.0, st.lam_d, None, None, st.B_il, None, st._bounds, record_decisions=True)
+    bw(0.0, st.lam_d, None, None, B_t, None, st._bounds, True)
     lib.oracle_dfr_average(P, ptr(of.proc_ptr), ptr(of.proc_layers), ptr(mbar), ptr(avg))
     lib.oracle_dfr_backward(*geo, 0.0, ptr(ost.lam), ptr(avg), None, ptr(ost.B), None, ptr(bounds))
-    for lam_t, B_t, b_t in ((st.lam_d, st.B_il, st._bounds), (lam2, B2, b2)):
+    for lam_t, Bx, b_t in ((st.lam_d, B_t, st._bounds), (lam2, B2, b2)):
         assert lam_t.cpu().numpy().tobytes() == ost.lam.tobytes()
-        assert _nodes(st, B_t).tobytes() == ost.B.tobytes()
+        assert nodes(Bx).tobytes() == ost.B.tobytes()
         assert b_t.cpu().numpy().tobytes() == bounds.tobytes()
+    # the recorded decisions walk to the full argmin
+    bits = torch.empty(of.num_layers, dtype=torch.float64, device=st.device)
+    st.dev.k_argmin_from_pass(B_t, bits)
+    assert bits.cpu().numpy().tobytes() == ost.subgradient().tobytes()
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("layout", ["node_parallel", "interleaved"])
 @pytest.mark.parametrize("mode", ["mma-only", "hybrid"])
 @pytest.mark.parametrize("case", SMALL, ids=[c["name"] for c in SMALL])
-def test_deferred_solve_matches_oracle(case, mode):
+def test_deferred_solve_matches_oracle(case, mode, layout, monkeypatch):
     from paper_2310_08230_b200 import qn
     from paper_2310_08230_b200.config import SolveConfig
     from paper_2310_08230_b200.dual import subgradient
     from paper_2310_08230_b200.primal import agreement_scores
 
+    if layout == "interleaved":
+        monkeypatch.setenv("DM_DFR_NP", "0")
     inst = gpu_instance(case)
     oi, of = oracle_twin(inst)
     iters = 12

@@ -9,7 +9,10 @@ sys.path.insert(0, ".")
 from bench import build_instance  # noqa: E402
 from paper_2310_08230_b200.dual import init_duals  # noqa: E402
 
-inst = build_instance(sys.argv[1] if len(sys.argv) > 1 else "c2", 0)
+import os
+
+os.environ["DM_DFR_NP"] = "0"  # this state keeps interleaved tables; the node-parallel passes use st.F / st.B
+inst = build_instance(sys.argv[1] if len(sys.argv) > 1 else "c2", 0, int(sys.argv[2]) if len(sys.argv) > 2 else 128)
 st = init_duals(inst, device="cuda:0", schedule="deferred")
 st.deferred_round(0.5)
 dev = st.dev
@@ -41,6 +44,10 @@ out = {
     "sweep_nodec": t(lambda: dev.dfr_backward(0.0, st.lam_d, None, None, st.B_il, None, bounds, False)),
     "k_backward_nodes": t(lambda: dev.k_backward(st.lam_d, st.B, bounds)),
     "average": t(lambda: dev.dfr_average(st.mbar, st.avg)),
+    "np_fw_mm": t(lambda: dev.dfr_np_forward(0.5, st.lam_d, None, st.B, st.F, st.mbar, bounds)),
+    "np_bw_mm_avg": t(lambda: dev.dfr_np_backward(0.5, st.lam_d, st.avg, st.F, st.B, st.mbar, bounds)),
+    "np_sweep_dec": t(lambda: dev.dfr_np_backward(0.0, st.lam_d, None, None, st.B, None, bounds, True)),
+    "np_fw_sweep": t(lambda: dev.dfr_np_forward(0.0, st.lam_d, None, None, st.F, None, bounds)),
     "flush_apply": t(lambda: dev.dfr_flush(st.mbar, st.lam_d)),
 }
 print(json.dumps(out))
