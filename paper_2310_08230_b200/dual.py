@@ -21,6 +21,8 @@ from .kernels import DeviceFlat, FlatBdds, dev_axpy_host, dev_sum
 
 FORWARD = "forward"
 BACKWARD = "backward"
+NP_MAX_DIAGRAMS = 200_000  # deferred schedule: node-parallel passes up to this many diagrams ...
+NP_MIN_LAYERS = 256  # ... or when some diagram is longer than this
 
 _F64 = torch.float64
 
@@ -116,7 +118,14 @@ class DualState:
             # tables in the sweep layout (dm_dfr_*): f_valid / b_valid then
             # refer to F_il / B_il, and the node-order F / B are filled from
             # them on demand
-            self._np = self.dev.dfr_node_parallel and os.environ.get("DM_DFR_NP", "1") != "0"
+            # node-parallel passes pay off when few diagrams leave most lanes
+            # idle or long diagrams set a serial floor (C4: 125 k diagrams,
+            # passes 1.3-1.5x faster; unsplit C2: 4,002-layer diagrams, 1.4-1.7x),
+            # lane-per-diagram passes when there are many short diagrams (C2:
+            # 637 k, 2-2.7x faster); DM_DFR_NP=1/0 forces either
+            env = os.environ.get("DM_DFR_NP")
+            auto = f.num_bdds <= NP_MAX_DIAGRAMS or int(f.table.max_layers) > NP_MIN_LAYERS
+            self._np = self.dev.dfr_node_parallel and (auto if env is None else env != "0")
             if not self._np:
                 n = self.dev.dfr_table_size()
                 self.F_il = torch.zeros(n, dtype=_F64, device=d)

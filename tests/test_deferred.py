@@ -114,8 +114,7 @@ def test_deferred_passes_match_oracle(case, omega, layout, monkeypatch):
     from oracle.clib import lib, ptr
     from paper_2310_08230_b200.dual import init_duals
 
-    if layout == "interleaved":
-        monkeypatch.setenv("DM_DFR_NP", "0")
+    monkeypatch.setenv("DM_DFR_NP", "0" if layout == "interleaved" else "1")
     inst = gpu_instance(case)
     oi, of = oracle_twin(inst)
     rng = np.random.default_rng(7)
@@ -184,8 +183,7 @@ def test_deferred_solve_matches_oracle(case, mode, layout, monkeypatch):
     from paper_2310_08230_b200.dual import subgradient
     from paper_2310_08230_b200.primal import agreement_scores
 
-    if layout == "interleaved":
-        monkeypatch.setenv("DM_DFR_NP", "0")
+    monkeypatch.setenv("DM_DFR_NP", "0" if layout == "interleaved" else "1")
     inst = gpu_instance(case)
     oi, of = oracle_twin(inst)
     iters = 12
