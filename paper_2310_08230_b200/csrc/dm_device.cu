@@ -523,6 +523,7 @@ struct MmaArgs {
     int *progress;              // highest level of a finished task (monotone hint)
     int lookahead;              // start polling inputs once progress >= level - lookahead (0: always)
     int warm;                   // prefetch the polled lines into L2 at task start
+    int hints;                  // streaming (evict-first) loads: 1 copy records, 2 arcs, 4 the static table
     const uint64_t *relax_layer;  // per-layer source nibbles (forward, W == 8 only)
     // node-parallel kernels: task -> visitation position, its copies (CSR) and
     // per-layer first/last flags (bit 0 first layer of its BDD, bit 1 last)
@@ -1083,7 +1084,8 @@ __device__ __forceinline__ NpLaneX np_lane(const MmaArgs &a, int64_t task, int l
     NpLaneX r;
     r.c = lane >> 2;
     r.q = lane & 3;
-    const int4 rec = a.np_rec[task * kNpCopies + r.c];  // records stored in this pass's task order
+    const int4 *rp = a.np_rec + task * kNpCopies + r.c;  // records stored in this pass's task order
+    const int4 rec = (a.hints & 1) ? __ldcs(rp) : *rp;
     const unsigned m = (unsigned)rec.z;
     r.k = (int)(m >> 24);
     r.act = r.c < r.k;
@@ -1150,12 +1152,18 @@ __global__ void __launch_bounds__(256) mma_np_forward_kernel(MmaArgs a) {
                 if (D) desc = a.relax_layer[r.l];
             }
             lam_l = a.lam[r.l];
-            if (i0 < r.w) z0 = a.zero_t[r.nlo + i0], o0 = a.one_t[r.nlo + i0];
-            if (i1 < r.w) z1 = a.zero_t[r.nlo + i1], o1 = a.one_t[r.nlo + i1];
+            if (a.hints & 2) {
+                if (i0 < r.w) z0 = __ldcs(a.zero_t + r.nlo + i0), o0 = __ldcs(a.one_t + r.nlo + i0);
+                if (i1 < r.w) z1 = __ldcs(a.zero_t + r.nlo + i1), o1 = __ldcs(a.one_t + r.nlo + i1);
+            } else {
+                if (i0 < r.w) z0 = a.zero_t[r.nlo + i0], o0 = a.one_t[r.nlo + i0];
+                if (i1 < r.w) z1 = a.zero_t[r.nlo + i1], o1 = a.one_t[r.nlo + i1];
+            }
         }
         // marginal arc terms (see layer_marginals): +INF FALSE/padding, -0.0 TRUE
-        const double t00 = arc_term(z0, z0 >= 0 ? a.B[z0] : 0.0), t01 = arc_term(z1, z1 >= 0 ? a.B[z1] : 0.0);
-        const double t10 = arc_term(o0, o0 >= 0 ? a.B[o0] : 0.0), t11 = arc_term(o1, o1 >= 0 ? a.B[o1] : 0.0);
+        auto bt = [&](int32_t t) { return t >= 0 ? ((a.hints & 4) ? __ldcs(a.B + t) : a.B[t]) : 0.0; };
+        const double t00 = arc_term(z0, bt(z0)), t01 = arc_term(z1, bt(z1));
+        const double t10 = arc_term(o0, bt(o0)), t11 = arc_term(o1, bt(o1));
         double f0 = DM_INF, f1 = DM_INF;
         bool have = !r.act || i0 >= r.w;
         nodes[i0] = DM_INF;
@@ -1270,8 +1278,9 @@ __global__ void __launch_bounds__(256) mma_np_backward_kernel(MmaArgs a) {
         for (int j = 0; j < 2; ++j) {
             const int i = i0 + j;
             if (r.act && i < r.w) {
-                const int32_t z = a.zero_t[r.nlo + i], o = a.one_t[r.nlo + i];
-                const double fv = a.F[r.nlo + i];
+                const int32_t z = (a.hints & 2) ? __ldcs(a.zero_t + r.nlo + i) : a.zero_t[r.nlo + i];
+                const int32_t o = (a.hints & 2) ? __ldcs(a.one_t + r.nlo + i) : a.one_t[r.nlo + i];
+                const double fv = (a.hints & 4) ? __ldcs(a.F + r.nlo + i) : a.F[r.nlo + i];
                 zt[j] = z;
                 ot[j] = o;
                 iz[j] = z >= 0 ? ((z - n0n) & 7) : 8;
@@ -2323,6 +2332,7 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.progress = f->progress;
     args.lookahead = f->mma_lookahead;
     args.warm = f->mma_warm;
+    args.hints = env_int("DM_MMA_HINTS", 0);
     args.relax_layer = f->relax_layer;
     args.task_pos = forward ? f->fw_pos : f->bw_pos;
     args.proc_ptr = f->proc_ptr;
