@@ -710,8 +710,10 @@ def c5_summary(args, dev, reps=5):
     for schedule in ("exact", "deferred"):
         c5_solve(insts, dev, schedule)  # warm-up
         times = []
+        res = None
         for _ in range(reps):
-            gc.collect()  # the previous batch's device state is released outside the clock
+            del res  # the previous batch's device state is released outside the clock
+            gc.collect()
             torch.cuda.synchronize()
             sec, res = c5_solve(insts, dev, schedule)
             times.append(sec)
