@@ -1,56 +1,37 @@
-# usage (on the GPU box via gpurun): bash tools/run_gpu.sh <steps...>
+# usage (on the GPU box via gpurun): bash tools/run_gpu.sh <step...>
+# every output lands in gpurun_out/ (merged back by gpurun)
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
+B="python bench.py --steps 2 --warmup 1 --no-extras --no-ttg --no-e2e --no-cpu-baseline"
 for step in "$@"; do
   case "$step" in
-    tests) timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
+    tests) timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log ;;
-    sweep) timeout 900 python tools/mma_sweep.py c2 > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err; echo "sweep rc=$?" >> gpurun_out/sweep.err ;;
-    pingpong) ./tools/pingpong > gpurun_out/pingpong.txt 2>&1 ;;
-    latency) ./tools/latency > gpurun_out/latency.txt 2>&1 ;;
-    trace) timeout 600 python tools/mma_trace.py c2 > gpurun_out/trace.jsonl 2> gpurun_out/trace.err; echo "trace rc=$?" >> gpurun_out/trace.err ;;
-    bench) timeout 900 python bench.py --steps 5 --warmup 2 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err ;;
-    ncu_list)
-      B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
-      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
-      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
-          --log-file gpurun_out/launches.csv $B > gpurun_out/ncu.log 2>&1; echo "ncu_list rc=$?" >> gpurun_out/ncu.log ;;
-    ncu_full)
-      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
-      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
-      for k in mma_np_forward mma_np_backward sweep_backward chunk_step_kernel k_argmin; do
-        timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
-            -o gpurun_out/full_$k $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full $k rc=$?" >> gpurun_out/ncu_full.log
+    bench) timeout 1500 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?" >> gpurun_out/bench_default.err ;;
+    bench_ref) timeout 1500 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "rc=$?" >> gpurun_out/bench_ref.err ;;
+    bench_c5) timeout 900 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err ;;
+    bench_split) timeout 600 python bench.py --config c4 --split --steps 20 --warmup 5 > gpurun_out/bench_split.json 2> gpurun_out/bench_split.err ;;
+    dstar) timeout 1500 python tools/dstar.py c2 c3 c4 > gpurun_out/dstar.json 2> gpurun_out/dstar.err
+           timeout 1200 python tools/dstar.py c2 --chunk 0 --iters-exact 300 --iters-deferred 600 >> gpurun_out/dstar.json 2>> gpurun_out/dstar.err
+           cp profiles/dstar.json gpurun_out/dstar_all.json ;;
+    ncu_list)  # launch lists of the exact and the deferred bench step (profiles/r02_launches_*.md)
+      timeout 600 $B > gpurun_out/plain.log 2>&1 && \
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02_launches_exact.csv $B > gpurun_out/ncu_le.log 2>&1
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02_launches_deferred.csv $B --schedule deferred > gpurun_out/ncu_ld.log 2>&1 ;;
+    ncu_dfr)  # one deferred round at C2 and C4 (profiles/r02_dfr_*_full.md via tools/ncu_multi.py)
+      for c in c2 c4; do
+        timeout 300 python tools/dfr_round.py $c > gpurun_out/round_$c.log 2>&1 && \
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:dfr_ -s 1 -c 5 -o gpurun_out/r02_dfr_$c python tools/dfr_round.py $c > gpurun_out/ncu_dfr_$c.log 2>&1
       done ;;
-    ncu_mma2)
-      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
-      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
+    ncu_mma)  # the exact passes at C2
+      timeout 600 $B > gpurun_out/plain.log 2>&1 && \
       for k in mma_np_forward mma_np_backward; do
-        timeout 1500 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
-            -o gpurun_out/full_$k $B >> gpurun_out/ncu_full.log 2>&1; echo "ncu_full $k rc=$?" >> gpurun_out/ncu_full.log
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/r02_$k $B >> gpurun_out/ncu_mma.log 2>&1
       done ;;
-    ncu_mma)
-      B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg"
-      timeout 900 $B > gpurun_out/plain.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_forward -s 1 -c 1 \
-          -o gpurun_out/prof_mma_fw $B > gpurun_out/ncu_mma.log 2>&1 && \
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:mma_backward -s 1 -c 1 \
-          -o gpurun_out/prof_mma_bw $B >> gpurun_out/ncu_mma.log 2>&1; echo "ncu_mma rc=$?" >> gpurun_out/ncu_mma.log ;;
-    ab) timeout 1200 python tools/ab_mma.py tools/ab/*.so tools/ab/*.so > gpurun_out/ab.jsonl 2> gpurun_out/ab.err ;;
-    abdesc) timeout 1200 python tools/ab_mma.py DM_MMA_DESC=0 DM_MMA_DESC=1 DM_MMA_DESC=0 DM_MMA_DESC=1 > gpurun_out/abdesc.jsonl 2> gpurun_out/abdesc.err ;;
-    abnp) timeout 1200 python tools/ab_mma.py DM_MMA_NP=0 DM_MMA_NP=1 DM_MMA_NP=0 DM_MMA_NP=1 > gpurun_out/abnp.jsonl 2> gpurun_out/abnp.err ;;
-    e2eprof) timeout 900 python tools/e2e_profile.py > gpurun_out/e2eprof.txt 2>&1 ;;
-    create) timeout 900 python tools/create_timing.py > gpurun_out/create.txt 2>&1 ;;
-    workbench) ./tools/workbench > gpurun_out/workbench.jsonl 2>&1 ;;
-    worklat) timeout 600 python tools/work_latency.py icosa > gpurun_out/worklat.txt 2>&1 ;;
-    timeline) timeout 900 python tools/timeline.py > gpurun_out/timeline.json 2> gpurun_out/timeline.err ;;
-    concur) timeout 900 python tools/concurrency.py > gpurun_out/concur.jsonl 2> gpurun_out/concur.err ;;
-    batch) timeout 1500 python tools/batch_solve.py 4 > gpurun_out/batch.jsonl 2> gpurun_out/batch.err ;;
-    phases) timeout 900 python tools/step_phases.py 12 > gpurun_out/phases.jsonl 2> gpurun_out/phases.err ;;
-    vec) timeout 300 python tools/vec_bench.py > gpurun_out/vec.json 2> gpurun_out/vec.err && \
-      timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -c 400 --csv \
-          --log-file gpurun_out/vec_launches.csv python tools/vec_bench.py > gpurun_out/vec_ncu.log 2>&1 ;;
-    prof) timeout 900 python tools/step_profile.py > gpurun_out/step_profile.txt 2>&1 ;;
-    sampler) timeout 900 python tools/sampler_cost.py > gpurun_out/sampler.txt 2>&1 ;;
+    variants) for c in c2 c4; do python tools/dfr_variants.py $c > gpurun_out/var_$c.json 2>>gpurun_out/var.err; done ;;
+    hints) for c in c2 c4; do python tools/ab_hints.py $c > gpurun_out/ab_hints_$c.json 2>>gpurun_out/ab_hints.err; done ;;
+    c5_phases) timeout 900 python tools/c5_phases.py > gpurun_out/c5_phases.jsonl 2> gpurun_out/c5_phases.err ;;
+    probe) for c in c3 c4 c2; do timeout 600 python tools/dfr_probe.py $c 0.4 0.5 > gpurun_out/probe_$c.json 2> gpurun_out/probe_$c.err; done ;;
+    *) echo "unknown step $step" ;;
   esac
 done
