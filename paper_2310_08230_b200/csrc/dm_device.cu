@@ -2332,7 +2332,9 @@ static int mma_pass(const dm_flat *f, bool forward, double *lam, double *F, doub
     args.progress = f->progress;
     args.lookahead = f->mma_lookahead;
     args.warm = f->mma_warm;
-    args.hints = env_int("DM_MMA_HINTS", 7);  // A/B (tools/ab_hints.py): bw -1 % at C2, -3 % at C4, fw flat
+    // A/B (tools/ab_hints.py, profiles/r02_mma_c2_full.md): hints 7 = bw -1 % at C2 / -3 % at C4, fw
+    // flat, but +10 % DRAM bytes per launch (4.43 / 4.30 GB vs 4.00 / 3.86): off by default
+    args.hints = env_int("DM_MMA_HINTS", 0);
     args.relax_layer = f->relax_layer;
     args.task_pos = forward ? f->fw_pos : f->bw_pos;
     args.proc_ptr = f->proc_ptr;
