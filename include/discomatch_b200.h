@@ -275,6 +275,42 @@ int dm_dfr_to_nodes(const dm_flat *f, const double *x_il, double *x, void *strea
 int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, double *lam, double delta, double boost,
                      uint64_t seed, int round, int8_t *values, int8_t *agrees, int *disagree, void *stream);
 
+/* --- batched quasi-Newton control of a merged instance (config C5) ----------
+ * A batch of independent instances concatenated block-diagonally into one
+ * flat (paper_2310_08230_b200/batch.py) runs every instance's own L-BFGS
+ * iteration side by side: instance k owns diagrams [bdd_off[k],
+ * bdd_off[k+1]) and dual coordinates [layer_off[k], layer_off[k+1]); its
+ * reductions are taken over its ranges in exactly the order a separate solve
+ * takes them (dm_sum's numpy tree per instance, dm_dot's 4096-chunks counted
+ * from its first coordinate), so every instance's trajectory is bit-identical
+ * to solving it alone.  Vectors that differ per instance (history pairs) are
+ * DEVICE arrays of n pointers to merged-length vectors; per-instance scalars
+ * are device arrays of n doubles; active[k] = 0 skips instance k.
+ *   dm_batch_sum       out[k] = numpy pairwise sum of x over instance k's diagrams
+ *   dm_batch_dot       out[k] = dm_dot order of a[k] . b[k] over its coordinates
+ *   dm_batch_update    mode 0: x = u; 1: x -= (coef*dot)*u, alpha_out = coef*dot
+ *                      (dm_axpy_dev); 2: x = (coef/dot)*x (dm_scale_dev);
+ *                      3: x += u*(alpha - coef*dot) (dm_lbfgs_up);
+ *                      4: x += coef*u (dm_axpy_host)
+ *   dm_batch_curvature s[k] = lam - lam_prev, y[k] = g_prev - g, lam_prev = lam
+ *   dm_batch_step_search  dm_step_search per instance (state: 8 doubles per
+ *                      instance, same layout), trial sweeps on lam + gamma_k*d */
+typedef struct dm_batch dm_batch;
+int dm_batch_create(const dm_flat *f, int n, const int64_t *bdd_off, const int64_t *layer_off, void *stream,
+                    dm_batch **out);
+void dm_batch_destroy(dm_batch *b);
+int dm_batch_sum(const dm_batch *b, const double *x, double *out, void *stream);
+int dm_batch_dot(const dm_batch *b, const double *const *a, const double *const *bb, const int8_t *active,
+                 double *out, void *stream);
+int dm_batch_update(const dm_batch *b, int mode, double *x, const double *const *u, const double *coef,
+                    const double *dot, const double *alpha, double *alpha_out, const int8_t *active, void *stream);
+int dm_batch_curvature(const dm_batch *b, const double *lam, double *lam_prev, const double *g, const double *g_prev,
+                       double *const *s, double *const *y, const int8_t *active, void *stream);
+int dm_batch_step_search(const dm_flat *f, const dm_batch *b, const double *lam, const double *d,
+                         const double *gamma_prev, const double *free_c, const double *min_ascent, double shrink,
+                         double grow, int max_trials, const int8_t *active, double *bounds, double *sums,
+                         double *state, void *stream);
+
 /* --- vectors over dual coordinates / variables ----------------------------- */
 /* dual.py:137-144: lam[l] = costs[var(l)] / count(var(l)); costs indexed by variable */
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream);

@@ -86,6 +86,13 @@ SIGNATURES = {
     "dm_dfr_boundary_average": ([_I, _P, _P, _P, _P, _P, _P, _INT, _P], _INT),
     "dm_dfr_to_nodes": ([_P, _P, _P, _P], _INT),
     "dm_perturb_round": ([_P, _P, _P, _P, _D, _D, ctypes.c_uint64, _INT, _P, _P, _P, _P], _INT),
+    "dm_batch_create": ([_P, _INT, _P, _P, _P, ctypes.POINTER(_P)], _INT),
+    "dm_batch_destroy": ([_P], None),
+    "dm_batch_sum": ([_P, _P, _P, _P], _INT),
+    "dm_batch_dot": ([_P, _P, _P, _P, _P, _P], _INT),
+    "dm_batch_update": ([_P, _INT, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
+    "dm_batch_curvature": ([_P, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
+    "dm_batch_step_search": ([_P, _P, _P, _P, _P, _P, _P, _D, _D, _INT, _P, _P, _P, _P, _P], _INT),
     "dm_init_duals": ([_P, _P, _P, _P], _INT),
     "dm_project_direction": ([_P, _P, _P, _P], _INT),
     "dm_lambda_sums": ([_P, _P, _P, _P], _INT),
@@ -153,7 +160,8 @@ KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_
                   "dm_lbfgs_direction", "dm_k_argmin_from_pass", "dm_curvature_pair", "dm_step_search",
                   "dm_flat_status_to", "dm_dfr_forward", "dm_dfr_backward", "dm_dfr_np_forward", "dm_dfr_np_backward", "dm_dfr_average", "dm_dfr_flush", "dm_dfr_to_nodes",
                   "dm_dfr_average_csr", "dm_dfr_boundary_gather", "dm_dfr_boundary_average",
-                  "dm_perturb_round"}
+                  "dm_perturb_round", "dm_batch_sum", "dm_batch_dot", "dm_batch_update", "dm_batch_curvature",
+                  "dm_batch_step_search"}
 launch_count = 0
 
 

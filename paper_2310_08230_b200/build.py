@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libdiscomatch_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-O3", "-Xcompiler", "-Wno-stringop-overflow"]
-SOURCES = ["dm_host.cpp", "dm_layout.cpp", "dm_device.cu", "dm_sweep.cu", "dm_plan.cu", "dm_deferred.cu"]
+SOURCES = ["dm_host.cpp", "dm_layout.cpp", "dm_device.cu", "dm_sweep.cu", "dm_plan.cu", "dm_deferred.cu", "dm_batch.cu"]
 
 
 def _nvcc() -> str:

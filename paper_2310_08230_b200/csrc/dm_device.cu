@@ -2567,6 +2567,103 @@ int dm_perturb_round(const dm_flat *f, const double *m0, const double *m1, doubl
     return check_stream_error("perturb_round");
 }
 
+// --- batched quasi-Newton control of a merged instance: dm_batch.cu -------
+struct dm_batch {
+    int device = 0;
+    dm::BatchPlan plan;
+    std::vector<void *> allocs;
+};
+
+int dm_batch_create(const dm_flat *f, int n, const int64_t *bdd_off, const int64_t *layer_off, void *stream,
+                    dm_batch **out) {
+    DM_CHECK_FLAT(f);
+    if (n < 1 || !bdd_off || !layer_off || !out || bdd_off[0] != 0 || layer_off[0] != 0 || bdd_off[n] != f->nb ||
+        layer_off[n] != f->L) {
+        dm::set_error("dm_batch_create: offsets must partition the flat's diagrams and layers");
+        return DM_ERR_INVALID;
+    }
+    for (int k = 0; k < n; ++k)
+        if (bdd_off[k + 1] < bdd_off[k] || layer_off[k + 1] < layer_off[k]) {
+            dm::set_error("dm_batch_create: offsets must be non-decreasing");
+            return DM_ERR_INVALID;
+        }
+    auto b = std::make_unique<dm_batch>();
+    b->device = f->device;
+    const int rc = dm::batch_build(bdd_off, layer_off, n, b->plan, b->allocs, stream);
+    if (rc) {
+        for (void *p : b->allocs) cudaFree(p);
+        return rc;
+    }
+    *out = b.release();
+    return DM_OK;
+}
+
+void dm_batch_destroy(dm_batch *b) {
+    if (!b) return;
+    DevGuard guard(b->device);
+    cudaDeviceSynchronize();
+    for (void *p : b->allocs) cudaFreeAsync(p, 0);
+    cudaGetLastError();
+    delete b;
+}
+
+#define DM_CHECK_BATCH(b)                         \
+    if (!(b)) {                                   \
+        dm::set_error("null batch handle");       \
+        return DM_ERR_INVALID;                    \
+    }                                             \
+    DevGuard dm_bguard_((b)->device)
+
+int dm_batch_sum(const dm_batch *b, const double *x, double *out, void *stream) {
+    DM_CHECK_BATCH(b);
+    return dm::batch_sum(b->plan, x, out, stream);
+}
+
+int dm_batch_dot(const dm_batch *b, const double *const *a, const double *const *bb, const int8_t *active,
+                 double *out, void *stream) {
+    DM_CHECK_BATCH(b);
+    return dm::batch_dot(b->plan, a, bb, active, out, stream);
+}
+
+int dm_batch_update(const dm_batch *b, int mode, double *x, const double *const *u, const double *coef,
+                    const double *dot, const double *alpha, double *alpha_out, const int8_t *active, void *stream) {
+    DM_CHECK_BATCH(b);
+    if (mode < dm::kBatchCopy || mode > dm::kBatchAxpyHost) {
+        dm::set_error("dm_batch_update: unknown mode");
+        return DM_ERR_INVALID;
+    }
+    return dm::batch_update(b->plan, mode, x, u, coef, dot, alpha, alpha_out, active, stream);
+}
+
+int dm_batch_curvature(const dm_batch *b, const double *lam, double *lam_prev, const double *g, const double *g_prev,
+                       double *const *s, double *const *y, const int8_t *active, void *stream) {
+    DM_CHECK_BATCH(b);
+    return dm::batch_curvature(b->plan, lam, lam_prev, g, g_prev, s, y, active, stream);
+}
+
+int dm_batch_step_search(const dm_flat *f, const dm_batch *b, const double *lam, const double *d,
+                         const double *gamma_prev, const double *free_c, const double *min_ascent, double shrink,
+                         double grow, int max_trials, const int8_t *active, double *bounds, double *sums,
+                         double *state, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!b || !lam || !d || !gamma_prev || !free_c || !min_ascent || !active || !bounds || !sums || !state ||
+        max_trials < 0) {
+        dm::set_error("dm_batch_step_search: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    int rc;
+    if ((rc = dm::batch_step_init(b->plan, state, gamma_prev, active, stream))) return rc;
+    // every trial is enqueued; stopped searches are evaluated too and ignored by their decision
+    for (int t = 0; t <= max_trials; ++t) {
+        if ((rc = dm::sweep_backward(f->sweep, lam, d, 0.0, nullptr, bounds, stream, state, b->plan.bdd_inst)))
+            return rc;
+        if ((rc = dm::batch_sum(b->plan, bounds, sums, stream))) return rc;
+        if ((rc = dm::batch_decide(b->plan, sums, state, free_c, min_ascent, shrink, grow, max_trials, t, stream)))
+            return rc;
+    }
+    return DM_OK;
+}
+
 int dm_init_duals(const dm_flat *f, const double *costs_by_var, double *lam, void *stream) {
     DM_CHECK_FLAT(f);
     const_cast<dm_flat *>(f)->dec_B = nullptr;  // new duals: recorded decisions are stale

@@ -151,8 +151,9 @@ int device_relax(const int32_t *layer_bdd, const int32_t *bl, const int32_t *lnl
 // kernels.py:95-120 (B may be null: trial evaluation, bounds only; d null: plain duals)
 // ctl (device step search, dm_step_search): gamma read from ctl[0], the
 // launch returns at once when ctl[5] (stop) is set.
+// bdd_inst (batched step search, dm_batch.cu): gamma of diagram j = ctl[8 * bdd_inst[j]]
 int sweep_backward(const SweepDev &s, const double *lam, const double *d, double gamma, double *B,
-                   double *bounds, void *stream, const double *ctl = nullptr);
+                   double *bounds, void *stream, const double *ctl = nullptr, const int32_t *bdd_inst = nullptr);
 // kernels.py:123-159
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream);
 // numpy-order pairwise sum of a device vector into out[0] (dm_device.cu's
@@ -189,5 +190,38 @@ int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, c
                          const int32_t *slot_hi, const double *buf, double *out, bool apply, void *stream);
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
                    const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
+
+// Batched quasi-Newton control of a merged block-diagonal instance
+// (dm_batch.cu): per-instance reduction plans and element -> instance maps.
+enum { kBatchCopy = 0, kBatchAxpyDev = 1, kBatchScaleDev = 2, kBatchLbfgsUp = 3, kBatchAxpyHost = 4 };
+struct BatchPlan {
+    int n = 0;
+    int64_t nb = 0, L = 0;
+    // per-instance numpy pairwise trees over the diagram segments
+    int64_t nleaves = 0, nvals = 0;
+    const int64_t *leaf_off = nullptr;
+    const int32_t *leaf_len = nullptr, *left = nullptr, *right = nullptr, *int_vid = nullptr;
+    const int32_t *hlo = nullptr, *inst_hlo = nullptr, *root = nullptr;
+    double *vals = nullptr;
+    // chunks of the layer segments (4096, aligned at each instance's first layer)
+    int64_t nchunks = 0;
+    const int64_t *chunk_off = nullptr;
+    const int32_t *chunk_len = nullptr, *chunk_inst = nullptr, *inst_chunk_lo = nullptr;
+    const void *tail_plans = nullptr, *tot_plans = nullptr, *full_plan = nullptr;  // SumPlan arrays
+    double *partial = nullptr;
+    const int32_t *bdd_inst = nullptr, *layer_inst = nullptr;
+};
+int batch_build(const int64_t *bdd_off, const int64_t *layer_off, int n, BatchPlan &b, std::vector<void *> &allocs,
+                void *stream);
+int batch_sum(const BatchPlan &b, const double *x, double *out, void *stream);
+int batch_dot(const BatchPlan &b, const double *const *a, const double *const *bb, const int8_t *active, double *out,
+              void *stream);
+int batch_update(const BatchPlan &b, int mode, double *x, const double *const *u, const double *coef,
+                 const double *dot, const double *alpha, double *alpha_out, const int8_t *active, void *stream);
+int batch_curvature(const BatchPlan &b, const double *lam, double *lam_prev, const double *g, const double *g_prev,
+                    double *const *s, double *const *y, const int8_t *active, void *stream);
+int batch_step_init(const BatchPlan &b, double *state, const double *gamma, const int8_t *active, void *stream);
+int batch_decide(const BatchPlan &b, const double *sums, double *state, const double *free_c,
+                 const double *min_ascent, double shrink, double grow, int max_trials, int trial, void *stream);
 
 }  // namespace dm

@@ -28,9 +28,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
                                                                         const double *__restrict__ d, double gamma,
                                                                         double *__restrict__ B,
                                                                         double *__restrict__ bounds,
-                                                                        const double *__restrict__ ctl) {
+                                                                        const double *__restrict__ ctl,
+                                                                        const int32_t *__restrict__ bdd_inst) {
     extern __shared__ double sm[];
-    if (kTrial && ctl) {  // device step search: ctl = dm_step_search state
+    if (kTrial && ctl && !bdd_inst) {  // device step search: ctl = dm_step_search state
         if (ctl[5] != 0.0) return;  // the search already stopped
         gamma = ctl[0];
     }
@@ -38,6 +39,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
     const int32_t j = s.grp_bdd[g * 32 + lane];
+    // batched step search (dm_batch.cu): each diagram's own instance's gamma
+    // (stopped searches are evaluated too and ignored by their decision)
+    if (kTrial && bdd_inst && j >= 0) gamma = ctl[8 * bdd_inst[j]];
     int32_t l0 = 0, nj = 0;
     if (j >= 0) {
         l0 = s.bdd_layer_lo[j];
@@ -193,7 +197,7 @@ int fail(cudaError_t e, const char *what) {
 
 template <int W>
 int launch_backward(const dm::SweepDev &s, const double *lam, const double *d, double gamma, double *B,
-                    double *bounds, cudaStream_t st, const double *ctl) {
+                    double *bounds, cudaStream_t st, const double *ctl, const int32_t *bdd_inst = nullptr) {
     const int blocks = (int)((s.groups * 32 + kSweepThreads - 1) / kSweepThreads);
     const size_t smem = 2 * W * kSweepThreads * sizeof(double);
     if (smem > 48 * 1024) {
@@ -203,13 +207,13 @@ int launch_backward(const dm::SweepDev &s, const double *lam, const double *d, d
         cudaFuncSetAttribute(sweep_backward_kernel<W, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (d && B)
-        sweep_backward_kernel<W, true, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
+        sweep_backward_kernel<W, true, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl, bdd_inst);
     else if (d)
-        sweep_backward_kernel<W, true, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
+        sweep_backward_kernel<W, true, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl, bdd_inst);
     else if (B)
-        sweep_backward_kernel<W, false, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
+        sweep_backward_kernel<W, false, true><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl, bdd_inst);
     else
-        sweep_backward_kernel<W, false, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl);
+        sweep_backward_kernel<W, false, false><<<blocks, kSweepThreads, smem, st>>>(s, lam, d, gamma, B, bounds, ctl, bdd_inst);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DM_OK : fail(e, "sweep_backward");
 }
@@ -230,12 +234,12 @@ int launch_forward(const dm::SweepDev &s, const double *lam, double *F, double *
 namespace dm {
 
 int sweep_backward(const SweepDev &s, const double *lam, const double *d, double gamma, double *B, double *bounds,
-                   void *stream, const double *ctl) {
+                   void *stream, const double *ctl, const int32_t *bdd_inst) {
     if (s.groups == 0) return DM_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    if (s.max_width <= 8) return launch_backward<8>(s, lam, d, gamma, B, bounds, st, ctl);
-    if (s.max_width <= 16) return launch_backward<16>(s, lam, d, gamma, B, bounds, st, ctl);
-    return launch_backward<32>(s, lam, d, gamma, B, bounds, st, ctl);
+    if (s.max_width <= 8) return launch_backward<8>(s, lam, d, gamma, B, bounds, st, ctl, bdd_inst);
+    if (s.max_width <= 16) return launch_backward<16>(s, lam, d, gamma, B, bounds, st, ctl, bdd_inst);
+    return launch_backward<32>(s, lam, d, gamma, B, bounds, st, ctl, bdd_inst);
 }
 
 int sweep_forward(const SweepDev &s, const double *lam, double *F, double *bounds, void *stream) {
@@ -311,92 +315,7 @@ __device__ __forceinline__ double step_update(const StepCoef &c, double xo, doub
     return kMode == kScale ? __dmul_rn(c.r, xi) : xi;
 }
 
-// numpy's pairwise recursion for one length n <= kChunk, planned on the host:
-// the leaves (<= 32 runs of <= 128 elements, left to right) are nodes
-// 0..nleaves-1; the additions are nodes nleaves.. in post-order (the root
-// last), each with its two children and its height above the leaves.
-// Up to 33 leaves for n <= 4096 (e.g. 217 lengths in [3849, 4095]).
-constexpr int kMaxLeaves = 33;
-struct SumPlan {
-    int32_t nleaves, nint, height;
-    uint16_t off[kMaxLeaves];
-    uint8_t len[kMaxLeaves];
-    uint8_t left[kMaxLeaves - 1], right[kMaxLeaves - 1], h[kMaxLeaves - 1];
-};
-
-int plan_rec(SumPlan &p, int off, int len, int &height, std::vector<int> &post) {
-    if (len <= 128) {
-        p.off[p.nleaves] = (uint16_t)off;
-        p.len[p.nleaves] = (uint8_t)len;
-        height = 0;
-        return p.nleaves++;
-    }
-    int n2 = len / 2;
-    n2 -= n2 % 8;
-    int hl, hr;
-    const int l = plan_rec(p, off, n2, hl, post);
-    const int r = plan_rec(p, off + n2, len - n2, hr, post);
-    height = 1 + (hl > hr ? hl : hr);
-    post.push_back(l);
-    post.push_back(r);
-    post.push_back(height);
-    return -(int)(post.size() / 3);  // internal node k (1-based) as -k
-}
-
-SumPlan make_sum_plan(int n) {
-    SumPlan p{};
-    if (n <= 0) return p;
-    std::vector<int> post;
-    int height;
-    plan_rec(p, 0, n, height, post);
-    p.nint = (int)post.size() / 3;
-    p.height = height;
-    auto id = [&](int v) { return v >= 0 ? v : p.nleaves + (-v - 1); };
-    for (int k = 0; k < p.nint; ++k) {
-        p.left[k] = (uint8_t)id(post[3 * k]);
-        p.right[k] = (uint8_t)id(post[3 * k + 1]);
-        p.h[k] = (uint8_t)post[3 * k + 2];
-    }
-    return p;
-}
-
-// 0.0 + numpy pairwise_sum(sm[0:n]) of shared-memory values, by a block of
-// any multiple of 32 threads: one octet per leaf (numpy's 8 accumulators),
-// then warp 0 adds the tree level by level.  Result on thread 0.
-__device__ double smem_pairwise(const double *sm, const SumPlan &p) {
-    __shared__ double node[2 * kMaxLeaves];
-    const int q = threadIdx.x & 7;
-    // octets in passes of blockDim/8 (uniform trip count: whole warps shuffle)
-    for (int base = 0; base < p.nleaves; base += (int)(blockDim.x >> 3)) {
-        const int oct = base + (int)(threadIdx.x >> 3);
-        const bool live = oct < p.nleaves;
-        const int off = live ? p.off[oct] : 0, len = live ? p.len[oct] : 0;
-        const int stop = len - (len % 8);
-        double r = 0.0;
-        if (len >= 8) {
-            r = sm[off + q];
-            for (int i = 8; i < stop; i += 8) r = __dadd_rn(r, sm[off + i + q]);
-        }
-#pragma unroll
-        for (int w = 1; w < 8; w <<= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, w));  // a+b == b+a exactly
-        if (live && q == 0) {
-            double res = len < 8 ? 0.0 : r;
-            for (int i = len < 8 ? 0 : stop; i < len; ++i) res = __dadd_rn(res, sm[off + i]);
-            node[oct] = res;
-        }
-    }
-    __syncthreads();
-    double total = 0.0;
-    if (threadIdx.x < 32 && p.nleaves > 0) {
-        const int k = threadIdx.x;  // internal nodes: at most 32, one per lane
-        for (int h = 1; h <= p.height; ++h) {
-            if (k < p.nint && p.h[k] == h) node[p.nleaves + k] = __dadd_rn(node[p.left[k]], node[p.right[k]]);
-            __syncwarp();
-        }
-        total = __dadd_rn(0.0, node[p.nleaves + p.nint - 1]);
-    }
-    return total;
-}
+#include "dm_reduce.cuh"
 
 struct FinishPlans {
     SumPlan chunk, tail, totals;

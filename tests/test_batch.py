@@ -100,3 +100,24 @@ def test_gpu_merged_hybrid_converges_to_every_instance_bound(schedule):
     for k, inst in enumerate(insts):
         one = qn.solve(inst, SolveConfig(mode="hybrid", max_iterations=1000), device="cuda:0")
         assert abs(res.bounds[k] - one.best_bound) <= 1e-5 * abs(one.best_bound), (k, res.bounds[k], one.best_bound)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("schedule", ["exact", "deferred"])
+def test_gpu_batched_hybrid_equals_separate_solves(schedule):
+    """BatchedSolver: every instance's own hybrid solve on one merged instance —
+    records, stopping and duals bit for bit against qn.solve of each."""
+    from bench import build_instance
+    from paper_2310_08230_b200 import qn
+    from paper_2310_08230_b200.batch import solve_batched
+
+    insts = [build_instance("c3", s) for s in (0, 3, 5, 8)]
+    cfg = SolveConfig(mode="hybrid", mma_schedule=schedule, max_iterations=60)
+    got = solve_batched(insts, cfg, device="cuda:0")
+    for k, inst in enumerate(insts):
+        one = qn.solve(inst, cfg, device="cuda:0")
+        assert got[k].bounds == one.bounds, k
+        assert [r.kind for r in got[k].records] == [r.kind for r in one.records], k
+        assert got[k].stop_reason == one.stop_reason and got[k].iterations == one.iterations
+        assert got[k].best_bound == one.best_bound
+        assert got[k].lam.tobytes() == one.state.lam.tobytes(), k
