@@ -352,11 +352,14 @@ class BatchedSolver:
                 from . import _native
                 from .kernels import _stream
 
+                # (the argument tensors are bound to names: a temporary's block could be
+                # reused by the next temporary before the kernels read it)
+                gamma_d = torch.as_tensor(gamma, **f64)
+                ascent_d = torch.as_tensor(min_ascent, **f64)
                 _native.call("dm_batch_step_search", st.dev.handle, self.h._h, st.lam_d.data_ptr(), d.data_ptr(),
-                             torch.as_tensor(gamma, **f64).data_ptr(), free_c_d.data_ptr(),
-                             torch.as_tensor(min_ascent, **f64).data_ptr(), float(scfg.shrink), float(scfg.grow),
-                             int(scfg.max_trials), active.data_ptr(), nb_scratch.data_ptr(), sums.data_ptr(),
-                             state_d.data_ptr(), _stream(dev))
+                             gamma_d.data_ptr(), free_c_d.data_ptr(), ascent_d.data_ptr(), float(scfg.shrink),
+                             float(scfg.grow), int(scfg.max_trials), active.data_ptr(), nb_scratch.data_ptr(),
+                             sums.data_ptr(), state_d.data_ptr(), _stream(dev))
                 ctl = state_d.cpu().numpy().reshape(n, 8)
                 st.sweeps += int(ctl[qn_on, 6].max()) if qn_on.any() else 0
                 for k in np.flatnonzero(qn_on):
@@ -404,8 +407,7 @@ class BatchedSolver:
                     rings[k].insert(0, (slot, 1.0 / sy[k], float(sy[k])))
                     if len(rings[k]) > m:
                         free_slots[k].append(rings[k].pop()[0])
-                prev = records[k][-2].dual_objective
-                if bound[k] - prev < cfg.dual_tolerance * max(1.0, abs(bound[k])):
+                if self._tolerance_met(records[k], bound[k], it, cfg):
                     stop_reason[k] = "dual_tolerance"
                 elif cfg.max_seconds is not None and t > cfg.max_seconds:
                     stop_reason[k] = "max_seconds"
@@ -422,6 +424,19 @@ class BatchedSolver:
             lam_final[k] = st.lam_d[lo:hi].cpu().numpy()
         return [BatchedResult(records[k], float(best[k]), int(iters[k]), stop_reason[k], lam_final[k])
                 for k in range(n)]
+
+    @staticmethod
+    def _tolerance_met(recs, bound, it, cfg) -> bool:
+        """DualSolver.step's dual-tolerance rule (one iteration's gain, or the
+        best bound over the stall window for the deferred schedule)."""
+        k = cfg.effective_stall_window
+        if k == 1:
+            return bound - recs[-2].dual_objective < cfg.dual_tolerance * max(1.0, abs(bound))
+        if it < k:
+            return False
+        recent = max(r.dual_objective for r in recs[-k:])
+        before = max(r.dual_objective for r in recs[:-k])
+        return recent - before < cfg.dual_tolerance * max(1.0, abs(bound))
 
     def _call_curv(self, lam, lam_prev, g, g_prev, s_p, y_p, act):
         self._call("dm_batch_curvature", lam.data_ptr(), lam_prev.data_ptr(), g.data_ptr(), g_prev.data_ptr(),
