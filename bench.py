@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="headline only: no other-schedule / C4 / C5 keys")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--split", action="store_true", help="one instance's diagrams partitioned over the ranks (C4)")
+    ap.add_argument("--c5-solver", choices=["hybrid", "averaging"], default="hybrid",
+                    help="--config c5: every instance's own hybrid solve (batch.BatchedSolver) or fixed-length "
+                         "averaging-only merged batches")
     ap.add_argument("--cpu-budget", type=float, default=300.0, help="wall budget (s) of a CPU time-to-gap run")
     ap.add_argument("--batch", type=int, default=0, help="also time K independent instances via qn.solve_batch")
     ap.add_argument("--batch-iters", type=int, default=30)
@@ -675,6 +678,26 @@ def c5_solve(insts, dev, schedule):
     return time.perf_counter() - t, res
 
 
+def c5_batched(insts, dev, schedule="exact"):
+    """One C5 step, hybrid: every instance's OWN qn.solve (default config, the
+    reference's stopping rule) side by side on one merged instance
+    (batch.BatchedSolver: per-instance L-BFGS, step search and stopping;
+    stopped instances compacted away) — bounds and duals bit-identical to
+    separate solves.  Merge, upload, plans, the solves and the per-instance
+    duals read back all inside the clock.  Returns (seconds, results, solver)."""
+    import torch
+
+    from paper_2310_08230_b200.batch import BatchedSolver
+    from paper_2310_08230_b200.config import SolveConfig
+
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    solver = BatchedSolver(insts, SolveConfig(mode="hybrid", mma_schedule=schedule), device=dev, reuse_buffers=True)
+    res = solver.solve()
+    torch.cuda.synchronize()
+    return time.perf_counter() - t, res, solver
+
+
 C5_ITERATIONS = {"exact": 25, "deferred": 100}
 
 
@@ -701,16 +724,46 @@ def c5_summary(args, dev, reps=5):
     insts = c5_instances(range(args.seed, args.seed + C5_INSTANCES))
     out = {"workload": f"c5: {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}, solved as ONE merged "
                        "block-diagonal instance (batch.py) from the lowered host tables: merge, upload, plans, "
-                       "averaging-only solve of a fixed length (per-instance duals bit-identical to separate solves of that "
-                       "length) and per-instance bounds inside the clock; quality = each instance's relative gap to "
-                       "its separate converged hybrid solve"}
+                       "solve and per-instance bounds inside the clock. 'hybrid': every instance's own hybrid solve "
+                       "to the reference's stopping rule (BatchedSolver); 'exact'/'deferred': averaging-only solves "
+                       "of a fixed length (per-instance duals bit-identical to separate solves of that length), "
+                       "quality = each instance's relative gap to its separate converged hybrid solve"}
     import gc
 
     import torch
 
     from paper_2310_08230_b200.config import SolveConfig
 
-    sep = [solve(i, SolveConfig(mode="hybrid"), device=dev).best_bound for i in insts]
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    sep_bounds = []
+    for i in insts:
+        r = solve(i, SolveConfig(mode="hybrid"), device=dev)
+        sep_bounds.append(r.bounds)
+        del r
+    torch.cuda.synchronize()
+    t_sep = time.perf_counter() - t
+    sep = [max(b) for b in sep_bounds]
+    c5_batched(insts, dev)  # warm-up
+    times = []
+    res = None
+    for _ in range(reps):
+        del res
+        gc.collect()
+        torch.cuda.synchronize()
+        sec, res, solver = c5_batched(insts, dev)
+        times.append(sec)
+    med = float(np.median(times))
+    out["hybrid"] = {"workload": "every instance's own hybrid qn.solve (default SolveConfig, the reference's stopping "
+                                 "rule) on one merged instance with per-instance L-BFGS / step search / stopping, "
+                                 "stopped instances compacted away (batch.BatchedSolver), from host tables",
+                     "instances_per_s": C5_INSTANCES / med, "seconds": med, "runs_s": times,
+                     "spread": (max(times) - min(times)) / med,
+                     "iterations_max": max(r.iterations for r in res),
+                     "iterations_sum": int(sum(r.iterations for r in res)),
+                     "compactions": solver.repacks,
+                     "bit_identical_to_separate_solves": all(r.bounds == b for r, b in zip(res, sep_bounds)),
+                     "separate_solves_one_after_another_s": t_sep}
     for schedule in ("exact", "deferred"):
         c5_solve(insts, dev, schedule)  # warm-up
         times = []
@@ -874,8 +927,10 @@ def run_c5(args, rank, world, local_rank):
     seeds r, r+N, ...; no collective on the data path).  One step = the
     rank's share of the batch merged into one block-diagonal instance
     (batch.py) and solved from the lowered HOST tables (merge, device upload
-    and every plan build included) to the reference's stopping rule with the
-    --schedule averaging schedule; warm-up = W such solves."""
+    and every plan build included): by default every instance's own hybrid
+    solve to the reference's stopping rule (--c5-solver hybrid,
+    BatchedSolver), else fixed-length averaging-only batches; --schedule
+    picks the averaging schedule; warm-up = W such solves."""
     import torch
 
     from paper_2310_08230_b200 import _native
@@ -889,8 +944,17 @@ def run_c5(args, rank, world, local_rank):
               + i.costs.nbytes for i in insts)
     with ClockSampler(local_rank) as clk:
         time.sleep(1.0)
+        hybrid = args.c5_solver == "hybrid"
+
+        def step():
+            if hybrid:
+                _, _, solver = c5_batched(insts, dev, args.schedule)
+                return solver.arc_updates
+            _, res = c5_solve(insts, dev, args.schedule)
+            return res.merged.state.arc_updates
+
         for _ in range(args.warmup):
-            c5_solve(insts, dev, args.schedule)
+            step()
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -901,8 +965,7 @@ def run_c5(args, rank, world, local_rank):
         start.record()
         arcs = 0
         for _ in range(args.steps):
-            _, res = c5_solve(insts, dev, args.schedule)
-            arcs += res.merged.state.arc_updates
+            arcs += step()
         end.record()
         torch.cuda.synchronize()
         clk.mark()
@@ -920,8 +983,11 @@ def run_c5(args, rank, world, local_rank):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "instances_per_s": n_inst / (max_ms / 1e3),
         "config": {"workload": f"c5: batch of {C5_INSTANCES} independent pairs, each {WORKLOADS['c3']}; "
-                               f"merged per GPU and solved from host arrays to the stopping rule ({args.schedule} "
-                               "schedule)",
+                               "merged per GPU and solved from host arrays: "
+                               + ("every instance's own hybrid solve to the reference's stopping rule "
+                                  "(BatchedSolver, bit-identical to separate solves)" if hybrid else
+                                  f"averaging-only, {C5_ITERATIONS[args.schedule]} iterations")
+                               + f" ({args.schedule} schedule)",
                    "parallelism": f"instance-sharded x{world} ({len(insts)} on rank 0), merged into one instance per GPU",
                    "l2": "each solve uploads its instance (inputs not L2-resident across steps)"},
         "gpu_launches": _native.launch_count - l0,

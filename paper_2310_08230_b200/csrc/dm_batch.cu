@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dm_internal.h"
@@ -254,9 +255,17 @@ int batch_build(const int64_t *bdd_off, const int64_t *layer_off, int n, BatchPl
     // per-instance pairwise trees over the diagram segments, one value space:
     // [every leaf ..., every internal node ...]
     std::vector<PairwisePlan> plans(n);
+    {  // the instances' trees are independent: built by a few host threads
+        const int nt = std::max(1, std::min(n, 8));
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                for (int k = t; k < n; k += nt) plans[k] = plan_pairwise(bdd_off[k + 1] - bdd_off[k]);
+            });
+        for (auto &x : th) x.join();
+    }
     int64_t NL = 0, NI = 0;
     for (int k = 0; k < n; ++k) {
-        plans[k] = plan_pairwise(bdd_off[k + 1] - bdd_off[k]);
         NL += (int64_t)plans[k].leaf_off.size();
         NI += (int64_t)plans[k].left.size();
     }
