@@ -39,6 +39,7 @@
 #include <string>
 
 #include "dm_internal.h"
+#include "dm_rows.cuh"
 
 #define DM_INF __longlong_as_double(0x7ff0000000000000LL)
 
@@ -63,6 +64,15 @@ __device__ __forceinline__ double c_zero(int32_t a, double fv, const double *nb)
 }
 __device__ __forceinline__ double c_one(int32_t b, double fl, const double *nb) {  // fl = fv + lam
     return b == dm::kTrue ? fl : (b == dm::kFalse ? DM_INF : __dadd_rn(fl, nb[b * kThreads]));
+}
+
+template <class R>
+__device__ __forceinline__ double c_zero(int32_t a, double fv, const R &nb) {
+    return a == dm::kTrue ? fv : (a == dm::kFalse ? DM_INF : __dadd_rn(fv, nb.get(a)));
+}
+template <class R>
+__device__ __forceinline__ double c_one(int32_t b, double fl, const R &nb) {  // fl = fv + lam
+    return b == dm::kTrue ? fl : (b == dm::kFalse ? DM_INF : __dadd_rn(fl, nb.get(b)));
 }
 
 // the dual update of one copy (see the header); returns lam'
@@ -93,6 +103,11 @@ constexpr int kAhead = 3;
 #define DM_DFR_WARM 0
 #endif
 constexpr bool kWarm = DM_DFR_WARM != 0;  // L2 warm-up of later positions (A/B: slower in the MM passes)
+#ifndef DM_DFR_WARM_NARROW
+#define DM_DFR_WARM_NARROW 0
+#endif
+// (A/B at C4: warming L2 in the narrow bodies only is slower too, 141 vs 118 us)
+constexpr int kWarmNarrow = DM_DFR_WARM_NARROW;
 constexpr int kWarps = kThreads / 32;
 
 struct Meta {
@@ -141,9 +156,11 @@ __device__ __forceinline__ double dfr_update_v(double lam_l, double a_l, double 
 }
 
 // Backward direction: positions k = 0 (every lane's last layer) .. K-1.
-template <int W, bool kMM, bool kAvg, bool kDec>
-__global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
-    extern __shared__ double sm[];
+// W: node slots the loops cover (>= the group's widest layer), WS: the slot
+// stride of the shared distance rows (the launch's width).
+template <int W, int WS, bool kMM, bool kAvg, bool kDec>
+__device__ __forceinline__ void dfr_backward_body(const DfrArgs &a, int64_t g, double *sm, int32_t *meta_w,
+                                                  int64_t *meta_s) {
     const dm::SweepDev &s = a.s;
     double *__restrict__ lamp = a.lam;
     const double *__restrict__ avgp = a.avg;
@@ -153,8 +170,6 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
     double *__restrict__ boundsp = a.bounds;
     uint64_t *__restrict__ decp = a.dec;
     const int lane = threadIdx.x & 31;
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= s.groups) return;
     const int32_t j = s.grp_bdd[g * 32 + lane];
     int32_t l0 = 0, nj = 0;
     if (j >= 0) {
@@ -163,17 +178,22 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    double *nb = sm + threadIdx.x;                  // distances of position k-1 (next layer)
-    double *cur = sm + W * kThreads + threadIdx.x;  // position k
+    constexpr bool kReg = W <= kRegRows;
+    Row<W, kReg, kThreads> nb, cur;  // distances of position k-1 (next layer) and of position k
+    if constexpr (kReg) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) nb.put(u, DM_INF), cur.put(u, DM_INF);
+    } else {
+        nb.p = sm + threadIdx.x;
+        cur.p = sm + WS * kThreads + threadIdx.x;
+    }
     // register double buffer: position k+1's arcs, F row and duals load while k computes
     int32_t za[W], oa[W];
     double fa[W];
     double lam_n = 0.0, avg_n = 0.0;
     int32_t w_n = 0;
     int64_t slot_n = 0;
-    __shared__ int32_t meta_w[kWarps][kMetaWin];
-    __shared__ int64_t meta_s[kWarps][kMetaWin];
-    Meta meta{meta_w[threadIdx.x >> 5], meta_s[threadIdx.x >> 5], 0};
+    Meta meta{meta_w, meta_s, 0};
     meta_window(meta, s, p0, K, 0, lane);
     auto fetch = [&](int32_t k) {
         w_n = meta.w[k - meta.lo];
@@ -198,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
         if (k + 1 + kAhead >= meta.lo + kMetaWin && meta.lo + kMetaWin < K) meta_window(meta, s, p0, K, k, lane);
         {
             const int32_t kp = k + 1 + kAhead;
-            if (kWarm && kp < K) {
+            if ((kWarm || W <= kWarmNarrow) && kp < K) {
                 const int32_t wp = meta.w[kp - meta.lo];
                 const int64_t sp = meta.slot[kp - meta.lo];
                 warm_rows<W>(s, lane, wp, sp, kMM ? inp : nullptr, wp, sp);
@@ -245,12 +265,12 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
         for (int i = 0; i < W; ++i)
             if (i < w) {
                 const int32_t za_ = z[i], ob = o[i];
-                const double c0 = za_ == dm::kTrue ? 0.0 : (za_ == dm::kFalse ? DM_INF : nb[za_ * kThreads]);
+                const double c0 = za_ == dm::kTrue ? 0.0 : (za_ == dm::kFalse ? DM_INF : nb.get(za_));
                 const double c1 =
-                    ob == dm::kTrue ? lam_l : (ob == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[ob * kThreads]));
+                    ob == dm::kTrue ? lam_l : (ob == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb.get(ob)));
                 const bool zero_wins = c0 <= c1;
                 const double v = zero_wins ? c0 : c1;
-                cur[i * kThreads] = v;
+                cur.put(i, v);
                 outp[(slot + i) * 32 + lane] = v;
                 if (kDec && W <= 8) {
                     const int32_t t = zero_wins ? za_ : ob;
@@ -258,18 +278,37 @@ __global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
                 }
             }
         if (kDec && W <= 8 && act) decp[l] = word;
-        double *t = nb;
-        nb = cur;
-        cur = t;
-        if (act && k == nj - 1) boundsp[j] = nb[0];  // root layer: single node
+        swap_rows(nb, cur);
+        if (act && k == nj - 1) boundsp[j] = nb.at(0);  // root layer: single node
     }
+}
+
+// The group's widest layer picks the narrowest unrolled body (bit-identical:
+// slots past a position's width are never touched): the long chains of a
+// split instance are two nodes wide, and a warp walking them runs a quarter
+// of the W = 8 instructions per position.
+template <int W, bool kMM, bool kAvg, bool kDec>
+__global__ void __launch_bounds__(kThreads) dfr_backward_kernel(DfrArgs a) {
+    extern __shared__ double sm[];
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= a.s.groups) return;
+    const int wid = threadIdx.x >> 5;
+    const int gw = a.s.grp_width ? a.s.grp_width[g] : W;
+    if (W > 2 && gw <= 2)
+        dfr_backward_body<2, W, kMM, kAvg, kDec>(a, g, sm, meta_w[wid], meta_s[wid]);
+    else if (W > 4 && gw <= 4)
+        dfr_backward_body<4, W, kMM, kAvg, kDec>(a, g, sm, meta_w[wid], meta_s[wid]);
+    else
+        dfr_backward_body<W, W, kMM, kAvg, kDec>(a, g, sm, meta_w[wid], meta_s[wid]);
 }
 
 // Forward direction: positions k = K-1 .. 0; lanes whose diagram is shorter
 // than the group's longest idle until their root position.
-template <int W, bool kMM, bool kAvg>
-__global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
-    extern __shared__ double sm[];
+template <int W, int WS, bool kMM, bool kAvg>
+__device__ __forceinline__ void dfr_forward_body(const DfrArgs &a, int64_t g, double *sm, int32_t *meta_w,
+                                                 int64_t *meta_s) {
     const dm::SweepDev &s = a.s;
     double *__restrict__ lamp = a.lam;
     const double *__restrict__ avgp = a.avg;
@@ -279,8 +318,6 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     double *__restrict__ boundsp = a.bounds;
     uint64_t *__restrict__ decp = a.dec;
     const int lane = threadIdx.x & 31;
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= s.groups) return;
     const int32_t j = s.grp_bdd[g * 32 + lane];
     int32_t l0 = 0, nj = 0;
     if (j >= 0) {
@@ -289,9 +326,17 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    double *cur = sm + threadIdx.x;                  // distances from the root, position k
-    double *nxt = sm + W * kThreads + threadIdx.x;   // position k-1
-    double *bn = sm + 2 * W * kThreads + threadIdx.x;  // B of position k-1 (kMM)
+    constexpr bool kReg = W <= kRegRows;
+    // distances from the root at position k and k-1, B of position k-1 (kMM)
+    Row<W, kReg, kThreads> cur, nxt, bn;
+    if constexpr (kReg) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) cur.put(u, DM_INF), nxt.put(u, DM_INF), bn.put(u, DM_INF);
+    } else {
+        cur.p = sm + threadIdx.x;
+        nxt.p = sm + WS * kThreads + threadIdx.x;
+        bn.p = sm + 2 * WS * kThreads + threadIdx.x;
+    }
     double tb = DM_INF;
     // register double buffer for position k-1
     int32_t za[W], oa[W];
@@ -299,9 +344,7 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
     double lam_n = 0.0, avg_n = 0.0;
     int32_t w_n = 0, wb_n = 0;
     int64_t slot_n = 0;
-    __shared__ int32_t meta_w[kWarps][kMetaWin];
-    __shared__ int64_t meta_s[kWarps][kMetaWin];
-    Meta meta{meta_w[threadIdx.x >> 5], meta_s[threadIdx.x >> 5], 0};
+    Meta meta{meta_w, meta_s, 0};
     meta_window(meta, s, p0, K, K > kMetaWin ? K - kMetaWin : 0, lane);
     auto fetch = [&](int32_t k) {  // k < nj
         w_n = meta.w[k - meta.lo];
@@ -337,7 +380,7 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         window_for(k);
         {
             const int32_t kp = k - 1 - kAhead;  // warm L2 for position kp (and the table rows of kp - 1)
-            if (kWarm && kp >= 0 && kp < nj) {
+            if ((kWarm || W <= kWarmNarrow) && kp >= 0 && kp < nj) {
                 const int32_t wp = meta.w[kp - meta.lo];
                 const int64_t sp = meta.slot[kp - meta.lo];
                 const int32_t wt = kp > 0 ? meta.w[kp - 1 - meta.lo] : 0;
@@ -360,26 +403,26 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         if (kMM) {
 #pragma unroll
             for (int u = 0; u < W; ++u)
-                if (u < wb_n) bn[u * kThreads] = ba[u];
+                if (u < wb_n) bn.put(u, ba[u]);
         }
         double lam_l = lam_n;
         const double a_l = avg_n;
         if (k > 0) fetch(k - 1);
         const int32_t l = l0 + nj - 1 - k;
         if (k == nj - 1) {  // root layer: F[root] = 0 (kernels.py:187-193)
-            cur[0] = 0.0;
+            cur.put(0, 0.0);
 #pragma unroll
-            for (int i = 1; i < W; ++i) cur[i * kThreads] = DM_INF;
+            for (int i = 1; i < W; ++i) cur.put(i, DM_INF);
         }
 #pragma unroll
         for (int i = 0; i < W; ++i)
-            if (i < w) outp[(slot + i) * 32 + lane] = cur[i * kThreads];
+            if (i < w) outp[(slot + i) * 32 + lane] = cur.at(i);
         if (kMM) {
             double m0 = DM_INF, m1 = DM_INF;
 #pragma unroll
             for (int i = 0; i < W; ++i)
                 if (i < w) {
-                    const double fv = cur[i * kThreads];
+                    const double fv = cur.at(i);
                     const double c0 = c_zero(z[i], fv, bn);
                     const double c1 = c_one(o[i], __dadd_rn(fv, lam_l), bn);
                     if (c0 < m0) m0 = c0;
@@ -394,30 +437,45 @@ __global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
         // push this layer's distances into the next one (kernels.py:241-269)
 #pragma unroll
         for (int u = 0; u < W; ++u)
-            if (u < wn) nxt[u * kThreads] = DM_INF;
+            if (u < wn) nxt.put(u, DM_INF);
 #pragma unroll
         for (int i = 0; i < W; ++i)
             if (i < w) {
-                const double fv = cur[i * kThreads];
+                const double fv = cur.at(i);
                 if (fv == DM_INF) continue;
                 const int32_t za_ = z[i], ob = o[i];
                 if (za_ >= 0) {
-                    if (fv < nxt[za_ * kThreads]) nxt[za_ * kThreads] = fv;
+                    if (fv < nxt.get(za_)) nxt.put_dyn(za_, fv);
                 } else if (za_ == dm::kTrue) {
                     if (fv < tb) tb = fv;
                 }
                 const double c = __dadd_rn(fv, lam_l);
                 if (ob >= 0) {
-                    if (c < nxt[ob * kThreads]) nxt[ob * kThreads] = c;
+                    if (c < nxt.get(ob)) nxt.put_dyn(ob, c);
                 } else if (ob == dm::kTrue) {
                     if (c < tb) tb = c;
                 }
             }
-        double *t = cur;
-        cur = nxt;
-        nxt = t;
+        swap_rows(cur, nxt);
     }
     if (j >= 0) boundsp[j] = tb;
+}
+
+template <int W, bool kMM, bool kAvg>
+__global__ void __launch_bounds__(kThreads) dfr_forward_kernel(DfrArgs a) {
+    extern __shared__ double sm[];
+    __shared__ int32_t meta_w[kWarps][kMetaWin];
+    __shared__ int64_t meta_s[kWarps][kMetaWin];
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= a.s.groups) return;
+    const int wid = threadIdx.x >> 5;
+    const int gw = a.s.grp_width ? a.s.grp_width[g] : W;
+    if (W > 2 && gw <= 2)
+        dfr_forward_body<2, W, kMM, kAvg>(a, g, sm, meta_w[wid], meta_s[wid]);
+    else if (W > 4 && gw <= 4)
+        dfr_forward_body<4, W, kMM, kAvg>(a, g, sm, meta_w[wid], meta_s[wid]);
+    else
+        dfr_forward_body<W, W, kMM, kAvg>(a, g, sm, meta_w[wid], meta_s[wid]);
 }
 
 // ---------------------------------------------------------------------------

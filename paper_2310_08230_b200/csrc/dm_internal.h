@@ -134,6 +134,7 @@ struct SweepDev {
     int64_t groups = 0, slots = 0;  // slots * 32 = elements of an interleaved table
     int32_t max_width = 0;
     const int32_t *grp_bdd = nullptr, *grp_npos = nullptr, *pos_width = nullptr;
+    const int32_t *grp_width = nullptr;  // widest layer of each group (null: max_width)
     const int64_t *grp_pos_lo = nullptr, *pos_slot = nullptr;
     const int32_t *zl = nullptr, *ol = nullptr;
     const int32_t *bdd_layer_lo = nullptr, *lnl = nullptr;

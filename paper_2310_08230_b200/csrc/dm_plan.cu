@@ -191,19 +191,22 @@ __global__ void sweep_total_kernel(const int32_t *cnt, const int64_t *excl, int6
 // widest layer at each position of each group (warp per group)
 __global__ void sweep_widths_kernel(const int32_t *bl, const int32_t *lnl, const int32_t *grp_bdd,
                                     const int32_t *grp_npos, const int64_t *grp_pos_lo, int64_t groups,
-                                    int32_t *pos_width, unsigned long long *max_width) {
+                                    int32_t *pos_width, int32_t *grp_width, unsigned long long *max_width) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     unsigned wmax = 0;
     for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < groups; g += warps) {
         const int32_t j = grp_bdd[g * 32 + lane], K = grp_npos[g];
         const int32_t nl = j >= 0 ? bl[j + 1] - bl[j] : 0, top = j >= 0 ? bl[j + 1] - 1 : 0;
+        unsigned gmax = 0;
         for (int32_t k = 0; k < K; ++k) {
             const unsigned w = k < nl ? (unsigned)(lnl[top - k + 1] - lnl[top - k]) : 0u;
             const unsigned m = __reduce_max_sync(kFull, w);
             if (lane == 0) pos_width[grp_pos_lo[g] + k] = (int32_t)m;
-            wmax = max(wmax, m);
+            gmax = max(gmax, m);
         }
+        if (lane == 0) grp_width[g] = (int32_t)gmax;
+        wmax = max(wmax, gmax);
     }
     if (lane == 0 && wmax) atomicMax(max_width, (unsigned long long)wmax);
 }
@@ -420,6 +423,7 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
     if (nb == 0) return 0;
     uint64_t *key = nullptr, *key2 = nullptr;
     int32_t *idx = nullptr, *idx2 = nullptr, *grp_bdd = nullptr, *grp_npos = nullptr, *pos_width = nullptr;
+    int32_t *grp_width = nullptr;
     int64_t *grp_pos_lo = nullptr, *pos_slot = nullptr, *stats = nullptr;
     int32_t *zl = nullptr, *ol = nullptr;
     void *tmp = nullptr;
@@ -434,7 +438,8 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
     if ((e = dalloc(&key, nb, s, scratch, scratch_bytes)) || (e = dalloc(&key2, nb, s, scratch, scratch_bytes)) ||
         (e = dalloc(&idx, nb, s, scratch, scratch_bytes)) || (e = dalloc(&idx2, nb, s, scratch, scratch_bytes)) ||
         (e = dalloc(&stats, 4, s, scratch, scratch_bytes)) || (e = dalloc(&grp_bdd, groups * 32, s, allocs, bytes)) ||
-        (e = dalloc(&grp_npos, groups, s, allocs, bytes)) || (e = dalloc(&grp_pos_lo, groups + 1, s, allocs, bytes)))
+        (e = dalloc(&grp_npos, groups, s, allocs, bytes)) || (e = dalloc(&grp_width, groups, s, allocs, bytes)) ||
+        (e = dalloc(&grp_pos_lo, groups + 1, s, allocs, bytes)))
         return fail(e, "allocation");
     auto release = [&] {
         for (void *p : scratch) cudaFreeAsync(p, s);
@@ -469,7 +474,7 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
             (e = dalloc(&pos_slot, npos_total, s, allocs, bytes)))
             break;
         sweep_widths_kernel<<<grid_for(groups * 32, 256), 256, 0, s>>>(bl, lnl, grp_bdd, grp_npos, grp_pos_lo, groups,
-                                                                       pos_width,
+                                                                       pos_width, grp_width,
                                                                        (unsigned long long *)stats + 1);
         if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan2, pos_width, pos_slot, (int)npos_total, s))) break;
         if (tmp_scan2 > tmp_bytes) {
@@ -500,6 +505,7 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
     if (e) return fail(e, "build");
     sd.grp_bdd = grp_bdd;
     sd.grp_npos = grp_npos;
+    sd.grp_width = grp_width;
     sd.grp_pos_lo = grp_pos_lo;
     sd.pos_width = pos_width;
     sd.pos_slot = pos_slot;

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "dm_internal.h"
+#include "dm_rows.cuh"
 
 #define DM_INF __longlong_as_double(0x7ff0000000000000LL)
 
@@ -23,21 +24,15 @@ namespace {
 
 constexpr int kSweepThreads = 128;
 
-template <int W, bool kTrial, bool kStore>
-__global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::SweepDev s, const double *__restrict__ lam,
-                                                                        const double *__restrict__ d, double gamma,
-                                                                        double *__restrict__ B,
-                                                                        double *__restrict__ bounds,
-                                                                        const double *__restrict__ ctl,
-                                                                        const int32_t *__restrict__ bdd_inst) {
-    extern __shared__ double sm[];
-    if (kTrial && ctl && !bdd_inst) {  // device step search: ctl = dm_step_search state
-        if (ctl[5] != 0.0) return;  // the search already stopped
-        gamma = ctl[0];
-    }
+// W: node slots the loops cover (>= the group's widest layer), WS: the slot
+// stride of the shared distance rows (the launch's width)
+template <int W, int WS, bool kTrial, bool kStore>
+__device__ __forceinline__ void sweep_backward_body(const dm::SweepDev &s, const double *__restrict__ lam,
+                                                    const double *__restrict__ d, double gamma,
+                                                    double *__restrict__ B, double *__restrict__ bounds,
+                                                    const double *__restrict__ ctl,
+                                                    const int32_t *__restrict__ bdd_inst, int64_t g, double *sm) {
     const int lane = threadIdx.x & 31;
-    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g >= s.groups) return;
     const int32_t j = s.grp_bdd[g * 32 + lane];
     // batched step search (dm_batch.cu): each diagram's own instance's gamma
     // (stopped searches are evaluated too and ignored by their decision)
@@ -49,8 +44,15 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    double *nb = sm + threadIdx.x;                       // distances of position k-1 (next layer)
-    double *cur = sm + W * kSweepThreads + threadIdx.x;  // distances of position k
+    constexpr bool kReg = W <= kRegRows;
+    Row<W, kReg, kSweepThreads> nb, cur;  // distances of position k-1 (next layer) and of position k
+    if constexpr (kReg) {
+#pragma unroll
+        for (int u = 0; u < W; ++u) nb.put(u, DM_INF), cur.put(u, DM_INF);
+    } else {
+        nb.p = sm + threadIdx.x;
+        cur.p = sm + WS * kSweepThreads + threadIdx.x;
+    }
     // Register double buffer: the arc targets and dual of position k+1 are
     // loaded while position k is computed, so each step waits on shared
     // memory only (the sweep is otherwise one DRAM round trip per layer).
@@ -98,11 +100,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
             vv[i] = 0.0;
             if (i < w) {
                 const int32_t a = z[i], b = o[i];
-                const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nb[a * kSweepThreads]);
-                const double c1 =
-                    b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb[b * kSweepThreads]));
+                const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nb.get(a));
+                const double c1 = b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nb.get(b)));
                 const double v = (c0 <= c1) ? c0 : c1;
-                cur[i * kSweepThreads] = v;
+                cur.put(i, v);
                 vv[i] = v;
             }
         }
@@ -125,11 +126,33 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
                 }
             }
         }
-        double *t = nb;
-        nb = cur;
-        cur = t;
-        if (act && k == nj - 1) bounds[j] = nb[0];  // root layer: single node
+        swap_rows(nb, cur);
+        if (act && k == nj - 1) bounds[j] = nb.at(0);  // root layer: single node
     }
+}
+
+// the group's widest layer picks the narrowest unrolled body (bit-identical)
+template <int W, bool kTrial, bool kStore>
+__global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::SweepDev s, const double *__restrict__ lam,
+                                                                        const double *__restrict__ d, double gamma,
+                                                                        double *__restrict__ B,
+                                                                        double *__restrict__ bounds,
+                                                                        const double *__restrict__ ctl,
+                                                                        const int32_t *__restrict__ bdd_inst) {
+    extern __shared__ double sm[];
+    if (kTrial && ctl && !bdd_inst) {  // device step search: ctl = dm_step_search state
+        if (ctl[5] != 0.0) return;  // the search already stopped
+        gamma = ctl[0];
+    }
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g >= s.groups) return;
+    const int gw = s.grp_width ? s.grp_width[g] : W;
+    if (W > 2 && gw <= 2)
+        sweep_backward_body<2, W, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, sm);
+    else if (W > 4 && gw <= 4)
+        sweep_backward_body<4, W, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, sm);
+    else
+        sweep_backward_body<W, W, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, sm);
 }
 
 template <int W>
