@@ -66,12 +66,12 @@ __device__ __forceinline__ double c_one(int32_t b, double fl, const double *nb) 
     return b == dm::kTrue ? fl : (b == dm::kFalse ? DM_INF : __dadd_rn(fl, nb[b * kThreads]));
 }
 
-template <class R>
-__device__ __forceinline__ double c_zero(int32_t a, double fv, const R &nb) {
+template <int W, bool kReg, int S>
+__device__ __forceinline__ double c_zero(int32_t a, double fv, const Row<W, kReg, S> &nb) {
     return a == dm::kTrue ? fv : (a == dm::kFalse ? DM_INF : __dadd_rn(fv, nb.get(a)));
 }
-template <class R>
-__device__ __forceinline__ double c_one(int32_t b, double fl, const R &nb) {  // fl = fv + lam
+template <int W, bool kReg, int S>
+__device__ __forceinline__ double c_one(int32_t b, double fl, const Row<W, kReg, S> &nb) {  // fl = fv + lam
     return b == dm::kTrue ? fl : (b == dm::kFalse ? DM_INF : __dadd_rn(fl, nb.get(b)));
 }
 
@@ -178,7 +178,7 @@ __device__ __forceinline__ void dfr_backward_body(const DfrArgs &a, int64_t g, d
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    constexpr bool kReg = W <= kRegRows;
+    constexpr bool kReg = W <= kRegRowsDfr;
     Row<W, kReg, kThreads> nb, cur;  // distances of position k-1 (next layer) and of position k
     if constexpr (kReg) {
 #pragma unroll
@@ -326,7 +326,7 @@ __device__ __forceinline__ void dfr_forward_body(const DfrArgs &a, int64_t g, do
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    constexpr bool kReg = W <= kRegRows;
+    constexpr bool kReg = W <= kRegRowsDfr;
     // distances from the root at position k and k-1, B of position k-1 (kMM)
     Row<W, kReg, kThreads> cur, nxt, bn;
     if constexpr (kReg) {

@@ -41,5 +41,8 @@ __device__ __forceinline__ void swap_rows(Row<W, kReg, STRIDE> &a, Row<W, kReg, 
     b = t;
 }
 
-// rows of a body: registers up to this width
-constexpr int kRegRows = 4;
+// rows in registers up to this width: the full-table sweeps (C4 node-order
+// refresh 130 -> 112 us); the deferred MM passes keep shared-memory rows
+// (register rows there: C4 flat, C2 forward 295 -> 400 us)
+constexpr int kRegRowsSweep = 4;
+constexpr int kRegRowsDfr = 0;

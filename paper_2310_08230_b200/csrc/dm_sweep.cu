@@ -44,7 +44,7 @@ __device__ __forceinline__ void sweep_backward_body(const dm::SweepDev &s, const
     }
     const int32_t K = s.grp_npos[g];
     const int64_t p0 = s.grp_pos_lo[g];
-    constexpr bool kReg = W <= kRegRows;
+    constexpr bool kReg = W <= kRegRowsSweep;
     Row<W, kReg, kSweepThreads> nb, cur;  // distances of position k-1 (next layer) and of position k
     if constexpr (kReg) {
 #pragma unroll
