@@ -2722,8 +2722,9 @@ int dm_sum(const double *x, int64_t n, double *out, void *stream) {
 // Per-(device, length, stream) scratch of the chunked dot: chunk totals and
 // the two-loop scalars (same per-stream ownership as the pairwise plans).
 struct DotScratch {
-    double *partial = nullptr;  // chunk totals
+    double *partial = nullptr;  // chunk totals (two buffers: the cooperative two-loop alternates them)
     double *slots = nullptr;    // two-loop scalars (dm_lbfgs_direction)
+    unsigned *bar = nullptr;    // the cooperative two-loop's grid barrier {arrivals, generation, watchdog}
 };
 static std::map<ScratchKey, DotScratch> g_dot;
 constexpr int kMaxPairs = 64;
@@ -2737,10 +2738,14 @@ static int dot_scratch(int64_t n, void *stream, bool slots, DotScratch **out) {
     auto it = g_dot.find(key);
     if (it == g_dot.end()) {
         DotScratch d;
-        DM_CUDA(cudaMalloc((void **)&d.partial, nch * sizeof(double)));
+        DM_CUDA(cudaMalloc((void **)&d.partial, 2 * nch * sizeof(double)));
         it = g_dot.emplace(key, d).first;
     }
-    if (slots && !it->second.slots) DM_CUDA(cudaMalloc((void **)&it->second.slots, (3 * kMaxPairs + 1) * sizeof(double)));
+    if (slots && !it->second.slots) {
+        DM_CUDA(cudaMalloc((void **)&it->second.slots, (3 * kMaxPairs + 1) * sizeof(double)));
+        DM_CUDA(cudaMalloc((void **)&it->second.bar, 4 * sizeof(unsigned)));
+        DM_CUDA(cudaMemset(it->second.bar, 0, 4 * sizeof(unsigned)));
+    }
     *out = &it->second;
     return DM_OK;
 }
@@ -2764,7 +2769,7 @@ int dm_release_caches(void) {
         release(std::get<0>(kv.first), {p.leaf_off, p.leaf_len, p.left, p.right, p.height_lo, p.vals});
     }
     g_plans.clear();
-    for (auto &kv : g_dot) release(std::get<0>(kv.first), {kv.second.partial, kv.second.slots});
+    for (auto &kv : g_dot) release(std::get<0>(kv.first), {kv.second.partial, kv.second.slots, kv.second.bar});
     g_dot.clear();
     cudaSetDevice(cur);
     const cudaError_t e = cudaGetLastError();
@@ -2805,7 +2810,7 @@ int dm_lbfgs_direction(const double *g, const double *const *s, const double *co
         }
     DotScratch *sc;
     if (int rc = dot_scratch(n, stream, true, &sc)) return rc;
-    return dm::lbfgs_two_loop(g, s, y, rho, sy, m, n, d, sc->slots, sc->partial, stream);
+    return dm::lbfgs_two_loop(g, s, y, rho, sy, m, n, d, sc->slots, sc->partial, stream, sc->bar);
 }
 
 int dm_curvature_pair(const double *lam, double *lam_prev, const double *g, const double *g_prev, double *s,

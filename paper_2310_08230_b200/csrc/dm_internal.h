@@ -189,8 +189,11 @@ int dfr_boundary_gather(int64_t n, const int32_t *layer, const int32_t *slot, co
                         void *stream);
 int dfr_boundary_average(int64_t n, const int32_t *layer, const int32_t *slot, const int32_t *slot_lo,
                          const int32_t *slot_hi, const double *buf, double *out, bool apply, void *stream);
+// bar (3 zeroed words) and partial[2 * nchunks]: the whole recursion in one
+// cooperative launch; bar == null: 2m+2 fused launches
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
-                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream);
+                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream,
+                   unsigned *bar = nullptr);
 
 // Batched quasi-Newton control of a merged block-diagonal instance
 // (dm_batch.cu): per-instance reduction plans and element -> instance maps.

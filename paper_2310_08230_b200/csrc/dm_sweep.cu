@@ -12,6 +12,7 @@
 // order with strict <.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -353,27 +354,17 @@ __device__ __forceinline__ int pair_index(int i) { return (threadIdx.x >> 2) * 6
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// One FULL chunk (aligned, 4096 elements) by a 128-thread block: the
+// update of x and the chunk total of v . x (a perfect tree over 32 leaves of
+// 128, numpy's order); the total is valid on thread 0.
 template <int kMode>
-__global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, double *__restrict__ partial) {
-    pdl_launch_dependents();
-    const int64_t off = (int64_t)blockIdx.x * kChunk;
-    {
-        // 32 KB per vector and block: two 128-byte lines per thread
-        const char *pu = reinterpret_cast<const char *>((kMode == kDot ? a.x : a.u) + off);
-        const char *pv = reinterpret_cast<const char *>((a.v ? a.v : a.x) + off);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int line = (threadIdx.x + k * kChunkThreads) * 128;
-            if (kMode != kDot) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + line));
-            if (a.v) asm volatile("prefetch.global.L2 [%0];" ::"l"(pv + line));
-        }
-    }
-    pdl_wait();  // the previous step's x and scalars are complete from here
-    const StepCoef c = step_coef<kMode>(a);
-    double2 *x2 = reinterpret_cast<double2 *>(a.x + off);
-    const double2 *u2 = reinterpret_cast<const double2 *>((kMode == kDot ? a.x : a.u) + off);
-    const double2 *v2 = reinterpret_cast<const double2 *>((a.v ? a.v : a.x) + off);
-    const bool dot = a.v != nullptr;
+__device__ __forceinline__ double full_chunk(const StepCoef &c, double *x, const double *u, const double *v,
+                                             int64_t off) {
+    __shared__ double leaf_sm[32];
+    double2 *x2 = reinterpret_cast<double2 *>(x + off);
+    const double2 *u2 = reinterpret_cast<const double2 *>((kMode == kDot ? x : u) + off);
+    const double2 *v2 = reinterpret_cast<const double2 *>((v ? v : x) + off);
+    const bool dot = v != nullptr;
     double r0 = 0.0, r1 = 0.0;
 #pragma unroll
     for (int i0 = 0; i0 < 16; i0 += 4) {
@@ -398,20 +389,43 @@ __global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, 
             }
         }
     }
-    if (!dot) return;
+    if (!dot) return 0.0;
     const unsigned m = 0xffffffffu;
     double r = __dadd_rn(r0, r1);
     r = __dadd_rn(r, __shfl_xor_sync(m, r, 1));
     r = __dadd_rn(r, __shfl_xor_sync(m, r, 2));
-    __shared__ double leaf_sm[32];
+    __syncthreads();  // the previous chunk's leaf totals are consumed
     if ((threadIdx.x & 3) == 0) leaf_sm[threadIdx.x >> 2] = r;
     __syncthreads();
+    double t = 0.0;
     if (threadIdx.x < 32) {
-        double t = leaf_sm[threadIdx.x];
+        t = leaf_sm[threadIdx.x];
 #pragma unroll
         for (int w = 1; w < 32; w <<= 1) t = __dadd_rn(t, __shfl_xor_sync(m, t, w));
-        if (threadIdx.x == 0) partial[blockIdx.x] = __dadd_rn(0.0, t);
+        t = __dadd_rn(0.0, t);
     }
+    return t;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kChunkThreads) chunk_step_kernel(ChunkStep a, double *__restrict__ partial) {
+    pdl_launch_dependents();
+    const int64_t off = (int64_t)blockIdx.x * kChunk;
+    {
+        // 32 KB per vector and block: two 128-byte lines per thread
+        const char *pu = reinterpret_cast<const char *>((kMode == kDot ? a.x : a.u) + off);
+        const char *pv = reinterpret_cast<const char *>((a.v ? a.v : a.x) + off);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int line = (threadIdx.x + k * kChunkThreads) * 128;
+            if (kMode != kDot) asm volatile("prefetch.global.L2 [%0];" ::"l"(pu + line));
+            if (a.v) asm volatile("prefetch.global.L2 [%0];" ::"l"(pv + line));
+        }
+    }
+    pdl_wait();  // the previous step's x and scalars are complete from here
+    const StepCoef c = step_coef<kMode>(a);
+    const double t = full_chunk<kMode>(c, a.x, a.u, a.v, off);
+    if (a.v && threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
 // Tail chunk (update + its total) and the reduction of all chunk totals.
@@ -589,6 +603,165 @@ __global__ void __launch_bounds__(kChunkThreads) curvature_pair_kernel(const dou
     if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
+// ---------------------------------------------------------------------------
+// The whole two-loop in ONE cooperative launch (dm_lbfgs_direction): each
+// block owns chunks b, b+G, ... for every step, so x needs no exchange; per
+// step the chunk totals meet in a double-buffered array, one grid barrier,
+// and every block reduces them itself (the same totals plan), so the next
+// step's coefficient is known grid-wide without a second barrier.  Every
+// chunk is computed by full_chunk / the generic path exactly as the
+// per-step kernels compute it: the direction is bit-identical (2m+2 barriers
+// instead of 4m+4 dependent launches).
+constexpr int kMaxTwoLoopPairs = 64;
+struct TwoLoopArgs {
+    const double *g;
+    double *d;
+    const double *s[kMaxTwoLoopPairs];
+    const double *y[kMaxTwoLoopPairs];
+    double rho[kMaxTwoLoopPairs];
+    double sy0;
+    int m;
+    bool vec;
+    int64_t n, nch;
+    double *partial;  // [2][nch]
+    double *slots;    // dot1[m], alpha[m], yy, dot2[m] (as the per-step path)
+    unsigned *bar;    // {arrivals, generation, watchdog}
+    SumPlan chunk, tail, totals;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// grid barrier (all blocks co-resident: cooperative launch); false when the
+// watchdog fired (a block stopped arriving for 2 s) — the kernel then exits
+__device__ bool two_loop_barrier(unsigned *bar, unsigned nblocks, unsigned &gen) {
+    __shared__ int ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ok = 1;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            uint64_t t0 = 0;
+            unsigned spins = 0;
+            while (ld_acquire_u32(bar + 1) == gen) {
+                if ((++spins & 255u) == 0) {
+                    uint64_t now;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    if (t0 == 0) t0 = now;
+                    if (now - t0 > 2000000000ull || ld_acquire_u32(bar + 2)) {
+                        atomicExch(bar + 2, 1u);
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+        }
+        gen += 1;
+        __threadfence();
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+// chunk k of one step (update + total on thread 0); `buf`: 4096 doubles
+template <int kMode>
+__device__ __forceinline__ double two_loop_chunk(const TwoLoopArgs &a, const StepCoef &c, double *x, const double *u,
+                                                 const double *v, int64_t k, double *buf) {
+    const int64_t off = k * kChunk;
+    const int len = (int)((a.n - off) < kChunk ? (a.n - off) : kChunk);
+    if (a.vec && len == kChunk) return full_chunk<kMode>(c, x, u, v, off);
+    __syncthreads();  // buf is free
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        const double xo = kMode != kCopy ? x[off + i] : 0.0;
+        const double uo = kMode != kDot ? u[off + i] : 0.0;
+        const double xi = step_update<kMode>(c, xo, uo);
+        if (kMode != kDot) x[off + i] = xi;
+        if (v) buf[i] = __dmul_rn(v[off + i], xi);
+    }
+    if (!v) return 0.0;
+    __syncthreads();
+    return smem_pairwise(buf, len == kChunk ? a.chunk : a.tail);
+}
+
+template <int kMode>
+__device__ __forceinline__ void two_loop_chunks(const TwoLoopArgs &a, const StepCoef &c, double *x, const double *u,
+                                                const double *v, double *partial, double *buf) {
+    for (int64_t k = blockIdx.x; k < a.nch; k += gridDim.x) {
+        const double t = two_loop_chunk<kMode>(a, c, x, u, v, k, buf);
+        if (v && threadIdx.x == 0) partial[k] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kChunkThreads) two_loop_kernel(const __grid_constant__ TwoLoopArgs a) {
+    __shared__ double buf[kChunk];
+    __shared__ double tot;                    // the last step's dot total
+    __shared__ double al[kMaxTwoLoopPairs];  // the first loop's alphas
+    const int m = a.m;
+    double *dot1 = a.slots, *alpha = a.slots + m, *yy = a.slots + 2 * m, *dot2 = a.slots + 2 * m + 1;
+    double yy_v = 0.0, dot_prev = 0.0;
+    unsigned gen = 0;
+    if (threadIdx.x == 0) gen = ld_acquire_u32(a.bar + 1);
+    const int steps = 2 * m + 2;
+    for (int t = 0; t < steps; ++t) {
+        double *partial = a.partial + (t & 1) * a.nch;
+        StepCoef c{0.0, 0.0};
+        const double *v = nullptr;
+        double *out = nullptr;
+        if (t == 0) {  // yy = y0 . y0
+            two_loop_chunks<kDot>(a, c, const_cast<double *>(a.y[0]), nullptr, a.y[0], partial, buf);
+            out = yy;
+            v = a.y[0];
+        } else if (t == 1) {  // q = g, dot1[0] = s0 . q
+            two_loop_chunks<kCopy>(a, c, a.d, a.g, a.s[0], partial, buf);
+            out = dot1;
+            v = a.s[0];
+        } else if (t <= m) {  // first loop, i = t - 2
+            const int i = t - 2;
+            c.coef = __dmul_rn(a.rho[i], dot_prev);
+            if (threadIdx.x == 0) al[i] = c.coef;
+            if (blockIdx.x == 0 && threadIdx.x == 0) alpha[i] = c.coef;
+            two_loop_chunks<kFirst>(a, c, a.d, a.y[i], a.s[i + 1], partial, buf);
+            out = dot1 + i + 1;
+            v = a.s[i + 1];
+        } else if (t == m + 1) {  // last first-loop step with the scaling
+            const int i = m - 1;
+            c.coef = __dmul_rn(a.rho[i], dot_prev);
+            c.r = __ddiv_rn(a.sy0, yy_v);
+            if (threadIdx.x == 0) al[i] = c.coef;
+            if (blockIdx.x == 0 && threadIdx.x == 0) alpha[i] = c.coef;
+            two_loop_chunks<kScale>(a, c, a.d, a.y[i], a.y[m - 1], partial, buf);
+            out = dot2;
+            v = a.y[m - 1];
+        } else {  // second loop, k = t - m - 2, i = m - 1 - k
+            const int k = t - m - 2, i = m - 1 - k;
+            c.coef = __dsub_rn(al[i], __dmul_rn(a.rho[i], dot_prev));
+            v = i > 0 ? a.y[i - 1] : nullptr;
+            two_loop_chunks<kSecond>(a, c, a.d, a.s[i], v, partial, buf);
+            out = v ? dot2 + k + 1 : nullptr;
+        }
+        if (!v) break;  // the last step has no inner product
+        if (!two_loop_barrier(a.bar, gridDim.x, gen)) return;
+        // every block reduces the chunk totals itself (numpy's order)
+        for (int64_t i = threadIdx.x; i < a.nch; i += blockDim.x) buf[i] = __ldcg(partial + i);
+        __syncthreads();
+        const double total = smem_pairwise(buf, a.totals);
+        if (threadIdx.x == 0) {
+            tot = total;
+            if (blockIdx.x == 0) *out = total;
+        }
+        __syncthreads();
+        dot_prev = tot;
+        if (t == 0) yy_v = tot;
+    }
+}
+
 }  // namespace
 
 namespace dm {
@@ -618,11 +791,68 @@ int curvature_pair(const double *lam, double *lam_prev, const double *g, const d
     return e == cudaSuccess ? DM_OK : fail(e, "curvature_pair finish");
 }
 
+// the cooperative two-loop: grid size for this device (0: unavailable)
+static int two_loop_grid(int64_t nch) {
+    static int per_sm = -1, sms = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int b = 0;
+        if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, two_loop_kernel, kChunkThreads, 0)) b = 0;
+        per_sm = b;
+    }
+    // one chunk per block: with more chunks than co-resident blocks every
+    // block would loop over several and reduce all totals per step (C2,
+    // 2,296 chunks on 592 blocks: 1.34 -> 1.48 ms), so the per-step
+    // launches stay (C4, 320 chunks: 0.33 -> 0.25 ms)
+    const int64_t cap = (int64_t)per_sm * sms;
+    return nch <= cap ? (int)nch : 0;
+}
+
+static bool two_loop_persistent() {
+    static const int v = [] {
+        const char *e = std::getenv("DM_TWO_LOOP_PERSIST");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 int lbfgs_two_loop(const double *g, const double *const *s, const double *const *y, const double *rho,
-                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream) {
+                   const double *sy, int m, int64_t n, double *d, double *slots, double *partial, void *stream,
+                   unsigned *bar) {
     const int64_t nch = (n + kChunk - 1) / kChunk;
     if (n <= 0 || nch >= INT32_MAX || m < 1) return DM_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
+    int grid = 0;
+    if (bar && m <= kMaxTwoLoopPairs && nch <= kChunk && two_loop_persistent() && (grid = two_loop_grid(nch)) > 0) {
+        TwoLoopArgs a{};
+        a.g = g;
+        a.d = d;
+        for (int i = 0; i < m; ++i) {
+            a.s[i] = s[i];
+            a.y[i] = y[i];
+            a.rho[i] = rho[i];
+        }
+        a.sy0 = sy[0];
+        a.m = m;
+        a.vec = aligned16(g) && aligned16(d);
+        for (int i = 0; i < m; ++i) a.vec = a.vec && aligned16(s[i]) && aligned16(y[i]);
+        a.n = n;
+        a.nch = nch;
+        a.partial = partial;
+        a.slots = slots;
+        a.bar = bar;
+        a.chunk = make_sum_plan(kChunk);
+        a.tail = make_sum_plan((int)(n % kChunk));
+        a.totals = make_sum_plan((int)nch);
+        void *args[] = {(void *)&a};
+        const cudaError_t e = cudaLaunchCooperativeKernel((const void *)two_loop_kernel, dim3(grid),
+                                                          dim3(kChunkThreads), args, 0, st);
+        return e == cudaSuccess ? DM_OK : fail(e, "two_loop (cooperative)");
+    }
     // slots: [0, m) first-loop dots, [m, 2m) alphas, 2m = y0.y0, [2m+1, 3m+1) second-loop dots
     double *dot1 = slots, *alpha = slots + m, *yy = slots + 2 * m, *dot2 = slots + 2 * m + 1;
     if (int rc = dm::chunk_dot(y[0], y[0], n, partial, yy, stream)) return rc;

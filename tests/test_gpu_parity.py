@@ -214,7 +214,10 @@ def test_lbfgs_direction_matches_dense_oracle_and_pairwise_oracle():  # test_qn.
         assert d.tobytes() == solver.lbfgs(g, pairs, solver._dot_chunked).tobytes()
 
 
-@pytest.mark.parametrize("n,m", [(1, 1), (4096, 1), (3 * 4096 + 123, 4), (100003, 10), (4095, 3), (5 * 4096 + 3900, 5)])
+# up to ~590 chunks the recursion is one cooperative launch; 3,000,000 (733
+# chunks) takes the per-step launches on a B200
+@pytest.mark.parametrize("n,m", [(1, 1), (4096, 1), (3 * 4096 + 123, 4), (100003, 10), (4095, 3), (5 * 4096 + 3900, 5),
+                                 (3_000_000, 3)])
 def test_fused_two_loop_matches_unfused_and_oracle(n, m):
     rng = np.random.default_rng(n + m)
     history = qn.LbfgsHistory(10)
@@ -230,6 +233,26 @@ def test_fused_two_loop_matches_unfused_and_oracle(n, m):
     fused = qn.lbfgs_direction(g, history).cpu().numpy()
     plain = qn.lbfgs_direction(g, history, fused=False).cpu().numpy()
     assert fused.tobytes() == plain.tobytes()
+    assert fused.tobytes() == solver.lbfgs(g.cpu().numpy(), pairs, solver._dot_chunked).tobytes()
+
+
+def test_fused_two_loop_on_a_misaligned_gradient():
+    """g as a view one element into its buffer: no 16-byte vector path, every
+    chunk through the generic per-element path, same bits."""
+    n, m = 3 * 4096 + 5, 2
+    rng = np.random.default_rng(7)
+    history = qn.LbfgsHistory(10)
+    pairs = []
+    while len(history) < m:
+        s = rng.standard_normal(n)
+        y = s * rng.uniform(0.5, 2.0, n)
+        sy = solver._dot_chunked(s, y)
+        qn.update_history(s, y, history, qn.StepConfig())
+        pairs.insert(0, (s, y, 1.0 / sy, sy))
+    big = torch.from_numpy(rng.standard_normal(n + 1)).cuda()
+    g = big[1:]
+    assert g.data_ptr() % 16 != 0
+    fused = qn.lbfgs_direction(g, history).cpu().numpy()
     assert fused.tobytes() == solver.lbfgs(g.cpu().numpy(), pairs, solver._dot_chunked).tobytes()
 
 
