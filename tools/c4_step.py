@@ -50,7 +50,9 @@ for _ in range(n):
     g = phase(log, "subgradient", lambda: subgradient_device(st))
     d = phase(log, "two_loop", lambda: qn.lbfgs_direction(g, run.history))
     d = phase(log, "project", lambda: qn.project_direction(d, st))
+    sw0 = st.sweeps
     gamma, ok = phase(log, "step_search", lambda: qn.find_step_size(st, d, run.gamma, run.step_cfg))
+    log["trials"] = log.get("trials", 0.0) + (st.sweeps - sw0)
     run.gamma = gamma
     if ok:
         phase(log, "shift", lambda: st.shift_lambda_scaled(gamma, d))

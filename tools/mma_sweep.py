@@ -28,8 +28,9 @@ def main():
     results = []
     ref = None
     configs = []
-    for threads, bps, sleep in ((256, 3, 0), (256, 3, 20), (256, 3, 50), (256, 3, 100), (256, 2, 0), (128, 3, 0),
-                                (128, 4, 0), (256, 1, 0), (128, 2, 0), (128, 1, 0), (64, 2, 0), (64, 1, 0), (256, 3, 0)):
+    for threads, bps, sleep in ((256, 3, 32), (256, 3, 0), (256, 3, 16), (256, 3, 64), (256, 2, 32), (256, 4, 32),
+                                (128, 4, 32), (128, 6, 32), (256, 2, 0), (256, 4, 0), (512, 1, 32), (512, 2, 32),
+                                (256, 3, 32)):
         configs.append((threads, bps, sleep, 0, 1 << 16))
     for threads, bps, sleep, probe, look in configs:
         try:
