@@ -266,6 +266,31 @@ def test_find_step_size_ascends_above_start():  # test_qn.py:104-114
     assert st.eval_lambda(st.lam + gamma * d) > dual_objective(st)
 
 
+def test_find_step_size_breaks_once_ascent_threshold_met():  # test_qn.py:128-137
+    """Any trial counts as sufficient ascent: the search stops after the
+    baseline and one trial — on the host loop (its fused trial evaluations
+    counted) and in the device search (its trial counter)."""
+    st = init_duals(kinked())
+    d = qn.project_direction(subgradient(st), st)
+    cfg = qn.StepConfig(min_ascent=-10.0)
+    calls = []
+    original = st.eval_step
+    st.eval_step = lambda dd, gamma: (calls.append(1), original(dd, gamma))[1]
+    qn.find_step_size(st, d, 1.0, cfg, on_device=False)
+    assert len(calls) == 2
+    del st.eval_step
+    _, _, trials = st.search_step(qn.as_device(d, st.device), 1.0, cfg.shrink, cfg.grow, cfg.min_ascent,
+                                  cfg.max_trials)
+    assert trials == 2
+
+
+def test_lbfgs_direction_requires_history():  # test_qn.py:57-59
+    from paper_2310_08230_b200.errors import EmptyHistory
+
+    with pytest.raises(EmptyHistory):
+        qn.lbfgs_direction(np.zeros(3), qn.LbfgsHistory(5))
+
+
 def test_solver_iteration_keeps_optimal_toy_unchanged():  # test_qn.py:149-158
     st = init_duals(toy())
     before = dual_objective(st)
