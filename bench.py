@@ -521,13 +521,28 @@ def run_b200(args, rank, world, local_rank):
             "gpu_launches": t["launches"], "kernels": t["kernels"], "roofline": roofline_of(t, args.config, sched),
             "clocks": t["clocks"],
         }
-    if rank != 0:
-        return None
     del t, st
     if world > 1:
-        # scaling runs report the headline only: rank 0's extras would keep it
-        # busy for minutes after the other ranks finished
+        # scaling runs report the headline and the end-to-end number only
+        # (rank 0's other extras would keep it busy for minutes after the
+        # other ranks finished); e2e: every rank solves its own instance from
+        # host buffers at the same time, whole-job work over the slowest rank
+        if not args.no_e2e:
+            torch.distributed.barrier()
+            e = e2e_run(args, inst, dev, sched)
+            total, max_ms = aggregate_work_time(e["value"] * e["seconds_per_step"], e["seconds_per_step"] * 1e3,
+                                                world, dev)
+            if rank == 0:
+                e["value"] = total / (max_ms / 1e3)
+                e["seconds_per_step"] = max_ms / 1e3
+                e["ms_per_iteration"] = max_ms / max(args.e2e_iters, 1)
+                e["h2d_bytes_per_step"] *= world  # every rank's instance (the per-rank figure is rank 0's)
+                e["d2h_bytes_per_step"] *= world
+                e["ranks"] = world
+                result["e2e"] = e
         return result
+    if rank != 0:
+        return None
     if not args.no_extras:
         other = "deferred" if sched == "exact" else "exact"
         o = timed_steps(args, inst, dev, other, 1, 0, local_rank, clocks=False)
