@@ -125,3 +125,27 @@ def test_gpu_batched_hybrid_equals_separate_solves(schedule, compact):
         assert got[k].stop_reason == one.stop_reason and got[k].iterations == one.iterations
         assert got[k].best_bound == one.best_bound
         assert got[k].lam.tobytes() == one.state.lam.tobytes(), k
+
+
+def test_batched_solver_runs_hybrid_solves_only():
+    from paper_2310_08230_b200.batch import BatchedSolver
+
+    with pytest.raises(ValueError, match="hybrid"):
+        BatchedSolver([], SolveConfig(mode="mma-only"))
+
+
+@pytest.mark.gpu
+def test_gpu_batched_single_instance_equals_its_solve():
+    """A batch of one: one batched iteration, then the instance's own
+    DualSolver loop (the hand-off) — identical to qn.solve."""
+    from bench import build_instance
+    from paper_2310_08230_b200 import qn
+    from paper_2310_08230_b200.batch import solve_batched
+
+    inst = build_instance("c3", 1)
+    cfg = SolveConfig(mode="hybrid", max_iterations=40)
+    (got,) = solve_batched([inst], cfg, device="cuda:0")
+    one = qn.solve(inst, cfg, device="cuda:0")
+    assert got.bounds == one.bounds
+    assert got.iterations == one.iterations and got.stop_reason == one.stop_reason
+    assert got.lam.tobytes() == one.state.lam.tobytes()
