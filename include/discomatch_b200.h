@@ -74,6 +74,14 @@ int dm_instance_from_bdds(int64_t num_variables, const double *costs, const int6
                           int64_t num_bdds, const int64_t *bdd_layer_lo, const int64_t *layer_var,
                           const int64_t *layer_node_lo, const int32_t *zeros, const int32_t *ones,
                           int64_t chunk_size, dm_instance **out);
+/* Variable numbering of a product space (product_space.py): a greedy row
+ * colouring — variables in index order take the smallest colour no variable
+ * of any of their rows already has (colour_out[V]).  Numbering variables by
+ * colour bounds the exact passes' DAG depth by the number of colours (every
+ * diagram chain advances at least one colour per layer): C4 1,665 -> 370
+ * levels.  No reference counterpart (the reference has no product space). */
+int dm_row_colouring(int64_t num_variables, int64_t num_rows, const int64_t *row_ptr, const int64_t *row_var,
+                     int64_t *colour_out);
 int dm_instance_get_info(const dm_instance *inst, dm_instance_info *info);
 /* Copy the FlatBdds arrays out (any pointer may be NULL to skip it):
  * costs[V], variable_order[V], bdd_layer_lo[nb+1], layer_node_lo[L+1],

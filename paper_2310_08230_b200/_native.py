@@ -52,6 +52,7 @@ SIGNATURES = {
     "dm_instance_from_rows": ([_I, _P, _I, _P, _P, _P, _P, _I, ctypes.POINTER(_P)], _INT),
     "dm_instance_from_bdds": ([_I, _P, _P, _I, _P, _P, _P, _P, _P, _I, ctypes.POINTER(_P)], _INT),
     "dm_condition_flat": ([_I, _P, _P, _I, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_I), ctypes.POINTER(_P)], _INT),
+    "dm_row_colouring": ([_I, _I, _P, _P, _P], _INT),
     "dm_instance_get_info": ([_P, ctypes.POINTER(InstanceInfo)], _INT),
     "dm_instance_export": ([_P] + [_P] * 11, _INT),
     "dm_instance_free": ([_P], None),

@@ -694,6 +694,51 @@ int dm_condition_flat(int64_t num_variables, const double *costs, const int64_t 
     return split_and_flatten(kept, std::move(cst), std::move(order), 0, out);
 }
 
+int dm_row_colouring(int64_t num_variables, int64_t num_rows, const int64_t *row_ptr, const int64_t *row_var,
+                     int64_t *colour_out) {
+    if (num_variables < 0 || num_rows < 0 || (num_rows && (!row_ptr || !row_var)) || (num_variables && !colour_out)) {
+        dm::set_error("dm_row_colouring: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    // variable -> rows (CSR)
+    std::vector<int64_t> vptr(num_variables + 1, 0);
+    for (int64_t r = 0; r < num_rows; ++r)
+        for (int64_t i = row_ptr[r]; i < row_ptr[r + 1]; ++i) {
+            const int64_t v = row_var[i];
+            if (v < 0 || v >= num_variables) {
+                dm::set_error("dm_row_colouring: variable id out of range");
+                return DM_ERR_INVALID;
+            }
+            ++vptr[v + 1];
+        }
+    for (int64_t v = 0; v < num_variables; ++v) vptr[v + 1] += vptr[v];
+    std::vector<int64_t> vrows(vptr[num_variables]), fill(vptr.begin(), vptr.end() - 1);
+    for (int64_t r = 0; r < num_rows; ++r)
+        for (int64_t i = row_ptr[r]; i < row_ptr[r + 1]; ++i) vrows[fill[row_var[i]]++] = r;
+    // colours each row already holds, as growing bitsets
+    std::vector<std::vector<uint64_t>> used(num_rows);
+    std::vector<uint64_t> taken;
+    for (int64_t v = 0; v < num_variables; ++v) {
+        taken.assign(taken.size(), 0);
+        for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+            const auto &u = used[vrows[k]];
+            if (u.size() > taken.size()) taken.resize(u.size(), 0);
+            for (size_t w = 0; w < u.size(); ++w) taken[w] |= u[w];
+        }
+        size_t w = 0;
+        while (w < taken.size() && taken[w] == ~0ull) ++w;
+        const int64_t c = (int64_t)(w * 64 + (w < taken.size() ? __builtin_ctzll(~taken[w]) : 0));
+        colour_out[v] = c;
+        const size_t cw = (size_t)(c >> 6);
+        for (int64_t k = vptr[v]; k < vptr[v + 1]; ++k) {
+            auto &u = used[vrows[k]];
+            if (u.size() <= cw) u.resize(cw + 1, 0);
+            u[cw] |= 1ull << (c & 63);
+        }
+    }
+    return DM_OK;
+}
+
 int dm_instance_get_info(const dm_instance *inst, dm_instance_info *info) {
     if (!inst || !info) {
         dm::set_error("invalid arguments");

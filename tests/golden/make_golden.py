@@ -114,8 +114,9 @@ LARGE = [("ps_c2", "c2", 0, 128, 3, 8), ("ps_c4", "c4", 0, 128, 3, 10),
 
 
 def main():
-    if sys.argv[1:] == ["--large"]:
-        append_product_cases(LARGE, "golden_large.json")
+    if sys.argv[1:2] == ["--large"]:
+        pick = sys.argv[2:]  # optional case names: only these are re-recorded
+        append_product_cases([c for c in LARGE if not pick or c[0] in pick], "golden_large.json")
         return
     if len(sys.argv) > 1:
         append_product_cases([EXTRA[c] for c in sys.argv[1:]])
