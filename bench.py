@@ -122,11 +122,11 @@ def oracle_instance(config: str, seed: int, chunk: int = 128):
     table, oracle/model.py), so the reference arm never maps the product
     library; the lowering is golden-pinned against the real reference
     (tests/test_oracle_golden.py, tests/test_large_parity.py)."""
-    from oracle import model
+    from oracle import clib, model
     from paper_2310_08230_b200 import product_space as ps
 
     t = time.perf_counter()
-    p = ps.synthetic_product_space(config, seed)
+    p = ps.synthetic_product_space(config, seed, colouring=clib.row_colouring)
     oi = model.instance_from_rows(p.costs, p.rows())
     if chunk:
         oi = model.split_instance(oi, chunk)

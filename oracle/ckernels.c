@@ -522,3 +522,56 @@ void oracle_dfr_average(i64 P, const i64 *proc_ptr, const i64 *proc_layers, cons
         }
     }
 }
+
+/* Greedy row colouring of a product space's variables (product_space.py's
+ * numbering of pruned spaces; the product computes it in dm_row_colouring):
+ * variables in index order take the smallest colour that no variable of any
+ * of their rows holds.  Lets the CPU arm build the same instance without the
+ * product library.  Returns the number of colours, -1 on bad input. */
+i64 oracle_row_colouring(i64 nv, i64 nrows, const i64 *row_ptr, const i64 *row_var, i64 *colour) {
+    i64 *vptr = calloc((size_t)nv + 1, sizeof(i64));
+    if (!vptr) return -1;
+    for (i64 r = 0; r < nrows; ++r)
+        for (i64 i = row_ptr[r]; i < row_ptr[r + 1]; ++i) {
+            if (row_var[i] < 0 || row_var[i] >= nv) {
+                free(vptr);
+                return -1;
+            }
+            ++vptr[row_var[i] + 1];
+        }
+    for (i64 v = 0; v < nv; ++v) vptr[v + 1] += vptr[v];
+    i64 *vrows = malloc((size_t)(vptr[nv] ? vptr[nv] : 1) * sizeof(i64));
+    i64 *fill = malloc((size_t)(nv ? nv : 1) * sizeof(i64));
+    for (i64 v = 0; v < nv; ++v) fill[v] = vptr[v];
+    for (i64 r = 0; r < nrows; ++r)
+        for (i64 i = row_ptr[r]; i < row_ptr[r + 1]; ++i) vrows[fill[row_var[i]]++] = r;
+    /* a colour bound: one more than the largest number of row neighbours */
+    i64 bound = 1;
+    for (i64 v = 0; v < nv; ++v) {
+        i64 d = 1;
+        for (i64 k = vptr[v]; k < vptr[v + 1]; ++k) d += row_ptr[vrows[k] + 1] - row_ptr[vrows[k]] - 1;
+        if (d > bound) bound = d;
+    }
+    const i64 words = bound / 64 + 1;
+    uint64_t *used = calloc((size_t)(nrows ? nrows : 1) * (size_t)words, sizeof(uint64_t));
+    uint64_t *taken = malloc((size_t)words * sizeof(uint64_t));
+    i64 ncol = 0;
+    for (i64 v = 0; v < nv; ++v) {
+        for (i64 w = 0; w < words; ++w) taken[w] = 0;
+        for (i64 k = vptr[v]; k < vptr[v + 1]; ++k) {
+            const uint64_t *u = used + vrows[k] * words;
+            for (i64 w = 0; w < words; ++w) taken[w] |= u[w];
+        }
+        i64 c = 0;
+        while (taken[c >> 6] >> (c & 63) & 1) ++c;
+        colour[v] = c;
+        if (c + 1 > ncol) ncol = c + 1;
+        for (i64 k = vptr[v]; k < vptr[v + 1]; ++k) used[vrows[k] * words + (c >> 6)] |= 1ull << (c & 63);
+    }
+    free(vptr);
+    free(vrows);
+    free(fill);
+    free(used);
+    free(taken);
+    return ncol;
+}

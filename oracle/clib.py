@@ -46,6 +46,7 @@ class _Lib:
                 "oracle_dfr_forward": ([_I, _P, _P, _P, _P, _D] + [_P] * 6, None),
                 "oracle_dfr_backward": ([_I, _P, _P, _P, _P, _D] + [_P] * 6, None),
                 "oracle_dfr_average": ([_I, _P, _P, _P, _P], None),
+                "oracle_row_colouring": ([_I, _I, _P, _P, _P], _I),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(h, name)
@@ -64,3 +65,14 @@ lib = _Lib()
 def ptr(a: np.ndarray) -> int:
     assert a.flags["C_CONTIGUOUS"], "oracle arrays must be contiguous"
     return a.ctypes.data
+
+
+def row_colouring(p) -> np.ndarray:
+    """Greedy row colouring of a ProductSpace (oracle_row_colouring): the CPU
+    arm's copy of the product's dm_row_colouring."""
+    colour = np.empty(p.num_variables, np.int64)
+    rp = np.ascontiguousarray(p.row_ptr, dtype=np.int64)
+    rv = np.ascontiguousarray(p.row_var, dtype=np.int64)
+    if lib.oracle_row_colouring(p.num_variables, p.num_rows, ptr(rp), ptr(rv), ptr(colour)) < 0:
+        raise ValueError("oracle_row_colouring: invalid rows")
+    return colour

@@ -303,7 +303,7 @@ def _canonical_rotation(m, n):
 
 def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray,
                         order: str = "auto", allowed: np.ndarray | None = None,
-                        order_seed: int = 2) -> ProductSpace:
+                        order_seed: int = 2, colouring=None) -> ProductSpace:
     """Enumerate P, order the variables, assemble rows and Eq. (2) costs.
 
     ``allowed`` (optional, bool (|V_M|, |V_N|)) keeps only product triangles
@@ -316,7 +316,9 @@ def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray
     Latin colours are sparse and the rows chain through many of them — C4's
     DAG depth 1,665 -> 370, C3's 752 -> 199, the longest row 366 / 197),
     "natural" (enumeration order); "auto" = "greedy" for a pruned space,
-    "colour" otherwise.
+    "colour" otherwise.  ``colouring`` (ProductSpace -> colours) replaces
+    the native ``row_colouring`` (bench.py's CPU arm passes the oracle's C
+    copy, so it builds the same instance without the product library).
     """
     if order == "auto":
         order = "greedy" if allowed is not None else "colour"
@@ -381,7 +383,7 @@ def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray
     m, n = _canonical_rotation(m, n)
     out = _assemble(M, N, feat_m, feat_n, m, n, kind, face_m, face_n)
     if order == "greedy":
-        perm = np.lexsort((np.arange(out.num_variables), row_colouring(out)))
+        perm = np.lexsort((np.arange(out.num_variables), (colouring or row_colouring)(out)))
         out = _assemble(M, N, feat_m, feat_n, m[perm], n[perm], kind[perm], face_m[perm], face_n[perm])
     return out
 
@@ -501,10 +503,10 @@ def synthetic_pair(config: str, seed: int = 0):
 PRUNING_K = {"c3": 10, "c4": 16}
 
 
-def synthetic_product_space(config: str, seed: int = 0) -> ProductSpace:
+def synthetic_product_space(config: str, seed: int = 0, colouring=None) -> ProductSpace:
     """The product-space ILP of a BASELINE config, pruned where the config
     says so (C3/C4: k-NN in descriptor space)."""
     M, N, fm, fn = synthetic_pair(config, seed)
     k = PRUNING_K.get(config)
     allowed = knn_allowed(fm, fn, k) if k else None
-    return build_product_space(M, N, fm, fn, allowed=allowed)
+    return build_product_space(M, N, fm, fn, allowed=allowed, colouring=colouring)

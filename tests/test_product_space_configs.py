@@ -67,3 +67,36 @@ def test_pruned_configs_keep_every_face_row_and_ground_truth(config):
     tt = (p.kind == ps.TRI_TRI) & (p.m == p.n).all(1)  # identity corner map
     gt_faces = np.flatnonzero(al[M.faces, N.faces].all(1))
     assert np.array_equal(np.unique(p.face_m[tt]), gt_faces)
+
+
+def test_pruned_spaces_are_numbered_by_a_greedy_row_colouring():
+    """C3 (pruned): the colour classes are valid (no two variables of a row
+    share a colour), the numbering is colour-major, the oracle's C copy of the
+    colouring gives the same colours (the CPU arm builds the same instance),
+    and the exact passes' depth is within a few levels of the colour count."""
+    import numpy as np
+
+    from oracle import clib
+    from paper_2310_08230_b200 import product_space as ps
+
+    p = ps.synthetic_product_space("c3", 0)
+    col = ps.row_colouring(p)
+    assert np.array_equal(col, clib.row_colouring(p))
+    for r in range(0, p.num_rows, 97):
+        c = col[p.row_var[p.row_ptr[r]:p.row_ptr[r + 1]]]
+        assert len(np.unique(c)) == len(c)
+    q = ps.synthetic_product_space("c3", 0, colouring=clib.row_colouring)
+    assert np.array_equal(q.row_var, p.row_var) and np.array_equal(q.costs, p.costs)
+    # the greedy numbering is a fixed point: variables already in colour order
+    assert np.array_equal(np.lexsort((np.arange(p.num_variables), col)), np.arange(p.num_variables))
+
+
+def test_reference_arm_builds_its_instance_without_the_product_library():
+    import subprocess
+    import sys
+
+    code = ("import bench; bench.oracle_instance('c3', 0); "
+            "from paper_2310_08230_b200 import _native; assert _native._lib is None, 'product library loaded'")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0, r.stderr[-2000:]
