@@ -91,13 +91,23 @@ def to_bytes(s):
 
 
 def main():
-    tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
+    args = sys.argv[1:]
+    traffic_name, cmd = "traffic", "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg` (C2)"
+    if "--traffic" in args:  # e.g. --traffic traffic_c4 --cmd "python bench.py --config c4 ...` (C4)"
+        i = args.index("--traffic")
+        traffic_name = args[i + 1]
+        del args[i:i + 2]
+    if "--cmd" in args:
+        i = args.index("--cmd")
+        cmd = args[i + 1]
+        del args[i:i + 2]
+    tag, lcsv, reps = args[0], args[1], args[2:]
     os.makedirs("profiles", exist_ok=True)
     agg = launches(lcsv)
     tot = sum(a[1] for a in agg.values()) or 1.0
     with open(f"profiles/{tag}_launches.md", "w") as f:
         f.write(f"# {tag}: kernel launch list (ncu --metrics gpu__time_duration.sum --clock-control none)\n\n")
-        f.write("Command: `python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-ttg` (C2), "
+        f.write(f"Command: `{cmd}, "
                 "all launches of the process (setup included). Serialised, cold-cache times: shares, not absolutes.\n\n")
         f.write("| kernel | launches | total ms | mean us | share |\n|---|---:|---:|---:|---:|\n")
         for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -113,7 +123,7 @@ def main():
             f.write("\n")
             if "dram__bytes_read.sum" in res and "dram__bytes_write.sum" in res:
                 traffic[k] = to_bytes(res["dram__bytes_read.sum"]) + to_bytes(res["dram__bytes_write.sum"])
-    json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
+    json.dump(traffic, open(f"profiles/{traffic_name}.json", "w"), indent=1)
     print(open(f"profiles/{tag}_launches.md").read())
     print(open(f"profiles/{tag}_full.md").read())
 
