@@ -132,6 +132,132 @@ __device__ __forceinline__ void sweep_backward_body(const dm::SweepDev &s, const
     }
 }
 
+// Two-node groups (the long chains of split rows, the sweep's critical
+// path on a pruned instance): the per-position metadata is staged per warp
+// in shared memory, a window of kSweepMetaWin positions at a time, and the
+// arc targets and duals are loaded kRingDepth positions ahead into a
+// register ring (the loop unrolled by the ring depth, so every slot index is
+// a constant) — a position then waits on neither a dependent metadata load
+// nor a load issued one short step earlier.  Same arithmetic as the body
+// above, bit for bit.
+#ifndef DM_SWEEP_RING
+#define DM_SWEEP_RING 1
+#endif
+constexpr bool kSweepRing = DM_SWEEP_RING != 0;
+constexpr int kSweepMetaWin = 64;
+constexpr int kRingDepth = 4;
+constexpr int kSweepWarps = kSweepThreads / 32;
+
+template <int W>
+struct RingSlot {
+    int32_t w;
+    int64_t slot;
+    int32_t z[W], o[W];
+    double lam, d;
+};
+
+template <int W, bool kTrial, bool kStore>
+__device__ __forceinline__ void sweep_backward_ring(const dm::SweepDev &s, const double *__restrict__ lam,
+                                                    const double *__restrict__ d, double gamma,
+                                                    double *__restrict__ B, double *__restrict__ bounds,
+                                                    const double *__restrict__ ctl,
+                                                    const int32_t *__restrict__ bdd_inst, int64_t g, int32_t *mw,
+                                                    int64_t *ms) {
+    const int lane = threadIdx.x & 31;
+    const int32_t j = s.grp_bdd[g * 32 + lane];
+    if (kTrial && bdd_inst && j >= 0) gamma = ctl[8 * bdd_inst[j]];
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = s.bdd_layer_lo[j];
+        nj = s.bdd_layer_lo[j + 1] - l0;
+    }
+    const int32_t K = s.grp_npos[g];
+    const int64_t p0 = s.grp_pos_lo[g];
+    int32_t mlo = 0;  // first position in the metadata window
+    auto window = [&](int32_t lo) {
+        __syncwarp();
+        for (int i = lane; i < kSweepMetaWin; i += 32)
+            if (lo + i < K) {
+                mw[i] = s.pos_width[p0 + lo + i];
+                ms[i] = s.pos_slot[p0 + lo + i];
+            }
+        __syncwarp();
+        mlo = lo;
+    };
+    window(0);
+    auto fetch = [&](RingSlot<W> &r, int32_t k) {
+        if (k >= mlo + kSweepMetaWin) window(k);  // uniform: k is the warp's
+        r.w = mw[k - mlo];
+        r.slot = ms[k - mlo];
+#pragma unroll
+        for (int i = 0; i < W; ++i)
+            if (i < r.w) {
+                r.z[i] = s.zl[(r.slot + i) * 32 + lane];
+                r.o[i] = s.ol[(r.slot + i) * 32 + lane];
+            }
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            r.lam = lam[l];
+            if (kTrial) r.d = d[l];
+        }
+    };
+    double nb[W], cur[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) nb[u] = cur[u] = DM_INF;
+    RingSlot<W> ring[kRingDepth];
+#pragma unroll
+    for (int r = 0; r < kRingDepth; ++r)
+        if (r < K) fetch(ring[r], r);
+    for (int32_t k0 = 0; k0 < K; k0 += kRingDepth) {
+#pragma unroll
+        for (int r = 0; r < kRingDepth; ++r) {
+            const int32_t k = k0 + r;
+            if (k < K) {
+                const RingSlot<W> c = ring[r];
+                if (k + kRingDepth < K) fetch(ring[r], k + kRingDepth);
+                const bool act = k < nj;
+                const int32_t l = l0 + nj - 1 - k;
+                double lam_l = act ? c.lam : 0.0;
+                if (kTrial && act) lam_l = __dadd_rn(lam_l, __dmul_rn(gamma, c.d));
+                auto nbget = [&](int32_t a) {
+                    double x = nb[0];
+#pragma unroll
+                    for (int u = 1; u < W; ++u) x = (a == u) ? nb[u] : x;
+                    return x;
+                };
+                double vv[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    vv[i] = 0.0;
+                    if (i < c.w) {
+                        const int32_t a = c.z[i], b = c.o[i];
+                        const double c0 = a == dm::kTrue ? 0.0 : (a == dm::kFalse ? DM_INF : nbget(a));
+                        const double c1 =
+                            b == dm::kTrue ? lam_l : (b == dm::kFalse ? DM_INF : __dadd_rn(lam_l, nbget(b)));
+                        const double v = (c0 <= c1) ? c0 : c1;
+                        cur[i] = v;
+                        vv[i] = v;
+                    }
+                }
+                if (kStore && act) {
+                    const int32_t vbase = s.lnl[l];
+                    const int32_t wl = s.lnl[l + 1] - vbase;
+#pragma unroll
+                    for (int i = 0; i < W; ++i)
+                        if (i < wl) B[vbase + i] = vv[i];
+                }
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    const double t = nb[u];
+                    nb[u] = cur[u];
+                    cur[u] = t;
+                }
+                if (act && k == nj - 1) bounds[j] = nb[0];  // root layer: single node
+            }
+        }
+    }
+}
+
 // the group's widest layer picks the narrowest unrolled body (bit-identical)
 template <int W, bool kTrial, bool kStore>
 __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::SweepDev s, const double *__restrict__ lam,
@@ -148,7 +274,13 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
     const int gw = s.grp_width ? s.grp_width[g] : W;
-    if (W > 2 && gw <= 2)
+    __shared__ int32_t meta_w[kSweepWarps][kSweepMetaWin];
+    __shared__ int64_t meta_s[kSweepWarps][kSweepMetaWin];
+    const int wid = threadIdx.x >> 5;
+    if (W > 2 && gw <= 2 && kSweepRing)
+        sweep_backward_ring<2, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, meta_w[wid],
+                                               meta_s[wid]);
+    else if (W > 2 && gw <= 2)
         sweep_backward_body<2, W, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, sm);
     else if (W > 4 && gw <= 4)
         sweep_backward_body<4, W, kTrial, kStore>(s, lam, d, gamma, B, bounds, ctl, bdd_inst, g, sm);
