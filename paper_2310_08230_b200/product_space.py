@@ -25,8 +25,10 @@ dependency DAG the B200 exact-MMA kernel schedules by levels.  Product
 triangles are numbered by a "row colour": every A^M and A^N row receives
 each colour at most once (a Latin-square colouring of the face pairs plus
 one colour per degenerate element), so both projection-row chains advance
-one level per colour and the DAG depth stays close to its lower bound, the
-longest projection row.  ``order="natural"`` keeps the enumeration order.
+one level per colour; a greedy colouring of every row's variables, taken in
+that order, then fixes the numbering (boundary rows and pruning leave the
+Latin colours sparse), and the DAG depth stays close to its lower bound,
+the longest row.  ``order="natural"`` keeps the enumeration order.
 """
 
 from __future__ import annotations
@@ -310,18 +312,18 @@ def build_product_space(M: Mesh, N: Mesh, feat_m: np.ndarray, feat_n: np.ndarray
     whose three vertex pairs are all allowed (k-NN / coarse-to-fine pruning,
     SPEC.md:489-500).
 
-    ``order``: "colour" (the Latin-square row colours, within 2 % of the
-    depth bound on a full product space), "greedy" (the colour order refined
-    by a greedy row colouring, dm_row_colouring: on a pruned space most
-    Latin colours are sparse and the rows chain through many of them — C4's
-    DAG depth 1,665 -> 370, C3's 752 -> 199, the longest row 366 / 197),
-    "natural" (enumeration order); "auto" = "greedy" for a pruned space,
-    "colour" otherwise.  ``colouring`` (ProductSpace -> colours) replaces
+    ``order``: "greedy" (default, "auto"): the Latin-square colour order
+    refined by a greedy row colouring (dm_row_colouring), numbering by the
+    refined colour — the exact passes' DAG depth is then bounded by the
+    number of colours: C4 1,665 -> 370 levels, C3 752 -> 199 (on a pruned
+    space most Latin colours are sparse and the rows chain through many of
+    them), C2 4,119 -> 4,064, C1 1,158 -> 1,016; "colour" (the Latin-square
+    colours alone), "natural" (enumeration order).  ``colouring`` (ProductSpace -> colours) replaces
     the native ``row_colouring`` (bench.py's CPU arm passes the oracle's C
     copy, so it builds the same instance without the product library).
     """
     if order == "auto":
-        order = "greedy" if allowed is not None else "colour"
+        order = "greedy"
     if feat_m.shape[1] != feat_n.shape[1]:
         raise ValueError("feature dimension mismatch")
     FM, FN = M.faces, N.faces

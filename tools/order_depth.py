@@ -55,18 +55,6 @@ def instance(p, perm=None):
     return IlpInstance.from_csr(p.costs[perm], p.row_ptr, inv[p.row_var], p.row_coef, p.row_rhs, 128)
 
 
-config = sys.argv[1] if len(sys.argv) > 1 else "c4"
-seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-p = ps.synthetic_product_space(config, seed)
-lens = np.diff(p.row_ptr)
-print(f"{config}: {p.num_variables} vars, {p.num_rows} rows, longest row {lens.max()}, "
-      f"rows > 128: {(lens > 128).sum()}", flush=True)
-t = time.perf_counter()
-inst = instance(p)
-print(f"colour order: depth {depth_of(inst.flat)}, max layers {inst.flat.max_layers} ({time.perf_counter() - t:.1f}s)",
-      flush=True)
-
-
 def greedy_colours(p, visit):
     """Smallest colour not used by an already coloured variable of any of the
     variable's rows, variables taken in `visit` order."""
@@ -90,11 +78,23 @@ def greedy_colours(p, visit):
     return colour
 
 
-for name, visit in (("greedy/colour order", np.arange(p.num_variables)),
-                    ("greedy/reverse", np.arange(p.num_variables)[::-1]),
-                    ("greedy/random", np.random.default_rng(0).permutation(p.num_variables))):
+
+if __name__ == "__main__":
+    config = sys.argv[1] if len(sys.argv) > 1 else "c4"
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    p = ps.synthetic_product_space(config, seed)
+    lens = np.diff(p.row_ptr)
+    print(f"{config}: {p.num_variables} vars, {p.num_rows} rows, longest row {lens.max()}, "
+          f"rows > 128: {(lens > 128).sum()}", flush=True)
     t = time.perf_counter()
-    col = greedy_colours(p, visit)
-    perm = np.lexsort((np.arange(p.num_variables), col))
-    inst2 = instance(p, perm)
-    print(f"{name}: {col.max() + 1} colours, depth {depth_of(inst2.flat)} ({time.perf_counter() - t:.1f}s)", flush=True)
+    inst = instance(p)
+    print(f"colour order: depth {depth_of(inst.flat)}, max layers {inst.flat.max_layers} ({time.perf_counter() - t:.1f}s)",
+          flush=True)
+    for name, visit in (("greedy/colour order", np.arange(p.num_variables)),
+                        ("greedy/reverse", np.arange(p.num_variables)[::-1]),
+                        ("greedy/random", np.random.default_rng(0).permutation(p.num_variables))):
+        t = time.perf_counter()
+        col = greedy_colours(p, visit)
+        perm = np.lexsort((np.arange(p.num_variables), col))
+        inst2 = instance(p, perm)
+        print(f"{name}: {col.max() + 1} colours, depth {depth_of(inst2.flat)} ({time.perf_counter() - t:.1f}s)", flush=True)
