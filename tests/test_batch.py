@@ -107,8 +107,8 @@ def test_gpu_merged_hybrid_converges_to_every_instance_bound(schedule):
 def test_gpu_batched_hybrid_equals_separate_solves(schedule, compact):
     """BatchedSolver: every instance's own hybrid solve on one merged instance —
     records, stopping and duals bit for bit against qn.solve of each; with
-    compaction the live instances are re-merged as others stop (separate
-    solves: 5, 26, 4, 56 and 36 exact iterations; 41, 100, 41, 89, 98 deferred)."""
+    compaction the live instances are re-merged as others stop (the five
+    separate solves stop at different iterations, so the batch shrinks)."""
     from bench import build_instance
     from paper_2310_08230_b200 import qn
     from paper_2310_08230_b200.batch import BatchedSolver
