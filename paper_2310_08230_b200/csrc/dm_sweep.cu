@@ -983,7 +983,11 @@ int lbfgs_two_loop(const double *g, const double *const *s, const double *const 
         void *args[] = {(void *)&a};
         const cudaError_t e = cudaLaunchCooperativeKernel((const void *)two_loop_kernel, dim3(grid),
                                                           dim3(kChunkThreads), args, 0, st);
-        return e == cudaSuccess ? DM_OK : fail(e, "two_loop (cooperative)");
+        if (e == cudaSuccess) return DM_OK;
+        // the grid no longer fits (another context holds part of the device):
+        // the per-step launches below compute the same bits
+        if (e != cudaErrorCooperativeLaunchTooLarge) return fail(e, "two_loop (cooperative)");
+        (void)cudaGetLastError();
     }
     // slots: [0, m) first-loop dots, [m, 2m) alphas, 2m = y0.y0, [2m+1, 3m+1) second-loop dots
     double *dot1 = slots, *alpha = slots + m, *yy = slots + 2 * m, *dot2 = slots + 2 * m + 1;
