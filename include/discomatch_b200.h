@@ -186,6 +186,13 @@ int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, do
 int dm_step_search(const dm_flat *f, const double *lam, const double *d, double gamma_prev,
                    double free_contribution, double shrink, double grow, double min_ascent,
                    int max_trials, double *bounds, double *state, void *stream);
+/* qn.py:203-206 + dual.py:164-165 without a host round trip: after
+ * dm_step_search, if state[2] (e_best) > base (the current objective)
+ * lam += state[3] * d (dm_axpy_host's roundings) and B / bounds are rebuilt
+ * (dm_k_backward); otherwise nothing changes.  out[3] = {gamma_best, used
+ * (1.0 / 0.0), trials} for the caller's next read-back. */
+int dm_qn_move(const dm_flat *f, double *lam, const double *d, double base, const double *state, double *out,
+               double *B, double *bounds, void *stream);
 /* kernels.py:123-159 */
 int dm_k_forward(const dm_flat *f, const double *lam, double *F, double *bounds, void *stream);
 /* kernels.py:162-270: exact (bitwise) Gauss-Seidel forward averaging pass */

@@ -65,6 +65,7 @@ SIGNATURES = {
     "dm_flat_task_levels": ([_P, _INT, _P, _P], _INT),
     "dm_flat_destroy": ([_P], None),
     "dm_k_backward": ([_P, _P, _P, _P, _P], _INT),
+    "dm_qn_move": ([_P, _P, _P, _D, _P, _P, _P, _P, _P], _INT),
     "dm_k_backward_trial": ([_P, _P, _P, _D, _P, _P, _P], _INT),
     "dm_debug_div_check": ([_INT, ctypes.c_uint64, ctypes.c_uint64, _P], _INT),
     "dm_flat_status_to": ([_P, _P, _P], _INT),
@@ -153,8 +154,8 @@ def check(rc: int, what: str = "") -> None:
 
 
 # kernels each entry point launches (for the bench's gpu_launches claim)
-LAUNCHES = {"dm_k_mma_forward": 3, "dm_k_mma_backward": 2, "dm_sum": 2, "dm_curvature_pair": 2}
-KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_k_forward", "dm_k_mma_forward",
+LAUNCHES = {"dm_k_mma_forward": 3, "dm_k_mma_backward": 2, "dm_sum": 2, "dm_curvature_pair": 2, "dm_qn_move": 2}
+KERNEL_ENTRIES = {"dm_k_backward", "dm_k_backward_trial", "dm_qn_move", "dm_k_forward", "dm_k_mma_forward",
                   "dm_k_mma_backward", "dm_k_min_marginals", "dm_k_argmin", "dm_init_duals",
                   "dm_project_direction", "dm_lambda_sums", "dm_agreement_scores", "dm_sum", "dm_dot",
                   "dm_axpy_dev", "dm_scale_dev", "dm_lbfgs_up", "dm_axpy_host", "dm_sub",

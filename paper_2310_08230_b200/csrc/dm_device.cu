@@ -364,6 +364,23 @@ __global__ void lbfgs_up_kernel(double *__restrict__ x, const double *__restrict
         x[i] = __dadd_rn(x[i], __dmul_rn(s[i], c));
 }
 
+// qn.py:203-206 on the device: the step search's verdict (e_best > base)
+// decides, and lam += gamma_best * d with axpy_host's two roundings; out =
+// {gamma_best, used, trials} for the host's end-of-iteration read-back
+__global__ void qn_move_kernel(double *__restrict__ x, const double *__restrict__ y, double base,
+                               const double *__restrict__ state, double *__restrict__ out, int64_t n) {
+    const bool used = state[2] > base;
+    const double g = state[3];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        out[0] = g;
+        out[1] = used ? 1.0 : 0.0;
+        out[2] = state[6];
+    }
+    if (!used) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], __dmul_rn(g, y[i]));
+}
+
 __global__ void axpy_host_kernel(double *__restrict__ x, double g, const double *__restrict__ y, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         x[i] = __dadd_rn(x[i], __dmul_rn(g, y[i]));
@@ -2234,6 +2251,22 @@ int dm_k_backward(const dm_flat *f, const double *lam, double *B, double *bounds
     }
     if (f->dec_B == B) const_cast<dm_flat *>(f)->dec_B = nullptr;  // recorded decisions no longer match B
     return dm::sweep_backward(f->sweep, lam, nullptr, 0.0, B, bounds, stream);
+}
+
+int dm_qn_move(const dm_flat *f, double *lam, const double *d, double base, const double *state, double *out,
+               double *B, double *bounds, void *stream) {
+    DM_CHECK_FLAT(f);
+    if (!lam || !d || !state || !out || !B || !bounds) {
+        dm::set_error("dm_qn_move: invalid arguments");
+        return DM_ERR_INVALID;
+    }
+    const cudaStream_t s = (cudaStream_t)stream;
+    qn_move_kernel<<<grid_stride_blocks(f->L), 256, 0, s>>>(lam, d, base, state, out, f->L);
+    if (int rc = check_stream_error("qn_move")) return rc;
+    if (f->nb == 0) return DM_OK;
+    if (f->dec_B == B) const_cast<dm_flat *>(f)->dec_B = nullptr;
+    // the averaging pass's refresh of B (dual.py:164-165), skipped on the device when nothing moved
+    return dm::sweep_backward(f->sweep, lam, nullptr, 0.0, B, bounds, stream, out + 1);
 }
 
 int dm_k_backward_trial(const dm_flat *f, const double *lam, const double *d, double gamma, double *B,

@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_backward_kernel(dm::Sweep
         if (ctl[5] != 0.0) return;  // the search already stopped
         gamma = ctl[0];
     }
+    if (!kTrial && ctl && *ctl == 0.0) return;  // gated refresh (dm_qn_move's verdict): nothing moved
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (g >= s.groups) return;
     const int gw = s.grp_width ? s.grp_width[g] : W;

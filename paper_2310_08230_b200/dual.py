@@ -102,6 +102,7 @@ class DualState:
         self._pending: list[int] = []  # bound slots not yet read, in order
         self._status_pending = False
         self._step_state = None
+        self._move_pending = False
         self.f_valid = False
         self.b_valid = False
         self._bound = -np.inf
@@ -366,6 +367,41 @@ class DualState:
         if self.pass_timer:
             self.pass_timer.count("step_search_trials", trials)
         return float(st[3]), float(st[2]), trials
+
+    def search_and_move(self, d: torch.Tensor, gamma_prev: float, shrink: float, grow: float, min_ascent: float,
+                        max_trials: int) -> None:
+        """find_step_size, the move it decides and the refresh of B (qn.py:203-206,
+        dual.py:164-165), all queued on the device (exact schedule, B valid):
+        dm_step_search, then dm_qn_move — lam += gamma_best * d and B rebuilt
+        iff the best trial beat the current objective.  No read-back: the
+        verdict {gamma_best, used, trials} lands in _slots[10:13] for the
+        next ``read_scalars`` (``take_move``)."""
+        if self.deferred or not self.b_valid:
+            raise ValueError("search_and_move needs the exact schedule and a valid B")
+        base = self.bound  # known on the host: the last read-back left nothing queued
+        if self._step_state is None:
+            self._step_state = torch.zeros(8, dtype=_F64, device=self.device)
+        ev = self.pass_timer.begin("step_search") if self.pass_timer else None
+        self.dev.step_search(self.lam_d, d, gamma_prev, self.free_contribution, shrink, grow, min_ascent,
+                             max_trials, self._scratch_bounds, self._step_state)
+        if ev:
+            self.pass_timer.end(ev)
+        self.dev.qn_move(self.lam_d, d, base, self._step_state, self._slots[10:13], self.B, self._bounds)
+        self._bgen += 1  # B rebuilt, or unchanged for unchanged duals
+        self.f_valid = False
+        self.b_valid = True
+        self._set_bound()
+        self._move_pending = True
+
+    def take_move(self, vals: np.ndarray) -> tuple[float, bool]:
+        """(gamma_best, used) of the last ``search_and_move`` from a read-back."""
+        self._move_pending = False
+        used = bool(vals[11] != 0.0)
+        trials = int(vals[12])
+        self.sweeps += trials + (1 if used else 0)
+        if self.pass_timer:
+            self.pass_timer.count("step_search_trials", trials)
+        return float(vals[10]), used
 
     # -- dual vectors per constraint ------------------------------------------
     def lambda_of(self, constraint: int) -> np.ndarray:

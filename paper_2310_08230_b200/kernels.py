@@ -89,6 +89,11 @@ class DeviceFlat:
     def k_backward(self, lam, B, bounds):
         _native.call("dm_k_backward", self._h, _ptr(lam), _ptr(B), _ptr(bounds), self._s())
 
+    def qn_move(self, lam, d, base, state, out, B, bounds):
+        """Device-side quasi-Newton move + gated refresh of B (dm_qn_move)."""
+        _native.call("dm_qn_move", self._h, _ptr(lam), _ptr(d), float(base), _ptr(state), _ptr(out), _ptr(B),
+                     _ptr(bounds), self._s())
+
     def k_backward_trial(self, lam, d, gamma, B, bounds):
         _native.call("dm_k_backward_trial", self._h, _ptr(lam), _ptr(d), float(gamma), _ptr(B), _ptr(bounds),
                      self._s())
