@@ -32,6 +32,9 @@ for step in "$@"; do
     hints) for c in c2 c4; do python tools/ab_hints.py $c > gpurun_out/ab_hints_$c.json 2>>gpurun_out/ab_hints.err; done ;;
     c5_phases) timeout 900 python tools/c5_phases.py > gpurun_out/c5_phases.jsonl 2> gpurun_out/c5_phases.err ;;
     probe) for c in c3 c4 c2; do timeout 600 python tools/dfr_probe.py $c 0.4 0.5 > gpurun_out/probe_$c.json 2> gpurun_out/probe_$c.err; done ;;
+    profile) bash tools/profile_round.sh ;;  # the final-round ncu captures (profiles/r02_final_*)
+    c5_batched) timeout 900 python tools/c5_batched.py 64 exact > gpurun_out/c5_batched.log 2>&1 ;;
+    steps) for c in c4 c2; do timeout 600 python tools/c4_step.py $c exact 20 > gpurun_out/step_$c.log 2>&1; done ;;
     *) echo "unknown step $step" ;;
   esac
 done
