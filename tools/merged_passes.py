@@ -1,3 +1,5 @@
+"""Exact passes, refresh and one trial sweep on the C5 batch merged into one
+instance (GPU tool): the throughput regime of the exact passes (wide, shallow DAG)."""
 import sys, json, time
 sys.path.insert(0, "."); sys.path.insert(0, "tools")
 import torch

@@ -1,3 +1,5 @@
+"""Averaging-only (mode mma-only) time to the 1e-3 gap at C4 for both schedules
+(GPU tool): how far plain averaging gets without the quasi-Newton step."""
 import sys, time, json
 sys.path.insert(0, ".")
 from bench import build_instance

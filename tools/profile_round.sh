@@ -1,3 +1,6 @@
+# The round's ncu evidence (GPU tool; summarise with tools/ncu_summary.py / ncu_multi.py into
+# profiles/r02_final_*): C2 launch lists of the exact and deferred bench step, --set full of the
+# exact passes and the argmin walk, the deferred kernels of one round at C2 and C4.
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 1 --no-extras --no-ttg --no-e2e --no-cpu-baseline"
 timeout 600 $B > gpurun_out/plain.log 2>&1
