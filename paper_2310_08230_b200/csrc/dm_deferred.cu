@@ -732,6 +732,241 @@ __global__ void __launch_bounds__(kNpThreads) dfr_np_forward_kernel(NpArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Node-parallel passes with a 2-deep register ring (diagrams of at most
+// kNpRingLayers layers): each 8-lane group stages its diagram's layer-node
+// offsets in shared memory once, so a position's row addresses need no
+// dependent global load, and the rows (arc targets, opposite-table values,
+// dual, average, publish descriptor) are loaded two positions ahead — the
+// loop unrolled by two so both ring slots are registers.  The per-position
+// arithmetic is the one-ahead kernels' above, operand for operand.
+constexpr int kNpRingLayers = 256;
+constexpr int kNpGroups = kNpThreads / 8;
+
+struct NpFwRow {
+    int32_t z, o, b, e, e2;
+    double bn, lam, avg;
+    uint64_t desc;
+};
+
+template <bool kMM, bool kAvg>
+__global__ void __launch_bounds__(kNpThreads) dfr_np_forward_ring_kernel(NpArgs a) {
+    __shared__ int32_t lnl_s[kNpGroups][kNpRingLayers + 1];
+    const int lane = threadIdx.x & 31, q = lane & 7, gb = lane & ~7;
+    const int64_t e = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4 + (lane >> 3);
+    const int32_t j = e < a.entries ? a.order[e] : -1;
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = a.bdd_layer_lo[j];
+        nj = a.bdd_layer_lo[j + 1] - l0;
+    }
+    int32_t K = nj;
+    K = max(K, __shfl_xor_sync(kFullMask, K, 8));
+    K = max(K, __shfl_xor_sync(kFullMask, K, 16));
+    if (K == 0) return;
+    int32_t *ln = lnl_s[threadIdx.x >> 3];
+    for (int i = q; i <= nj; i += 8) ln[i] = a.lnl[l0 + i];
+    __syncwarp();
+    auto load = [&](NpFwRow &r, int32_t p) {
+        r.z = r.o = dm::kFalse;
+        r.bn = DM_INF;
+        r.b = r.e = r.e2 = 0;
+        r.lam = r.avg = 0.0;
+        r.desc = ~0ull;
+        if (p < nj) {
+            const int32_t l = l0 + p;
+            r.b = ln[p];
+            r.e = ln[p + 1];
+            r.e2 = p + 1 < nj ? ln[p + 2] : r.e;
+            if (q < r.e - r.b) {
+                r.z = a.zero_t[r.b + q];
+                r.o = a.one_t[r.b + q];
+            }
+            if (kMM && q < r.e2 - r.e) r.bn = a.in[r.e + q];
+            r.lam = a.lam[l];
+            if (kAvg) r.avg = a.avg[l];
+            r.desc = a.relax[l];
+        }
+    };
+    double fq = q == 0 ? 0.0 : DM_INF;  // F of node q of the current layer (root: F[root] = 0)
+    double tb = DM_INF;
+    auto body = [&](int32_t p, const NpFwRow &c) {
+        const bool act = p < nj;
+        const int32_t l = l0 + p;
+        const int32_t base = c.b, w = c.e - c.b, nbase = c.e, wn = c.e2 - c.e;
+        const int32_t z = c.z, o = c.o;
+        const double bnq = c.bn;
+        double lam_l = c.lam;
+        const double a_l = c.avg;
+        const uint64_t desc = c.desc;
+        const bool valid = act && q < w;
+        if (valid) a.out[base + q] = fq;
+        if (kMM) {
+            const double bz = __shfl_sync(kFullMask, bnq, gb + (z >= 0 ? z - nbase : 0));
+            const double bo = __shfl_sync(kFullMask, bnq, gb + (o >= 0 ? o - nbase : 0));
+            double c0 = DM_INF, c1 = DM_INF;
+            if (valid) {
+                c0 = z == dm::kTrue ? fq : (z == dm::kFalse ? DM_INF : __dadd_rn(fq, bz));
+                const double fl = __dadd_rn(fq, lam_l);
+                c1 = o == dm::kTrue ? fl : (o == dm::kFalse ? DM_INF : __dadd_rn(fl, bo));
+            }
+            const double m0 = lmin8(c0, q), m1 = lmin8(c1, q);
+            if (act) {
+                double mb;
+                lam_l = dfr_update_v<kAvg>(lam_l, a_l, m0, m1, a.omega, mb);
+                if (q == 0) {
+                    a.mbar[l] = mb;
+                    a.lam[l] = lam_l;
+                }
+            }
+        } else if (kAvg && act) {
+            lam_l = __dadd_rn(lam_l, a_l);
+            if (q == 0) a.lam[l] = lam_l;
+        }
+        double t_loc = DM_INF;
+        if (valid && fq != DM_INF) {
+            if (z == dm::kTrue) t_loc = fq;
+            const double cc = __dadd_rn(fq, lam_l);
+            if (o == dm::kTrue && cc < t_loc) t_loc = cc;
+        }
+        t_loc = lmin8(t_loc, q);
+        if (act && t_loc < tb) tb = t_loc;
+        const int zs = (int)((desc >> (8 * q)) & 15), os = (int)((desc >> (8 * q + 4)) & 15);
+        const double fz = __shfl_sync(kFullMask, fq, gb + (zs < 8 ? zs : 0));
+        const double fo = __shfl_sync(kFullMask, fq, gb + (os < 8 ? os : 0));
+        double fnew = DM_INF;
+        if (act && q < wn) {
+            const double cz = zs < 8 ? fz : DM_INF;
+            const double co = os < 8 ? __dadd_rn(fo, lam_l) : DM_INF;
+            const double first = (os < zs) ? co : cz, second = (os < zs) ? cz : co;
+            if (first < fnew) fnew = first;
+            if (second < fnew) fnew = second;
+        }
+        fq = fnew;
+    };
+    NpFwRow r0, r1;
+    load(r0, 0);
+    load(r1, 1);
+    for (int32_t p0 = 0; p0 < K; p0 += 2) {
+        {
+            const NpFwRow c = r0;
+            if (p0 + 2 < K) load(r0, p0 + 2);
+            body(p0, c);
+        }
+        if (p0 + 1 < K) {
+            const NpFwRow c = r1;
+            if (p0 + 3 < K) load(r1, p0 + 3);
+            body(p0 + 1, c);
+        }
+    }
+    if (j >= 0 && q == 0) a.bounds[j] = tb;
+}
+
+struct NpBwRow {
+    int32_t z, o, b, e;
+    double f, lam, avg;
+};
+
+template <bool kMM, bool kAvg, bool kDec>
+__global__ void __launch_bounds__(kNpThreads) dfr_np_backward_ring_kernel(NpArgs a) {
+    __shared__ int32_t lnl_s[kNpGroups][kNpRingLayers + 1];
+    const int lane = threadIdx.x & 31, q = lane & 7, gb = lane & ~7;
+    const int64_t e = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4 + (lane >> 3);
+    const int32_t j = e < a.entries ? a.order[e] : -1;
+    int32_t l0 = 0, nj = 0;
+    if (j >= 0) {
+        l0 = a.bdd_layer_lo[j];
+        nj = a.bdd_layer_lo[j + 1] - l0;
+    }
+    int32_t K = nj;
+    K = max(K, __shfl_xor_sync(kFullMask, K, 8));
+    K = max(K, __shfl_xor_sync(kFullMask, K, 16));
+    if (K == 0) return;
+    int32_t *ln = lnl_s[threadIdx.x >> 3];
+    for (int i = q; i <= nj; i += 8) ln[i] = a.lnl[l0 + i];
+    __syncwarp();
+    auto load = [&](NpBwRow &r, int32_t k) {  // position k = layer l0 + nj - 1 - k
+        r.z = r.o = dm::kFalse;
+        r.f = 0.0;
+        r.b = r.e = 0;
+        r.lam = r.avg = 0.0;
+        if (k < nj) {
+            const int32_t l = l0 + nj - 1 - k;
+            r.b = ln[nj - 1 - k];
+            r.e = ln[nj - k];
+            if (q < r.e - r.b) {
+                r.z = a.zero_t[r.b + q];
+                r.o = a.one_t[r.b + q];
+                if (kMM) r.f = a.in[r.b + q];
+            }
+            r.lam = a.lam[l];
+            if (kAvg) r.avg = a.avg[l];
+        }
+    };
+    double bnext = DM_INF;  // B of node q of the next layer (position k-1)
+    int32_t nbase = 0;
+    auto body = [&](int32_t k, const NpBwRow &c) {
+        const bool act = k < nj;
+        const int32_t l = l0 + nj - 1 - k;
+        const int32_t base = c.b, w = c.e - c.b;
+        const int32_t z = c.z, o = c.o;
+        const double fv = c.f;
+        double lam_l = c.lam;
+        const double a_l = c.avg;
+        const bool valid = act && q < w;
+        const double bz = __shfl_sync(kFullMask, bnext, gb + (z >= 0 ? z - nbase : 0));
+        const double bo = __shfl_sync(kFullMask, bnext, gb + (o >= 0 ? o - nbase : 0));
+        if (kMM) {
+            double c0 = DM_INF, c1 = DM_INF;
+            if (valid) {
+                c0 = z == dm::kTrue ? fv : (z == dm::kFalse ? DM_INF : __dadd_rn(fv, bz));
+                const double fl = __dadd_rn(fv, lam_l);
+                c1 = o == dm::kTrue ? fl : (o == dm::kFalse ? DM_INF : __dadd_rn(fl, bo));
+            }
+            const double m0 = lmin8(c0, q), m1 = lmin8(c1, q);
+            if (act) {
+                double mb;
+                lam_l = dfr_update_v<kAvg>(lam_l, a_l, m0, m1, a.omega, mb);
+                if (q == 0) a.mbar[l] = mb;
+            }
+        } else if (kAvg && act) {
+            lam_l = __dadd_rn(lam_l, a_l);
+        }
+        if ((kMM || kAvg) && act && q == 0) a.lam[l] = lam_l;
+        const double c0 = z == dm::kTrue ? 0.0 : (z == dm::kFalse ? DM_INF : bz);
+        const double c1 = o == dm::kTrue ? lam_l : (o == dm::kFalse ? DM_INF : __dadd_rn(lam_l, bo));
+        const bool zero_wins = c0 <= c1;
+        const double bq = zero_wins ? c0 : c1;
+        if (valid) a.out[base + q] = bq;
+        if (kDec) {
+            const int32_t t = zero_wins ? z : o;
+            uint64_t word = valid ? (uint64_t)((((t >= 0) ? t - nbase : 0) << 1) | (zero_wins ? 0 : 1)) << (8 * q) : 0ull;
+            word |= __shfl_xor_sync(kFullMask, word, 1);
+            word |= __shfl_xor_sync(kFullMask, word, 2);
+            word |= __shfl_xor_sync(kFullMask, word, 4);
+            if (act && q == 0) a.dec[l] = word;
+        }
+        bnext = valid ? bq : DM_INF;
+        nbase = base;
+        if (act && k == nj - 1 && q == 0) a.bounds[j] = bq;  // root layer: single node
+    };
+    NpBwRow r0, r1;
+    load(r0, 0);
+    load(r1, 1);
+    for (int32_t k0 = 0; k0 < K; k0 += 2) {
+        {
+            const NpBwRow c = r0;
+            if (k0 + 2 < K) load(r0, k0 + 2);
+            body(k0, c);
+        }
+        if (k0 + 1 < K) {
+            const NpBwRow c = r1;
+            if (k0 + 3 < K) load(r1, k0 + 3);
+            body(k0 + 1, c);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined passes (W = 8, the product-space instances): every position's
 // inputs go through a per-warp ring of kStages shared-memory stages filled
 // by cp.async — the arc rows, the opposite table's rows (coalesced 16-byte
@@ -1129,6 +1364,14 @@ int launch(Kern kern, const DfrArgs &a, size_t smem, cudaStream_t st, const char
     return e == cudaSuccess ? DM_OK : fail(e, what);
 }
 
+bool np_ring() {
+    static const int v = [] {
+        const char *e = std::getenv("DM_DFR_NP_RING");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 bool use_pipe() {
     static const int v = [] {
         const char *e = std::getenv("DM_DFR_PIPE");
@@ -1253,6 +1496,23 @@ int dfr_np_pass(const SweepDev &s, const int32_t *zero_t, const int32_t *one_t, 
     const int blocks = (int)((warps * 32 + kNpThreads - 1) / kNpThreads);
     const cudaStream_t st = (cudaStream_t)stream;
     const bool mm = mbar != nullptr, av = avg != nullptr, dc = a.dec != nullptr;
+    if (s.max_layers > 0 && s.max_layers <= kNpRingLayers && np_ring()) {
+        if (forward) {
+            if (mm && av) dfr_np_forward_ring_kernel<true, true><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (mm) dfr_np_forward_ring_kernel<true, false><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (av) dfr_np_forward_ring_kernel<false, true><<<blocks, kNpThreads, 0, st>>>(a);
+            else dfr_np_forward_ring_kernel<false, false><<<blocks, kNpThreads, 0, st>>>(a);
+        } else {
+            if (mm && av) dfr_np_backward_ring_kernel<true, true, false><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (mm) dfr_np_backward_ring_kernel<true, false, false><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (av && dc) dfr_np_backward_ring_kernel<false, true, true><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (av) dfr_np_backward_ring_kernel<false, true, false><<<blocks, kNpThreads, 0, st>>>(a);
+            else if (dc) dfr_np_backward_ring_kernel<false, false, true><<<blocks, kNpThreads, 0, st>>>(a);
+            else dfr_np_backward_ring_kernel<false, false, false><<<blocks, kNpThreads, 0, st>>>(a);
+        }
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? DM_OK : fail(e, forward ? "dfr_np_forward" : "dfr_np_backward");
+    }
     if (forward) {
         if (mm && av) dfr_np_forward_kernel<true, true><<<blocks, kNpThreads, 0, st>>>(a);
         else if (mm) dfr_np_forward_kernel<true, false><<<blocks, kNpThreads, 0, st>>>(a);

@@ -132,7 +132,7 @@ bool build_relax_by_layer(const int64_t *bdd_layer_lo, int64_t nb, const int64_t
 // need to read duals and write distances (dm_sweep.cu).
 struct SweepDev {
     int64_t groups = 0, slots = 0;  // slots * 32 = elements of an interleaved table
-    int32_t max_width = 0;
+    int32_t max_width = 0, max_layers = 0;
     const int32_t *grp_bdd = nullptr, *grp_npos = nullptr, *pos_width = nullptr;
     const int32_t *grp_width = nullptr;  // widest layer of each group (null: max_width)
     const int64_t *grp_pos_lo = nullptr, *pos_slot = nullptr;

@@ -485,7 +485,9 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
         }
         if ((e = cub::DeviceScan::ExclusiveSum(tmp, tmp_scan2, pos_width, pos_slot, (int)npos_total, s))) break;
         sweep_total_kernel<<<1, 1, 0, s>>>(pos_width, pos_slot, npos_total, stats);
-        if ((e = cudaMemcpyAsync(host, stats, 16, cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
+        // the longest diagram's layers: the first group's (groups are longest first)
+        if ((e = cudaMemcpyAsync(stats + 2, grp_npos, sizeof(int32_t), cudaMemcpyDeviceToDevice, s))) break;
+        if ((e = cudaMemcpyAsync(host, stats, 24, cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s)))
             break;
         mark("slots");
         const int64_t slots = host[0];
@@ -495,6 +497,7 @@ int device_sweep_layout(const int32_t *bl, const int32_t *lnl, int64_t nb, Sweep
             break;
         }
         sd.max_width = (int32_t)host[1];
+        sd.max_layers = (int32_t)(host[2] & 0xffffffff);
         sd.slots = slots;
         if ((e = dalloc(&zl, slots * 32, s, allocs, bytes)) || (e = dalloc(&ol, slots * 32, s, allocs, bytes))) break;
         e = cudaGetLastError();
