@@ -149,3 +149,20 @@ def test_gpu_batched_single_instance_equals_its_solve():
     assert got.bounds == one.bounds
     assert got.iterations == one.iterations and got.stop_reason == one.stop_reason
     assert got.lam.tobytes() == one.state.lam.tobytes()
+
+
+@pytest.mark.gpu
+def test_gpu_batched_time_limit_stops_every_instance():
+    """max_seconds = 0: every instance stops after its first iteration with
+    the time-limit reason, as its separate solve does."""
+    from bench import build_instance
+    from paper_2310_08230_b200 import qn
+    from paper_2310_08230_b200.batch import solve_batched
+
+    insts = [build_instance("c3", s) for s in (2, 4)]
+    cfg = SolveConfig(mode="hybrid", max_iterations=30, max_seconds=0.0)
+    got = solve_batched(insts, cfg, device="cuda:0")
+    for g, inst in zip(got, insts):
+        one = qn.solve(inst, cfg, device="cuda:0")
+        assert g.stop_reason == one.stop_reason == "max_seconds"
+        assert g.bounds == one.bounds and g.iterations == one.iterations == 1
