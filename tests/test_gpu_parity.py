@@ -508,7 +508,7 @@ def test_exact_pass_division_matches_ddiv(k):
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("n", [4096 * 4096 + 4096, 20_000_003])
+@pytest.mark.parametrize("n", [4096 * 4096 + 4096, 20_000_003, 40_000_001])
 def test_two_loop_and_curvature_pair_beyond_4096_chunks(n):
     """The fused L-BFGS two-loop and the curvature pair on vectors longer than
     4096 chunks, bitwise against the oracle's two-loop in chunked-dot order."""
