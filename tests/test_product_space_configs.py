@@ -100,3 +100,21 @@ def test_reference_arm_builds_its_instance_without_the_product_library():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,latin_depth", [("c3", 752), ("c1", 1158)])
+def test_exact_pass_depth_follows_the_colour_count(config, latin_depth):
+    """The device level orders of the greedy-numbered spaces: the exact
+    passes' DAG depth stays within the split couplings of the colour count,
+    well under the Latin-square numbering's ("Numbering of a
+    product space")."""
+    from paper_2310_08230_b200.dual import init_duals
+    from paper_2310_08230_b200.ilp import IlpInstance
+
+    p = ps.synthetic_product_space(config, 0)
+    colours = int(ps.row_colouring(p).max()) + 1
+    inst = IlpInstance.from_csr(p.costs, p.row_ptr, p.row_var, p.row_coef, p.row_rhs, 128)
+    info = init_duals(inst, device="cuda:0").dev.info
+    assert info["fw_depth"] == info["bw_depth"]
+    assert colours <= info["fw_depth"] <= colours + 16 < latin_depth
