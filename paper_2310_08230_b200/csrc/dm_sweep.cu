@@ -145,7 +145,10 @@ __device__ __forceinline__ void sweep_backward_body(const dm::SweepDev &s, const
 #endif
 constexpr bool kSweepRing = DM_SWEEP_RING != 0;
 constexpr int kSweepMetaWin = 64;
-constexpr int kRingDepth = 4;
+#ifndef DM_RING_DEPTH
+#define DM_RING_DEPTH 4
+#endif
+constexpr int kRingDepth = DM_RING_DEPTH;
 constexpr int kSweepWarps = kSweepThreads / 32;
 
 template <int W>
